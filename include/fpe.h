@@ -1,0 +1,179 @@
+/*
+ * fpe.h -- C ABI of the B200 Fast Polynomial Evaluator (libfpe.so).
+ *
+ * The calls follow the problem statement of Algorithm FPE_p:
+ *   preconditioning  "Data: the list of coefficients a_0..a_d and the precision p"
+ *                    (scales, concave cover, good indices G_p)
+ *   evaluation       "Data: pre-conditioned P at precision p; finite subset Z of C*"
+ *                    -> Q_lambda(z) for every z in Z
+ * plus the full Horner scheme as the context baseline.
+ *
+ * Conventions
+ *  - All entry points are extern "C", return fpe_status unless noted, and never
+ *    throw.  On failure fpe_last_error_detail() (thread-local) says why.
+ *  - Pointers are plain host or device pointers; stream arguments are
+ *    cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Complex data are interleaved (re, im) pairs of the dtype's real type.
+ *  - Results are returned in extended range: value = mantissa * 2^exp with
+ *    max(|re|,|im|) of the mantissa in [1/2, 1) (or all zero with exp = 0),
+ *    because z^d overflows any hardware float.
+ *  - Results are a pure function of (handle, z): bitwise independent of the
+ *    batch, its order, and the sharding across GPUs.
+ */
+#ifndef FPE_H_
+#define FPE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FPE_OK = 0,
+    FPE_ERR_INVALID_ARG = 1,      /* bad pointer / size / dtype; nothing enqueued            */
+    FPE_ERR_ZERO_POLY = 2,        /* all coefficients are zero                               */
+    FPE_ERR_NONFINITE_COEFF = 3,  /* a NaN or inf coefficient                                 */
+    FPE_ERR_UNSUPPORTED = 4,      /* e.g. coefficient dynamic range beyond the fp64/fp32 path */
+    FPE_ERR_OOM = 5,              /* device or host allocation failed                         */
+    FPE_ERR_CUDA = 6              /* a CUDA runtime error (detail has the CUDA message)       */
+} fpe_status;
+
+typedef enum {
+    FPE_R64 = 0,  /* double            */
+    FPE_C64 = 1,  /* double re, im     */
+    FPE_R32 = 2,  /* float             */
+    FPE_C32 = 3   /* float re, im      */
+} fpe_dtype;
+
+/* Opaque, immutable preconditioned polynomial ("pre-conditioned P at precision p",
+ * PAPER.md:1245).  Owns its device buffer until fpe_destroy. */
+typedef struct fpe_poly_s* fpe_poly;
+
+typedef struct {
+    int64_t d;          /* n_coeffs - 1                                                  */
+    int64_t k_min;      /* first nonzero index                                           */
+    int64_t k_max;      /* last nonzero index; d_eff = k_max - k_min (R3)      */
+    int64_t n_hull;     /* vertices of the canonical concave cover    */
+    int64_t n_good;     /* |G_p| (eq:threshold)                      */
+    int32_t p;          /* precision in bits (53 for fp64, 24 for fp32 by default)        */
+    int32_t drop;       /* D = p + s(d_eff) + 3 unless overridden   */
+    int32_t shift;      /* stored coefficients are a_k * 2^-shift (exact)                 */
+    int32_t sparse;     /* 1: compact good-index list; 0: dense masked coefficient array  */
+    int32_t dtype;      /* fpe_dtype of the coefficients                                   */
+    int32_t reserved;
+    size_t bytes;       /* size of the flat device buffer                                  */
+} fpe_poly_info;
+
+/* Per-point diagnostics of the evaluation phase (lines 5-8 of Algorithm FPE_p). */
+typedef struct {
+    double  lambda;     /* correctly rounded fp64 log2|z| (eq:defLambda); -inf for z = 0  */
+    int32_t region;     /* index of the cover vertex k_lambda (smallest argmax); -1: non-finite z */
+    int32_t l;          /* band [l, r] (def:LRN)                       */
+    int32_t r;
+    int32_t kept;       /* K = #(G_p cap [l, r])                                           */
+    int32_t hard;       /* 1 if lambda was within 2^-96 |lambda| of an fp64 rounding boundary */
+    int32_t pad;
+} fpe_diag;
+
+/*
+ * fpe_precondition -- lines 2-4 of Algorithm FPE_p.
+ *   coeffs        a_0..a_d, n_coeffs = d+1 entries of dtype dt (host or device pointer;
+ *                 read during the call only, then copied).
+ *   p_bits        precision p; 0 selects 53 (R64/C64) or 24 (R32/C32).
+ *   drop_override 0: D = p + s(d_eff) + 3; > 0: D = drop_override (tests only).
+ *   device        CUDA device ordinal that will own the handle's buffer.
+ *   stream        stream for the host->device upload (the call synchronises it).
+ *   out           receives the handle.
+ * Errors: INVALID_ARG (NULL pointers, n_coeffs < 1, bad dtype), ZERO_POLY,
+ *         NONFINITE_COEFF, UNSUPPORTED (coefficient scales of the good terms span more
+ *         than the working format can hold after a common power-of-two shift), OOM, CUDA.
+ */
+fpe_status fpe_precondition(const void* coeffs, int64_t n_coeffs, fpe_dtype dt,
+                            int32_t p_bits, int32_t drop_override, int device,
+                            void* stream, fpe_poly* out);
+
+/*
+ * fpe_precondition_host -- the same preconditioning, entirely on the host (no CUDA call):
+ * writes the flat buffer that fpe_poly_device_buffer would hold into the host array buf.
+ * With buf == NULL or cap too small, only *bytes (the required size) is set and
+ * FPE_ERR_INVALID_ARG is returned.  Used to prepare / ship a handle without a GPU.
+ */
+fpe_status fpe_precondition_host(const void* coeffs_host, int64_t n_coeffs, fpe_dtype dt,
+                                 int32_t p_bits, int32_t drop_override, void* buf, size_t cap,
+                                 size_t* bytes);
+
+fpe_status fpe_poly_get_info(fpe_poly h, fpe_poly_info* out);
+
+/* Canonical cover vertices (hk[i], hh[i] = s(a_hk[i])) into host arrays of capacity cap;
+ * *n receives the vertex count (INVALID_ARG if cap is too small). */
+fpe_status fpe_poly_get_hull(fpe_poly h, int32_t* hk, int32_t* hh, int64_t cap, int64_t* n);
+
+/* The handle's flat device buffer (immutable; e.g. for ncclBroadcast to other ranks). */
+fpe_status fpe_poly_device_buffer(fpe_poly h, const void** dptr, size_t* bytes);
+
+/* Copy the flat buffer (h's fpe_poly_info.bytes bytes) to dst, a host or device pointer
+ * of capacity cap (synchronous on `stream`). */
+fpe_status fpe_poly_export(fpe_poly h, void* dst, size_t cap, void* stream);
+
+/* A new handle on `device` from a flat buffer produced by fpe_poly_device_buffer,
+ * fpe_poly_export or fpe_precondition_host (possibly received from another rank); ptr may
+ * be a host or a device pointer.  The buffer is validated (magic, version, size) and copied.
+ * INVALID_ARG if it is not an fpe buffer. */
+fpe_status fpe_poly_from_device_buffer(const void* ptr, size_t bytes, int device,
+                                       void* stream, fpe_poly* out);
+
+/* Bytes of device workspace fpe_evaluate / fpe_horner need for n_points points. */
+fpe_status fpe_eval_workspace_size(fpe_poly h, int64_t n_points, size_t* bytes);
+
+/*
+ * fpe_evaluate -- lines 5-9 of Algorithm FPE_p for every point.
+ *   points      n_points device values of dtype pt_dt.  pt_dt must have the coefficient
+ *               dtype's precision (64 or 32 bit); a real polynomial at real points uses
+ *               the real path, every other combination is evaluated in complex.
+ *   values_out  device, n_points values: complex (interleaved) unless both the polynomial
+ *               and the points are real; precision as pt_dt.
+ *   exps_out    device int64[n_points] binary exponents, or NULL: then values are returned
+ *               ldexp'd to plain floats (which may overflow to inf or underflow to 0).
+ *   diag_out    device fpe_diag[n_points] or NULL.
+ *   workspace   device scratch of at least fpe_eval_workspace_size bytes.
+ * Per-point cases: z = 0 gives a_0 (0 if a_0 = 0) with region 0, l = r = k_min;
+ *   a non-finite z gives NaN with region -1.  Asynchronous on `stream`.
+ * Errors: INVALID_ARG (no work enqueued), CUDA.
+ */
+fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
+                        void* values_out, int64_t* exps_out, fpe_diag* diag_out,
+                        void* workspace, size_t ws_bytes, void* stream);
+
+/*
+ * fpe_evaluate_host -- the same as fpe_evaluate for HOST buffers (points in, values and
+ * exponents out), staging through device memory owned by the handle; host<->device copies
+ * are pipelined with the kernels in chunks.  Pinned host memory gives full copy bandwidth.
+ * Synchronous: returns when the host outputs are written.  Not thread-safe per handle.
+ */
+fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_dt,
+                             int64_t n_points, void* values_host, int64_t* exps_host,
+                             void* stream);
+
+/*
+ * fpe_horner -- the full Horner scheme over all coefficients a_k_min..a_k_max with
+ * in-loop exponent rescaling, the context baseline of the benchmark.
+ * Arguments as fpe_evaluate (no diagnostics).
+ */
+fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
+                      void* values_out, int64_t* exps_out, void* workspace, size_t ws_bytes,
+                      void* stream);
+
+/* Counters of the last fpe_evaluate on this handle's stream-ordered statistics buffer:
+ * stats[0] = hard-to-round lambdas, stats[1] = kernel launches.  Host array of 4. */
+fpe_status fpe_last_stats(fpe_poly h, int64_t* stats4);
+
+void fpe_destroy(fpe_poly h);
+const char* fpe_status_string(fpe_status s);
+const char* fpe_last_error_detail(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPE_H_ */

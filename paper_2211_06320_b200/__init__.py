@@ -1,0 +1,241 @@
+"""B200-native Fast Polynomial Evaluator (arXiv 2211.06320) -- Python binding.
+
+A thin layer over libfpe.so (include/fpe.h): it marshals torch tensors to
+pointers and back.  Every step of the evaluation runs in the library's sm_100a
+kernels; torch provides device memory, streams and process groups only.
+
+    import paper_2211_06320_b200 as fpe
+    poly = fpe.precondition(coeffs)              # Algorithm FPE_p lines 2-4
+    vals, exps = poly.evaluate(points_cuda)      # lines 5-9: value = vals * 2**exps
+    vals, exps = poly.horner(points_cuda)        # full Horner (context baseline)
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import (DIAG_BYTES, FPE_C32, FPE_C64, FPE_R32, FPE_R64, FpeError, FpeInfo, check, lib)
+
+__all__ = ["precondition", "precondition_buffer", "Poly", "FpeError", "diag_fields", "header_fields"]
+
+_TORCH_DT = None
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    m = {torch.float64: FPE_R64, torch.complex128: FPE_C64, torch.float32: FPE_R32, torch.complex64: FPE_C32}
+    if isinstance(t, torch.Tensor):
+        if t.dtype not in m:
+            raise TypeError(f"unsupported dtype {t.dtype}")
+        return m[t.dtype]
+    dt = np.asarray(t).dtype
+    nm = {np.dtype(np.float64): FPE_R64, np.dtype(np.complex128): FPE_C64,
+          np.dtype(np.float32): FPE_R32, np.dtype(np.complex64): FPE_C32}
+    if dt not in nm:
+        raise TypeError(f"unsupported dtype {dt}")
+    return nm[dt]
+
+
+def _stream_ptr(stream, device):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _out_dtype(poly_dt: int, pt_dt: int):
+    torch = _torch()
+    cplx = poly_dt in (FPE_C64, FPE_C32) or pt_dt in (FPE_C64, FPE_C32)
+    f32 = pt_dt in (FPE_R32, FPE_C32)
+    if f32:
+        return torch.complex64 if cplx else torch.float32
+    return torch.complex128 if cplx else torch.float64
+
+
+class Poly:
+    """Handle of an immutable preconditioned polynomial on one CUDA device."""
+
+    def __init__(self, handle: C.c_void_p, device: int):
+        self._h = handle
+        self.device = device
+        info = FpeInfo()
+        check(lib().fpe_poly_get_info(self._h, C.byref(info)), "fpe_poly_get_info")
+        self.info = {f: getattr(info, f) for f, _ in FpeInfo._fields_ if f != "reserved"}
+        self._ws = None
+
+    # -- metadata -----------------------------------------------------------
+    @property
+    def nbytes(self) -> int:
+        return int(self.info["bytes"])
+
+    def hull(self):
+        n = int(self.info["n_hull"])
+        hk = np.empty(n, np.int32); hh = np.empty(n, np.int32); cnt = C.c_int64(0)
+        check(lib().fpe_poly_get_hull(self._h, hk.ctypes.data, hh.ctypes.data, n, C.byref(cnt)), "fpe_poly_get_hull")
+        return hk, hh
+
+    def device_buffer(self):
+        p = C.c_void_p(); b = C.c_size_t()
+        check(lib().fpe_poly_device_buffer(self._h, C.byref(p), C.byref(b)), "fpe_poly_device_buffer")
+        return p.value, b.value
+
+    def export(self, dst_ptr: int, cap: int, stream=None):
+        check(lib().fpe_poly_export(self._h, C.c_void_p(dst_ptr), cap, _stream_ptr(stream, self.device)),
+              "fpe_poly_export")
+
+    @classmethod
+    def from_buffer(cls, ptr: int, nbytes: int, device: int = 0, stream=None):
+        h = C.c_void_p()
+        check(lib().fpe_poly_from_device_buffer(C.c_void_p(ptr), nbytes, device, _stream_ptr(stream, device),
+                                                C.byref(h)), "fpe_poly_from_device_buffer")
+        return cls(h, device)
+
+    # -- evaluation ---------------------------------------------------------
+    def workspace(self, n: int):
+        torch = _torch()
+        sz = C.c_size_t()
+        check(lib().fpe_eval_workspace_size(self._h, n, C.byref(sz)), "fpe_eval_workspace_size")
+        if self._ws is None or self._ws.numel() < sz.value:
+            self._ws = torch.empty(max(sz.value, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
+        return self._ws
+
+    def evaluate(self, points, exps: bool = True, diag: bool = False, out=None, stream=None):
+        """Q_lambda(z) for every point (device tensor).  Returns (values, exps[, diag])."""
+        return self._run(lib().fpe_evaluate, points, exps, diag, out, stream, "fpe_evaluate")
+
+    def horner(self, points, exps: bool = True, out=None, stream=None):
+        """Full Horner over all stored coefficients (context baseline)."""
+        return self._run(lib().fpe_horner, points, exps, False, out, stream, "fpe_horner")
+
+    def _run(self, fn, points, want_exps, want_diag, out, stream, where):
+        torch = _torch()
+        if not points.is_cuda:
+            raise ValueError("points must be a CUDA tensor (use evaluate_host for host arrays)")
+        points = points.contiguous()
+        n = points.numel()
+        pdt = _dtype_code(points)
+        dev = points.device
+        vals = out if out is not None else torch.empty(n, dtype=_out_dtype(self.info["dtype"], pdt), device=dev)
+        e = torch.empty(n, dtype=torch.int64, device=dev) if want_exps else None
+        dg = torch.empty((n, DIAG_BYTES), dtype=torch.uint8, device=dev) if want_diag else None
+        ws = self.workspace(n)
+        args = [self._h, C.c_void_p(points.data_ptr()), pdt, n, C.c_void_p(vals.data_ptr()),
+                C.c_void_p(e.data_ptr() if e is not None else 0)]
+        if fn is lib().fpe_evaluate:
+            args.append(C.c_void_p(dg.data_ptr() if dg is not None else 0))
+        args += [C.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, dev)]
+        check(fn(*args), where)
+        if want_diag:
+            return vals, e, dg
+        return vals, e
+
+    def evaluate_host(self, points: np.ndarray, exps: bool = True):
+        """End-to-end evaluation from host memory (pinned for full bandwidth)."""
+        pts = np.ascontiguousarray(points)
+        pdt = _dtype_code(pts)
+        n = len(pts)
+        torch = _torch()
+        odt = _out_dtype(self.info["dtype"], pdt)
+        npdt = {torch.complex128: np.complex128, torch.float64: np.float64,
+                torch.complex64: np.complex64, torch.float32: np.float32}[odt]
+        vals = np.empty(n, npdt)
+        e = np.empty(n, np.int64) if exps else None
+        check(lib().fpe_evaluate_host(self._h, pts.ctypes.data, pdt, n, vals.ctypes.data,
+                                      e.ctypes.data if e is not None else None, None), "fpe_evaluate_host")
+        return vals, e
+
+    def evaluate_host_ptr(self, pts_ptr: int, pdt: int, n: int, vals_ptr: int, exps_ptr: int):
+        """Raw-pointer variant of evaluate_host (pinned torch tensors in bench.py)."""
+        check(lib().fpe_evaluate_host(self._h, C.c_void_p(pts_ptr), pdt, n, C.c_void_p(vals_ptr),
+                                      C.c_void_p(exps_ptr), None), "fpe_evaluate_host")
+
+    def last_stats(self):
+        s = np.zeros(4, np.int64)
+        check(lib().fpe_last_stats(self._h, s.ctypes.data), "fpe_last_stats")
+        return {"hard_lambdas": int(s[0]), "launches": int(s[1])}
+
+    def close(self):
+        if self._h:
+            lib().fpe_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def precondition(coeffs, p: int | None = None, drop: int | None = None, device: int | None = None,
+                 stream=None) -> Poly:
+    """Algorithm FPE_p lines 2-4 on a numpy array or torch tensor (host or device)."""
+    torch = _torch()
+    dt = _dtype_code(coeffs)
+    if device is None:
+        device = coeffs.device.index if isinstance(coeffs, torch.Tensor) and coeffs.is_cuda else torch.cuda.current_device()
+    keep = coeffs
+    if isinstance(coeffs, torch.Tensor):
+        keep = coeffs.contiguous()
+        ptr = keep.data_ptr()
+    else:
+        keep = np.ascontiguousarray(coeffs)
+        ptr = keep.ctypes.data
+    n = keep.numel() if isinstance(keep, torch.Tensor) else len(keep)
+    h = C.c_void_p()
+    check(lib().fpe_precondition(C.c_void_p(ptr), n, dt, p or 0, drop or 0, device,
+                                 _stream_ptr(stream, device), C.byref(h)), "fpe_precondition")
+    return Poly(h, device)
+
+
+def precondition_buffer(coeffs: np.ndarray, p: int | None = None, drop: int | None = None) -> np.ndarray:
+    """Host-only preconditioning: the flat buffer (uint8) a handle would hold.  No GPU needed."""
+    a = np.ascontiguousarray(coeffs)
+    dt = _dtype_code(a)
+    sz = C.c_size_t(0)
+    st = lib().fpe_precondition_host(a.ctypes.data, len(a), dt, p or 0, drop or 0, None, 0, C.byref(sz))
+    if st != 1:   # INVALID_ARG carries the size query
+        check(st, "fpe_precondition_host")
+    buf = np.zeros(sz.value, np.uint8)
+    check(lib().fpe_precondition_host(a.ctypes.data, len(a), dt, p or 0, drop or 0, buf.ctypes.data,
+                                      sz.value, C.byref(sz)), "fpe_precondition_host")
+    return buf
+
+
+_HDR = np.dtype([("magic", "<u8"), ("version", "<u4"), ("dtype", "<i4"), ("n_coeffs", "<i8"), ("k_min", "<i8"),
+                 ("k_max", "<i8"), ("n_hull", "<i8"), ("n_good", "<i8"), ("p", "<i4"), ("drop", "<i4"),
+                 ("shift", "<i4"), ("sparse", "<i4"), ("all_good", "<i4"), ("pad0", "<i4"), ("off_hull", "<u8"),
+                 ("off_coef", "<u8"), ("off_prefix", "<u8"), ("off_sidx", "<u8"), ("bytes", "<u8")])
+
+
+def header_fields(buf: np.ndarray) -> dict:
+    """Decode the 256-byte header and the sections of a flat buffer (host uint8 array)."""
+    h = np.frombuffer(buf[:_HDR.itemsize].tobytes(), dtype=_HDR)[0]
+    d = {k: int(h[k]) for k in _HDR.names}
+    nv = d["n_hull"]
+    hull = np.frombuffer(buf[d["off_hull"]:d["off_hull"] + 8 * nv].tobytes(), dtype=np.int32).reshape(nv, 2)
+    d["hk"], d["hh"] = hull[:, 0].copy(), hull[:, 1].copy()
+    cdt = {FPE_R64: np.float64, FPE_C64: np.complex128, FPE_R32: np.float32, FPE_C32: np.complex64}[d["dtype"]]
+    ncoef = d["n_good"] if d["sparse"] else d["k_max"] - d["k_min"] + 1
+    sz = np.dtype(cdt).itemsize
+    d["coef"] = np.frombuffer(buf[d["off_coef"]:d["off_coef"] + sz * ncoef].tobytes(), dtype=cdt)
+    if d["off_sidx"]:
+        d["sidx"] = np.frombuffer(buf[d["off_sidx"]:d["off_sidx"] + 4 * d["n_good"]].tobytes(), dtype=np.int32)
+    if d["off_prefix"]:
+        m = d["k_max"] - d["k_min"] + 2
+        d["prefix"] = np.frombuffer(buf[d["off_prefix"]:d["off_prefix"] + 4 * m].tobytes(), dtype=np.int32)
+    return d
+
+
+def diag_fields(dg):
+    """Split a (n, 32) uint8 diag tensor into named tensors (lambda, region, l, r, kept, hard)."""
+    raw = dg.contiguous()
+    lam = raw[:, 0:8].contiguous().view(_torch().float64).reshape(-1)
+    ints = raw[:, 8:32].contiguous().view(_torch().int32).reshape(-1, 6)
+    return {"lambda": lam, "region": ints[:, 0], "l": ints[:, 1], "r": ints[:, 2],
+            "kept": ints[:, 3], "hard": ints[:, 4]}

@@ -1,0 +1,346 @@
+// api.cu -- the C ABI of include/fpe.h.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+#include "fpe_internal.h"
+#include "kernels.cuh"
+
+namespace fpe {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+#define FPE_CUDA(call)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      fpe::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return FPE_ERR_CUDA;                                                                  \
+    }                                                                                       \
+  } while (0)
+
+static size_t dtype_size(int dt) {
+  switch (dt) { case FPE_R64: return 8; case FPE_C64: return 16; case FPE_R32: return 4; case FPE_C32: return 8; }
+  return 0;
+}
+static bool dtype_ok(int dt) { return dt >= FPE_R64 && dt <= FPE_C32; }
+static bool is_f32(int dt) { return dt == FPE_R32 || dt == FPE_C32; }
+
+// RAII device guard
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) { cudaGetDevice(&prev); if (prev != dev) cudaSetDevice(dev); }
+  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+static size_t ws_bytes_for(long long n) {
+  return ((size_t)n * sizeof(int2) + 255) & ~size_t(255);
+}
+
+}  // namespace fpe
+
+fpe::PolyDev fpe_poly_s::view() const {
+  fpe::PolyDev P;
+  const char* b = static_cast<const char*>(dbuf);
+  P.hull = reinterpret_cast<const int2*>(b + hdr.off_hull);
+  P.coef = b + hdr.off_coef;
+  P.prefix = hdr.off_prefix ? reinterpret_cast<const int32_t*>(b + hdr.off_prefix) : nullptr;
+  P.sidx = hdr.off_sidx ? reinterpret_cast<const int32_t*>(b + hdr.off_sidx) : nullptr;
+  P.k_min = hdr.k_min; P.k_max = hdr.k_max; P.n_good = hdr.n_good;
+  P.nv = (int)hdr.n_hull; P.drop = hdr.drop; P.shift = hdr.shift;
+  P.sparse = hdr.sparse; P.all_good = hdr.all_good; P.cdt = hdr.dtype;
+  return P;
+}
+
+using namespace fpe;
+
+static fpe_status finish_handle(fpe_poly h) {
+  FPE_CUDA(cudaMalloc(&h->dstats, 4 * sizeof(unsigned long long)));
+  FPE_CUDA(cudaMemset(h->dstats, 0, 4 * sizeof(unsigned long long)));
+  return FPE_OK;
+}
+
+extern "C" {
+
+const char* fpe_status_string(fpe_status s) {
+  switch (s) {
+    case FPE_OK: return "FPE_OK";
+    case FPE_ERR_INVALID_ARG: return "FPE_ERR_INVALID_ARG";
+    case FPE_ERR_ZERO_POLY: return "FPE_ERR_ZERO_POLY";
+    case FPE_ERR_NONFINITE_COEFF: return "FPE_ERR_NONFINITE_COEFF";
+    case FPE_ERR_UNSUPPORTED: return "FPE_ERR_UNSUPPORTED";
+    case FPE_ERR_OOM: return "FPE_ERR_OOM";
+    case FPE_ERR_CUDA: return "FPE_ERR_CUDA";
+  }
+  return "FPE_ERR_UNKNOWN";
+}
+
+const char* fpe_last_error_detail(void) { return g_err; }
+
+void fpe_destroy(fpe_poly h) {
+  if (!h) return;
+  DeviceGuard g(h->device);
+  if (h->dbuf) cudaFree(h->dbuf);
+  if (h->dstats) cudaFree(h->dstats);
+  if (h->st_dev) cudaFree(h->st_dev);
+  for (void* s : h->st_streams) if (s) cudaStreamDestroy(static_cast<cudaStream_t>(s));
+  delete h;
+}
+
+fpe_status fpe_precondition(const void* coeffs, int64_t n_coeffs, fpe_dtype dt, int32_t p_bits,
+                            int32_t drop_override, int device, void* stream, fpe_poly* out) {
+  if (!coeffs || !out || n_coeffs < 1 || !dtype_ok(dt) || p_bits < 0 || drop_override < 0) {
+    set_error("fpe_precondition: invalid argument");
+    return FPE_ERR_INVALID_ARG;
+  }
+  if (n_coeffs > (1ll << 31) - 2) { set_error("fpe_precondition: n_coeffs > 2^31-2"); return FPE_ERR_UNSUPPORTED; }
+  *out = nullptr;
+  int ndev = 0;
+  FPE_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) { set_error("fpe_precondition: bad device %d", device); return FPE_ERR_INVALID_ARG; }
+  DeviceGuard g(device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // host copy of the coefficients (they may live on the device)
+  const size_t nbytes = (size_t)n_coeffs * dtype_size(dt);
+  std::vector<uint8_t> host;
+  const void* src = coeffs;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, coeffs) == cudaSuccess &&
+      (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged)) {
+    host.resize(nbytes);
+    FPE_CUDA(cudaMemcpyAsync(host.data(), coeffs, nbytes, cudaMemcpyDeviceToHost, s));
+    FPE_CUDA(cudaStreamSynchronize(s));
+    src = host.data();
+  }
+  cudaGetLastError();  // clear a benign error from cudaPointerGetAttributes on plain host memory
+  fpe_poly h = new (std::nothrow) fpe_poly_s();
+  if (!h) { set_error("out of host memory"); return FPE_ERR_OOM; }
+  h->device = device;
+  std::vector<uint8_t> flat;
+  fpe_status st = precondition_host(src, n_coeffs, dt, p_bits, drop_override, flat, h->hdr, h->hk, h->hh);
+  if (st != FPE_OK) { delete h; return st; }
+  if (cudaMalloc(&h->dbuf, flat.size()) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("cudaMalloc(%zu) failed", flat.size());
+    delete h;
+    return FPE_ERR_OOM;
+  }
+  cudaError_t e = cudaMemcpyAsync(h->dbuf, flat.data(), flat.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) { set_error("upload failed: %s", cudaGetErrorString(e)); fpe_destroy(h); return FPE_ERR_CUDA; }
+  st = finish_handle(h);
+  if (st != FPE_OK) { fpe_destroy(h); return st; }
+  *out = h;
+  return FPE_OK;
+}
+
+fpe_status fpe_precondition_host(const void* coeffs, int64_t n_coeffs, fpe_dtype dt, int32_t p_bits,
+                                 int32_t drop_override, void* buf, size_t cap, size_t* bytes) {
+  if (!coeffs || !bytes || n_coeffs < 1 || !dtype_ok(dt) || p_bits < 0 || drop_override < 0) {
+    set_error("fpe_precondition_host: invalid argument");
+    return FPE_ERR_INVALID_ARG;
+  }
+  if (n_coeffs > (1ll << 31) - 2) { set_error("fpe_precondition_host: n_coeffs > 2^31-2"); return FPE_ERR_UNSUPPORTED; }
+  std::vector<uint8_t> flat;
+  Header hdr;
+  std::vector<int32_t> hk, hh;
+  fpe_status st = precondition_host(coeffs, n_coeffs, dt, p_bits, drop_override, flat, hdr, hk, hh);
+  if (st != FPE_OK) return st;
+  *bytes = flat.size();
+  if (!buf || cap < flat.size()) { set_error("fpe_precondition_host: need %zu bytes", flat.size()); return FPE_ERR_INVALID_ARG; }
+  std::memcpy(buf, flat.data(), flat.size());
+  return FPE_OK;
+}
+
+fpe_status fpe_poly_export(fpe_poly h, void* dst, size_t cap, void* stream) {
+  if (!h || !dst || cap < h->hdr.bytes) { set_error("fpe_poly_export: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  FPE_CUDA(cudaMemcpyAsync(dst, h->dbuf, h->hdr.bytes, cudaMemcpyDefault, s));
+  FPE_CUDA(cudaStreamSynchronize(s));
+  return FPE_OK;
+}
+
+fpe_status fpe_poly_get_info(fpe_poly h, fpe_poly_info* out) {
+  if (!h || !out) { set_error("fpe_poly_get_info: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  out->d = h->hdr.n_coeffs - 1;
+  out->k_min = h->hdr.k_min; out->k_max = h->hdr.k_max;
+  out->n_hull = h->hdr.n_hull; out->n_good = h->hdr.n_good;
+  out->p = h->hdr.p; out->drop = h->hdr.drop; out->shift = h->hdr.shift;
+  out->sparse = h->hdr.sparse; out->dtype = h->hdr.dtype; out->reserved = 0;
+  out->bytes = h->hdr.bytes;
+  return FPE_OK;
+}
+
+fpe_status fpe_poly_get_hull(fpe_poly h, int32_t* hk, int32_t* hh, int64_t cap, int64_t* n) {
+  if (!h || !n) { set_error("fpe_poly_get_hull: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  *n = (int64_t)h->hk.size();
+  if (cap < *n || !hk || !hh) { set_error("fpe_poly_get_hull: capacity %lld < %lld", (long long)cap, (long long)*n); return FPE_ERR_INVALID_ARG; }
+  std::copy(h->hk.begin(), h->hk.end(), hk);
+  std::copy(h->hh.begin(), h->hh.end(), hh);
+  return FPE_OK;
+}
+
+fpe_status fpe_poly_device_buffer(fpe_poly h, const void** dptr, size_t* bytes) {
+  if (!h || !dptr || !bytes) { set_error("fpe_poly_device_buffer: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  *dptr = h->dbuf;
+  *bytes = h->hdr.bytes;
+  return FPE_OK;
+}
+
+fpe_status fpe_poly_from_device_buffer(const void* dptr, size_t bytes, int device, void* stream, fpe_poly* out) {
+  if (!dptr || !out || bytes < sizeof(Header)) { set_error("fpe_poly_from_device_buffer: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  *out = nullptr;
+  DeviceGuard g(device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  fpe_poly h = new (std::nothrow) fpe_poly_s();
+  if (!h) { set_error("out of host memory"); return FPE_ERR_OOM; }
+  h->device = device;
+  cudaError_t e = cudaMemcpyAsync(&h->hdr, dptr, sizeof(Header), cudaMemcpyDefault, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) { set_error("header read failed: %s", cudaGetErrorString(e)); delete h; return FPE_ERR_CUDA; }
+  if (h->hdr.magic != kMagic || h->hdr.version != kVersion || h->hdr.bytes != bytes) {
+    set_error("fpe_poly_from_device_buffer: not an fpe buffer (magic/version/size mismatch)");
+    delete h;
+    return FPE_ERR_INVALID_ARG;
+  }
+  if (cudaMalloc(&h->dbuf, bytes) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc failed"); delete h; return FPE_ERR_OOM; }
+  std::vector<int2> hull(h->hdr.n_hull);
+  e = cudaMemcpyAsync(h->dbuf, dptr, bytes, cudaMemcpyDefault, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hull.data(), static_cast<const char*>(dptr) + h->hdr.off_hull,
+                                            hull.size() * sizeof(int2), cudaMemcpyDefault, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) { set_error("buffer copy failed: %s", cudaGetErrorString(e)); fpe_destroy(h); return FPE_ERR_CUDA; }
+  for (auto v : hull) { h->hk.push_back(v.x); h->hh.push_back(v.y); }
+  fpe_status st = finish_handle(h);
+  if (st != FPE_OK) { fpe_destroy(h); return st; }
+  *out = h;
+  return FPE_OK;
+}
+
+fpe_status fpe_eval_workspace_size(fpe_poly h, int64_t n_points, size_t* bytes) {
+  if (!h || !bytes || n_points < 0) { set_error("fpe_eval_workspace_size: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  *bytes = ws_bytes_for(n_points);
+  return FPE_OK;
+}
+
+static fpe_status check_eval_args(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n, void* values) {
+  if (!h || n < 0 || !dtype_ok(pt_dt) || (n > 0 && (!points || !values))) {
+    set_error("fpe_evaluate: invalid argument");
+    return FPE_ERR_INVALID_ARG;
+  }
+  if (is_f32(pt_dt) != is_f32(h->hdr.dtype)) {
+    set_error("fpe_evaluate: point precision (%s) must match the coefficient precision",
+              is_f32(pt_dt) ? "fp32" : "fp64");
+    return FPE_ERR_INVALID_ARG;
+  }
+  return FPE_OK;
+}
+
+fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
+                        void* values_out, int64_t* exps_out, fpe_diag* diag_out,
+                        void* workspace, size_t ws_bytes, void* stream) {
+  fpe_status st = check_eval_args(h, points, pt_dt, n_points, values_out);
+  if (st != FPE_OK) return st;
+  if (n_points == 0) return FPE_OK;
+  if (!workspace || ws_bytes < ws_bytes_for(n_points)) {
+    set_error("fpe_evaluate: workspace of %zu bytes < %zu", ws_bytes, ws_bytes_for(n_points));
+    return FPE_ERR_INVALID_ARG;
+  }
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  PolyDev P = h->view();
+  int2* lr = static_cast<int2*>(workspace);
+  FPE_CUDA(cudaMemsetAsync(h->dstats, 0, sizeof(unsigned long long), s));
+  launch_classify(pt_dt, points, n_points, P, lr, diag_out, h->dstats, s);
+  launch_eval_point(pt_dt, points, n_points, P, lr, values_out, reinterpret_cast<long long*>(exps_out), s);
+  h->last_launches = 2;
+  FPE_CUDA(cudaGetLastError());
+  return FPE_OK;
+}
+
+fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
+                      void* values_out, int64_t* exps_out, void* workspace, size_t ws_bytes, void* stream) {
+  (void)workspace; (void)ws_bytes;
+  fpe_status st = check_eval_args(h, points, pt_dt, n_points, values_out);
+  if (st != FPE_OK) return st;
+  if (n_points == 0) return FPE_OK;
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  PolyDev P = h->view();
+  launch_horner(pt_dt, points, n_points, P, values_out, reinterpret_cast<long long*>(exps_out), s);
+  h->last_launches = 1;
+  FPE_CUDA(cudaGetLastError());
+  return FPE_OK;
+}
+
+fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_dt, int64_t n_points,
+                             void* values_host, int64_t* exps_host, void* stream) {
+  fpe_status st = check_eval_args(h, points_host, pt_dt, n_points, values_host);
+  if (st != FPE_OK) return st;
+  if (n_points == 0) return FPE_OK;
+  DeviceGuard g(h->device);
+  (void)stream;
+  const bool cplx_out = (pt_dt == FPE_C64 || pt_dt == FPE_C32 || h->hdr.dtype == FPE_C64 || h->hdr.dtype == FPE_C32);
+  const size_t in_sz = dtype_size(pt_dt);
+  const size_t out_sz = is_f32(pt_dt) ? (cplx_out ? 8 : 4) : (cplx_out ? 16 : 8);
+  const long long chunk = std::min<long long>(n_points, 1ll << 22);
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t per = al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8) + ws_bytes_for(chunk);
+  if (h->st_bytes < 2 * per) {
+    if (h->st_dev) { cudaFree(h->st_dev); h->st_dev = nullptr; h->st_bytes = 0; }
+    if (cudaMalloc(&h->st_dev, 2 * per) != cudaSuccess) { cudaGetLastError(); set_error("staging cudaMalloc failed"); return FPE_ERR_OOM; }
+    h->st_bytes = 2 * per;
+  }
+  for (int b = 0; b < 2; ++b)
+    if (!h->st_streams[b]) {
+      cudaStream_t ns;
+      FPE_CUDA(cudaStreamCreateWithFlags(&ns, cudaStreamNonBlocking));
+      h->st_streams[b] = ns;
+    }
+  PolyDev P = h->view();
+  long long launches = 0;
+  for (long long off = 0, c = 0; off < n_points; off += chunk, ++c) {
+    const long long m = std::min(chunk, n_points - off);
+    const int b = (int)(c & 1);
+    cudaStream_t s = static_cast<cudaStream_t>(h->st_streams[b]);
+    char* base = static_cast<char*>(h->st_dev) + b * per;
+    void* dp = base;
+    void* dv = base + al(chunk * in_sz);
+    long long* de = reinterpret_cast<long long*>(base + al(chunk * in_sz) + al(chunk * out_sz));
+    int2* lr = reinterpret_cast<int2*>(base + al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8));
+    FPE_CUDA(cudaMemcpyAsync(dp, static_cast<const char*>(points_host) + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s));
+    launch_classify(pt_dt, dp, m, P, lr, nullptr, h->dstats, s);
+    launch_eval_point(pt_dt, dp, m, P, lr, dv, exps_host ? de : nullptr, s);
+    launches += 2;
+    FPE_CUDA(cudaGetLastError());
+    FPE_CUDA(cudaMemcpyAsync(static_cast<char*>(values_host) + off * out_sz, dv, m * out_sz, cudaMemcpyDeviceToHost, s));
+    if (exps_host) FPE_CUDA(cudaMemcpyAsync(exps_host + off, de, m * 8, cudaMemcpyDeviceToHost, s));
+  }
+  for (int b = 0; b < 2; ++b) FPE_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(h->st_streams[b])));
+  h->last_launches = launches;
+  return FPE_OK;
+}
+
+fpe_status fpe_last_stats(fpe_poly h, int64_t* stats4) {
+  if (!h || !stats4) { set_error("fpe_last_stats: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  DeviceGuard g(h->device);
+  unsigned long long v[4];
+  FPE_CUDA(cudaMemcpy(v, h->dstats, sizeof(v), cudaMemcpyDeviceToHost));
+  stats4[0] = (int64_t)v[0];
+  stats4[1] = h->last_launches;
+  stats4[2] = 0; stats4[3] = 0;
+  return FPE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// fpe_internal.h -- layout of the preconditioned polynomial and kernel parameters.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+#include <vector_types.h>
+#include "../../include/fpe.h"
+
+namespace fpe {
+
+constexpr uint64_t kMagic = 0x4650453230304232ull;  // "FPE200B2"
+constexpr uint32_t kVersion = 1;
+
+// First 256 bytes of the flat device buffer (also kept on the host in the handle).
+// Sections follow, each 256-byte aligned:
+//   hull   int2[n_hull]                (k, s(a_k)) of the canonical cover vertices
+//   coef   dense : CT[d_eff + 1]        a_k 2^-shift for k in [k_min, k_max], 0 where k not in G_p
+//          sparse: CT[n_good]           a_k 2^-shift for the good indices
+//   prefix int32[d_eff + 2]             dense & not all_good: #G_p below k (k - k_min)
+//   sidx   int32[n_good]                sparse: the good indices, increasing
+struct Header {
+  uint64_t magic;
+  uint32_t version;
+  int32_t dtype;        // fpe_dtype of the stored coefficients
+  int64_t n_coeffs, k_min, k_max, n_hull, n_good;
+  int32_t p, drop, shift, sparse, all_good, pad0;
+  uint64_t off_hull, off_coef, off_prefix, off_sidx, bytes;
+  uint8_t reserved[136];
+};
+static_assert(sizeof(Header) == 256, "header must be 256 bytes");
+
+// Kernel-side view of a handle.
+struct PolyDev {
+  const int2* hull;
+  const void* coef;
+  const int32_t* prefix;
+  const int32_t* sidx;
+  long long k_min, k_max, n_good;
+  int nv, drop, shift, sparse, all_good, cdt;
+};
+
+}  // namespace fpe
+
+struct fpe_poly_s {
+  fpe::Header hdr;
+  int device = 0;
+  void* dbuf = nullptr;                 // flat device buffer (owned)
+  std::vector<int32_t> hk, hh;          // host copy of the cover
+  unsigned long long* dstats = nullptr; // device counters (hard-to-round lambdas)
+  long long last_launches = 0;
+  // staging for fpe_evaluate_host (grown on demand, owned)
+  void* st_dev = nullptr; size_t st_bytes = 0;
+  void* st_streams[2] = {nullptr, nullptr};
+  fpe::PolyDev view() const;
+};
+
+namespace fpe {
+void set_error(const char* fmt, ...);
+fpe_status precondition_host(const void* coeffs_host, int64_t n, fpe_dtype dt, int32_t p_bits,
+                             int32_t drop_override, std::vector<uint8_t>& flat, Header& hdr,
+                             std::vector<int32_t>& hk, std::vector<int32_t>& hh);
+}  // namespace fpe

@@ -1,0 +1,15 @@
+// kernels.cuh -- launchers of kernels.cu (host side).
+#pragma once
+#include <cuda_runtime.h>
+#include "fpe_internal.h"
+
+namespace fpe {
+constexpr int kSmemHullMax = 6144;   // cover vertices staged in shared memory (48 KiB)
+
+void launch_classify(int pk, const void* pts, long long n, const PolyDev& P, int2* lr, fpe_diag* diag,
+                     unsigned long long* hard, cudaStream_t s);
+bool launch_eval_point(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
+                       long long* exps, cudaStream_t s);
+bool launch_horner(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
+                   cudaStream_t s);
+}  // namespace fpe

@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle.
+
+Indexing (lambda, region = k_lambda vertex, l, r, K) must match bit-exactly;
+values must satisfy |P_gpu - P_ref| <= 2^-45 S (fp64) or 2^-16 S (fp32),
+S = sum_k |a_k||z|^k (BASELINE.json north_star), with P_ref the oracle's
+Q_lambda in binary128.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from parity import abs_sum_log2, check_indexing, gpu_eval, rel_err_vs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL64 = 2.0 ** -45
+TOL32 = 2.0 ** -16
+
+
+@pytest.fixture(scope="module")
+def fpe():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2211_06320_b200 import build
+    build.build()
+    import paper_2211_06320_b200 as m
+    return m
+
+
+def _values_ok(P, poly_coeffs, pts, out, idx, tol, cls=None):
+    sub = pts[idx]
+    c = P.classify(sub) if cls is None else {k: v[idx] for k, v in cls.items()}
+    Q = P.fpe_eval(sub, c)
+    l2S = abs_sum_log2(poly_coeffs, sub)
+    err = rel_err_vs(Q, out["v"][idx], out["e"][idx], l2S)
+    fin = np.isfinite(l2S) & (c["l"] >= 0)
+    assert np.all(err[fin] <= tol), (np.max(err[fin]), idx[np.argmax(np.where(fin, err, 0))])
+    return err[fin]
+
+
+# ------------------------------------------------------------------ cfg 1 -----
+def test_cfg1_all_points(fpe):
+    a = workloads.coefficients(1)
+    pts = workloads.points(1)
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    out = gpu_eval(poly, pts)
+    cls = check_indexing(P, pts, out["diag"])
+    err = _values_ok(P, a, pts, out, np.arange(len(pts)), TOL64, cls)
+    assert np.max(err) < 2.0 ** -48
+    # Theorem thm:equivAlgo on the sphere: mean #[l, r] < 1 + 1.9046 sqrt(d (p + s(d) + 3))
+    width = cls["r"] - cls["l"] + 1
+    assert width.mean() < 1 + 1.9046 * math.sqrt(P.d_eff * P.drop)
+
+
+def test_worked_example_through_abi(fpe, worked):
+    s = np.array(worked["scales"])
+    a = np.ldexp(1.0, s - 1).astype(np.complex128)
+    pts = np.array([np.exp(0.3j), 0.125 * np.exp(1.1j), 1.0 + 0j, 0.125 + 0j])
+    for drop, tag in ((6, "drop6"), (None, "drop13")):
+        poly = fpe.precondition(a, p=6, drop=drop)
+        out = gpu_eval(poly, pts)
+        d = out["diag"]
+        band = worked["derived_not_printed"]["band_" + tag]
+        W = worked["derived_not_printed"]["W_" + tag]
+        for i in (0, 2):
+            assert [d["l"][i], d["r"][i]] == band["lambda0"] and d["kept"][i] == len(W["lambda0"])
+        for i in (1, 3):
+            assert [d["l"][i], d["r"][i]] == band["lambda_m3"] and d["kept"][i] == len(W["lambda_m3"])
+        P = oracle.OraclePoly(a, p=6, drop=drop)
+        check_indexing(P, pts, d)
+
+
+def test_special_points(fpe):
+    a = workloads.coefficients(1, d=200)
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    hk, hh = P.hk, P.hh
+    sp = [0j, 1 + 0j, -1 + 0j, 1j, -1j, 2.0 + 0j, 0.5j, 2.0 ** -1074 + 0j, complex(2.0 ** 1000, 0),
+          complex(1e300, 1e300), complex(1e-300, 1e-310), complex(1.0, 2.0 ** -30), complex(1.0, 1e-200),
+          complex(1 - 2 ** -53, 2 ** -26), complex(math.nextafter(1.0, 2.0), 0), complex(0.6, 0.8),
+          complex(3 / 5, -4 / 5), np.exp(1j * 2.0), complex(math.sqrt(0.5), math.sqrt(0.5))]
+    # |z| = 2^slope exactly for integer hull slopes (argmax ties), and dyadic radii
+    for j in range(len(hk) - 1):
+        sl = (hh[j + 1] - hh[j]) / (hk[j + 1] - hk[j])
+        if float(sl).is_integer():
+            sp.append(complex(2.0 ** (-sl), 0))
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        t = rng.uniform(0, 2 * np.pi)
+        sp.append(np.exp(1j * t) * (1 + rng.choice([-1, 1]) * 2.0 ** -rng.integers(1, 60)))
+    pts = np.array(sp, dtype=np.complex128)
+    out = gpu_eval(poly, pts)
+    cls = check_indexing(P, pts, out["diag"])
+    finite = np.isfinite(pts)
+    _values_ok(P, a, pts, out, np.flatnonzero(finite & (pts != 0)), TOL64, cls)
+    # z = 0 gives a_0 exactly
+    v0 = out["v"][0] * 2.0 ** out["e"][0]
+    assert v0 == a[0]
+    nanpts = np.array([complex(np.nan, 0), complex(np.inf, 1), complex(0, -np.inf)])
+    o2 = gpu_eval(poly, nanpts)
+    assert np.all(np.isnan(o2["v"].real)) and np.all(o2["diag"]["region"] == -1)
+
+
+def test_empty_and_ragged(fpe):
+    a = workloads.coefficients(1, d=50)
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    e = torch.empty(0, dtype=torch.complex128, device="cuda")
+    v, ex = poly.evaluate(e)
+    assert v.numel() == 0
+    for n in (1, 31, 127, 129, 1000, 4097):
+        pts = workloads.sphere_points(1, n)
+        out = gpu_eval(poly, pts)
+        cls = check_indexing(P, pts, out["diag"])
+        _values_ok(P, a, pts, out, np.arange(n), TOL64, cls)
+
+
+# ------------------------------------------------------- full-size configs ----
+def _sampled_config(fpe, cfg, n_idx, n_val, fp32=False, n_points=None):
+    a = workloads.coefficients(cfg)
+    pts = workloads.points(cfg, n_points)
+    if fp32:
+        a, pts = workloads.to_fp32(a), workloads.to_fp32(pts)
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    t = torch.from_numpy(pts).cuda()
+    v, e, dg = poly.evaluate(t, exps=True, diag=True)
+    idx = workloads.sample_indices(len(pts), n_idx, salt=cfg)
+    it = torch.from_numpy(idx).cuda()
+    import paper_2211_06320_b200 as m
+    D = {k: x[it].cpu().numpy() for k, x in m.diag_fields(dg).items()}
+    kept_all = m.diag_fields(dg)["kept"].double()
+    stats = {"mean_K": float(kept_all.mean()), "max_K": int(kept_all.max()),
+             "hard": int(m.diag_fields(dg)["hard"].sum())}
+    out = {"v": v[it].cpu().numpy(), "e": e[it].cpu().numpy()}
+    del v, e, dg, t
+    torch.cuda.empty_cache()
+    sub = pts[idx]
+    cls = check_indexing(P, sub, D)
+    vi = np.arange(min(n_val, len(idx)))
+    _values_ok(P, a, sub, out, vi, TOL32 if fp32 else TOL64, cls)
+    assert stats["hard"] == 0
+    return P, stats
+
+
+def test_cfg2_real_full(fpe):
+    P, st = _sampled_config(fpe, 2, 1 << 14, 256)
+    assert st["mean_K"] < 1 + 1.7673 * math.sqrt(P.d_eff * (P.drop + 1)) * 2   # real-line constant, loose
+
+
+def test_cfg3_bigrange_full(fpe):
+    P, st = _sampled_config(fpe, 3, 1 << 14, 128)
+    assert st["mean_K"] < 1 + 1.9046 * math.sqrt(P.d_eff * P.drop)
+
+
+def test_cfg4_sparse_full(fpe):
+    P, st = _sampled_config(fpe, 4, 1 << 14, 512)
+    assert st["max_K"] <= 4096
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+def test_cfg5_full(fpe, fp32):
+    P, st = _sampled_config(fpe, 5, 1 << 13, 64, fp32=fp32)
+    assert st["mean_K"] < 1 + 1.9046 * math.sqrt(P.d_eff * P.drop)
+
+
+# --------------------------------------------------------- other entry points --
+def test_horner_context(fpe):
+    a = workloads.coefficients(1)
+    pts = workloads.points(1, 2048)
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    out = gpu_eval(poly, pts, horner=True)
+    H = P.horner(pts)
+    l2S = abs_sum_log2(a, pts)
+    err = rel_err_vs(H, out["v"], out["e"], l2S)
+    assert np.all(err <= TOL64), err.max()
+    # large degree and large |z|: exponent tracking (cfg3 family, 16 points)
+    a3 = workloads.coefficients(3, d=(1 << 16) - 1)
+    p3 = workloads.points(3, 16) * np.array([1, 1e3, 1e-3, 7] * 4)
+    poly3 = fpe.precondition(a3)
+    P3 = oracle.OraclePoly(a3)
+    out = gpu_eval(poly3, p3, horner=True)
+    err = rel_err_vs(P3.horner(p3), out["v"], out["e"], abs_sum_log2(a3, p3))
+    assert np.all(err <= TOL64), err.max()
+
+
+def test_evaluate_host_matches_device(fpe):
+    a = workloads.coefficients(1)
+    pts = workloads.points(1)
+    poly = fpe.precondition(a)
+    out = gpu_eval(poly, pts, diag=False)
+    hv, he = poly.evaluate_host(pts)
+    assert np.array_equal(hv, out["v"]) and np.array_equal(he, out["e"])
+
+
+def test_determinism_permutation_and_batches(fpe):
+    a = workloads.coefficients(3, d=(1 << 16) - 1)
+    pts = workloads.points(3, 1 << 15)
+    poly = fpe.precondition(a)
+    base = gpu_eval(poly, pts, diag=False)
+    perm = np.random.default_rng(9).permutation(len(pts))
+    o = gpu_eval(poly, pts[perm], diag=False)
+    assert np.array_equal(o["v"], base["v"][perm]) and np.array_equal(o["e"], base["e"][perm])
+    parts = [gpu_eval(poly, pts[i:i + 5000], diag=False) for i in range(0, len(pts), 5000)]
+    assert np.array_equal(np.concatenate([p["v"] for p in parts]), base["v"])
+
+
+def test_buffer_roundtrip(fpe):
+    a = workloads.coefficients(4, d=1 << 16)
+    poly = fpe.precondition(a)
+    ptr, nb = poly.device_buffer()
+    poly2 = fpe.Poly.from_buffer(ptr, nb, device=0)
+    host = fpe.precondition_buffer(a)
+    poly3 = fpe.Poly.from_buffer(host.ctypes.data, len(host), device=0)
+    pts = workloads.points(4, 4096)
+    o1, o2, o3 = (gpu_eval(p, pts, diag=False) for p in (poly, poly2, poly3))
+    assert np.array_equal(o1["v"], o2["v"]) and np.array_equal(o1["v"], o3["v"])
+    with pytest.raises(fpe.FpeError):
+        bad = np.zeros(512, np.uint8)
+        fpe.Poly.from_buffer(bad.ctypes.data, len(bad), device=0)
+
+
+def test_plain_float_output(fpe):
+    a = workloads.coefficients(1, d=30)
+    poly = fpe.precondition(a)
+    pts = workloads.points(1, 1000)
+    t = torch.from_numpy(pts).cuda()
+    v1, e1 = poly.evaluate(t, exps=True)
+    v2, _ = poly.evaluate(t, exps=False)
+    v1, e1, v2 = v1.cpu().numpy(), e1.cpu().numpy(), v2.cpu().numpy()
+    ref_re = np.ldexp(v1.real, np.clip(e1, -4000, 4000).astype(np.int32))
+    ref_im = np.ldexp(v1.imag, np.clip(e1, -4000, 4000).astype(np.int32))
+    assert np.array_equal(v2.real, ref_re) and np.array_equal(v2.imag, ref_im)
