@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""bench.py -- FPE multi-point evaluation throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fpe|reference] [--config 3]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
+
+A step is one pass of the whole hot path -- fpe_evaluate: classification (lambda, k_lambda,
+[l, r]) and window evaluation of every point -- over one batch of synthetic points
+already resident in HBM.  Workload (default): BASELINE.json configs[2], complex fp64,
+d = 2^20 - 1, |a_k| = 2^(200 sin(pi k/d) + N(0,4)), 2^26 points uniform on the Riemann
+sphere per rank (weak scaling: every rank evaluates its own 2^26-point batch; the
+preconditioned polynomial is replicated once with an NCCL broadcast, untimed).
+Points (1 GiB/rank) exceed the 126 MB L2, so no flush is needed between steps.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "polynomial evals/sec (fp64 complex, d=2^20) at 1/2/4/8 B200; % of roofline"
+FP64_FMA_PEAK = 148 * 64 * 1.965e9      # SMs x fp64 FMA lanes/clk/SM x max SM clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fpe", choices=["fpe", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--points", type=int, default=0, help="override points per rank")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0:
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "fpe" else "gloo"
+        dist.init_process_group(backend=backend)
+        pg = dist
+    if args.impl == "fpe":
+        torch.cuda.set_device(local)
+    return world, rank, local, pg
+
+
+def reduce_max(pg, v: float, device) -> float:
+    if pg is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(pg, v: float, device) -> float:
+    if pg is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=pg.ReduceOp.SUM)
+    return float(t.item())
+
+
+def algorithmic_fma(diag_fields, cplx: bool) -> float:
+    """sum over points of c (K + 2 ceil(log2 l) [l > 0]): the paper's count (PAPER.md:1621-1627,
+    1321-1324), c = 4 fp64 FMAs per complex multiply-add, 1 for real."""
+    import torch
+    K = diag_fields["kept"].double()
+    l = diag_fields["l"].double()
+    pw = torch.where(l > 0, 2.0 * torch.ceil(torch.log2(torch.clamp(l, min=1.0))), torch.zeros_like(l))
+    c = 4.0 if cplx else 1.0
+    return float((c * (K + pw)).sum())
+
+
+def cpu_baseline(cfg: int, sample: int):
+    """The oracle as it stands (oracle/, binary128, OpenMP over all host cores), timed on a
+    bounded sample of the same workload: classification + Q_lambda for `sample` points."""
+    import numpy as np
+
+    import oracle
+    import workloads
+    a = workloads.coefficients(cfg)
+    t0 = time.perf_counter()
+    P = oracle.OraclePoly(a)
+    t_pre = time.perf_counter() - t0
+    pts = workloads.points(cfg, sample, shard=977)
+    t0 = time.perf_counter()
+    c = P.classify(pts)
+    P.fpe_eval(pts, c)
+    dt = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": sample / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
+            "sample": f"{sample} points of cfg{cfg} (same distribution, shard 977): binary128 classify + "
+                      f"Q_lambda; preconditioning {t_pre:.2f}s not included",
+            "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (CPU) on rank 0, each step a bounded sample."""
+    world, rank, local, pg = dist_setup(args)
+    if rank != 0:
+        return
+    import oracle
+    import workloads
+    cfg = args.config
+    sample = args.cpu_sample or 1024
+    a = workloads.coefficients(cfg)
+    P = oracle.OraclePoly(a)
+    pts = workloads.points(cfg, sample, shard=977)
+    for _ in range(args.warmup):
+        P.fpe_eval(pts[:64], P.classify(pts[:64]))
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        P.fpe_eval(pts, P.classify(pts))
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    val = sample / (ms * 1e-3)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    line = {"metric": METRIC, "value": val, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f128", "data": "synthetic", "impl": "reference",
+            "config": {"workload": workloads.CONFIGS[cfg]["name"], "points_per_step": sample, "sample": True},
+            "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{sample} points of cfg{cfg} per step (binary128 oracle)"},
+            "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_fpe(args):
+    import numpy as np
+    import torch
+
+    import paper_2211_06320_b200 as fpe
+    import workloads
+    from paper_2211_06320_b200 import dist as fdist
+
+    world, rank, local, pg = dist_setup(args)
+    dev = torch.device("cuda", local)
+    cfg = args.config
+    c = workloads.CONFIGS[cfg]
+    n = args.points or c["n_points"]
+    # -- replicate the preconditioned polynomial (rank 0 builds, NCCL broadcast; untimed) --
+    poly = None
+    if rank == 0:
+        poly = fpe.precondition(workloads.coefficients(cfg), device=local)
+    poly = fdist.replicate(poly, src=0, device=local) if pg is not None else poly
+    cplx = c["dtype"].startswith("c")
+    pts_np = workloads.points(cfg, n, shard=rank)
+    pts = torch.from_numpy(pts_np).to(dev)
+    vals = torch.empty(n, dtype=torch.complex128 if cplx else torch.float64, device=dev)
+    exps = torch.empty(n, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        poly.evaluate(pts, exps=True, out=vals)
+
+    # algorithmic work from one untimed diagnostic pass
+    _, _, dg = poly.evaluate(pts, exps=True, diag=True)
+    D = fpe.diag_fields(dg)
+    fma_total = algorithmic_fma(D, cplx)
+    meanK = float(D["kept"].double().mean())
+    hard = int(D["hard"].sum())
+    del dg, D
+    torch.cuda.empty_cache()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # -- timed region ------------------------------------------------------------------------
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = reduce_max(pg, ms_local, dev)
+    total_points = reduce_sum(pg, float(n), dev)
+    value = total_points / (ms * 1e-3)
+    launches = poly.last_stats()["launches"]
+
+    # -- per-kernel durations, live, on the launch stream (profiling events) --------------------
+    poly.set_profiling(True)
+    stage_acc = {}
+    for _ in range(max(3, min(args.steps, 5))):
+        step()
+        for name, t in poly.last_stage_ms():
+            stage_acc.setdefault(name, []).append(t)
+    poly.set_profiling(False)
+    stages = {k: statistics.mean(v) for k, v in stage_acc.items()}
+    dom = max(stages, key=stages.get)
+    dom_ms = stages[dom]
+    achieved = 2.0 * fma_total / (dom_ms * 1e-3) / 1e12        # TFLOP/s (2 flops per FMA)
+    peak = 2.0 * FP64_FMA_PEAK / 1e12
+
+    # -- end to end through the public API with host buffers (pinned) ---------------------------
+    e2e = None
+    if not args.no_e2e:
+        hp = torch.from_numpy(pts_np).pin_memory()
+        hv = torch.empty(n, dtype=vals.dtype).pin_memory()
+        he = torch.empty(n, dtype=torch.int64).pin_memory()
+        pdt = 1 if cplx else 0
+        poly.evaluate_host_ptr(hp.data_ptr(), pdt, n, hv.data_ptr(), he.data_ptr())
+        if pg is not None:
+            pg.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            poly.evaluate_host_ptr(hp.data_ptr(), pdt, n, hv.data_ptr(), he.data_ptr())
+        dt = (time.perf_counter() - t0) / args.e2e_steps
+        dt = reduce_max(pg, dt, dev)
+        e2e = {"value": total_points / dt, "unit": "evals/s", "h2d_bytes_per_step": int(n * pts.element_size()),
+               "d2h_bytes_per_step": int(n * (vals.element_size() + 8)), "ms_per_step": dt * 1e3}
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline(cfg, args.cpu_sample or 65536)
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": c["name"], "points_per_gpu": n, "degree": c["d"], "parallelism": f"points x{world}",
+                   "l2": "inputs (1 GiB/rank) larger than L2; no flush", "mean_kept_terms": meanK,
+                   "hard_lambdas": hard},
+        "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "peak_note": "fp64 FMA: 148 SM x 64 lanes x 1.965 GHz x 2 (guide unit counts/clock)",
+                     "algorithmic_fma_per_launch": fma_total, "kernel_ms": dom_ms, "stages_ms": stages},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches * args.steps),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_fpe(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,16 @@ fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n
                       void* values_out, int64_t* exps_out, void* workspace, size_t ws_bytes,
                       void* stream);
 
+/*
+ * Per-stage timing (measurement support for bench.py).  With fpe_set_profiling(h, 1) every
+ * later fpe_evaluate / fpe_horner on h records CUDA events on its stream around each kernel;
+ * fpe_last_stage_ms (synchronising the stream of that call) returns the stage durations in
+ * launch order (up to cap) and *n, and fpe_stage_name(h, i) names stage i.
+ */
+fpe_status fpe_set_profiling(fpe_poly h, int enable);
+fpe_status fpe_last_stage_ms(fpe_poly h, float* ms, int cap, int* n);
+const char* fpe_stage_name(fpe_poly h, int i);
+
 /* Counters of the last fpe_evaluate on this handle's stream-ordered statistics buffer:
  * stats[0] = hard-to-round lambdas, stats[1] = kernel launches.  Host array of 4. */
 fpe_status fpe_last_stats(fpe_poly h, int64_t* stats4);

@@ -155,6 +155,16 @@ class Poly:
         check(lib().fpe_evaluate_host(self._h, C.c_void_p(pts_ptr), pdt, n, C.c_void_p(vals_ptr),
                                       C.c_void_p(exps_ptr), None), "fpe_evaluate_host")
 
+    def set_profiling(self, on: bool = True):
+        check(lib().fpe_set_profiling(self._h, 1 if on else 0), "fpe_set_profiling")
+
+    def last_stage_ms(self):
+        """[(stage name, ms)] of the last evaluate/horner call (profiling must be on)."""
+        ms = (C.c_float * 16)()
+        n = C.c_int(0)
+        check(lib().fpe_last_stage_ms(self._h, ms, 16, C.byref(n)), "fpe_last_stage_ms")
+        return [(lib().fpe_stage_name(self._h, i).decode(), float(ms[i])) for i in range(n.value)]
+
     def last_stats(self):
         s = np.zeros(4, np.int64)
         check(lib().fpe_last_stats(self._h, s.ctypes.data), "fpe_last_stats")

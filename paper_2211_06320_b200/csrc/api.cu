@@ -47,6 +47,24 @@ static size_t ws_bytes_for(long long n) {
   return ((size_t)n * sizeof(int2) + 255) & ~size_t(255);
 }
 
+// Records an event before the first stage and after each stage when profiling is on.
+struct Stager {
+  fpe_poly h;
+  cudaStream_t s;
+  Stager(fpe_poly h_, cudaStream_t s_) : h(h_), s(s_) {
+    h->n_stages = 0;
+    h->prof_stream = s;
+    if (h->profiling) cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[0]), s);
+  }
+  void done(const char* name) {
+    if (h->n_stages < 15) {
+      h->stage_names[h->n_stages] = name;
+      ++h->n_stages;
+      if (h->profiling) cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[h->n_stages]), s);
+    }
+  }
+};
+
 }  // namespace fpe
 
 fpe::PolyDev fpe_poly_s::view() const {
@@ -94,6 +112,7 @@ void fpe_destroy(fpe_poly h) {
   if (h->dstats) cudaFree(h->dstats);
   if (h->st_dev) cudaFree(h->st_dev);
   for (void* s : h->st_streams) if (s) cudaStreamDestroy(static_cast<cudaStream_t>(s));
+  for (void* e : h->prof_events) if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   delete h;
 }
 
@@ -262,8 +281,11 @@ fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t
   PolyDev P = h->view();
   int2* lr = static_cast<int2*>(workspace);
   FPE_CUDA(cudaMemsetAsync(h->dstats, 0, sizeof(unsigned long long), s));
+  Stager stg(h, s);
   launch_classify(pt_dt, points, n_points, P, lr, diag_out, h->dstats, s);
+  stg.done("classify");
   launch_eval_point(pt_dt, points, n_points, P, lr, values_out, reinterpret_cast<long long*>(exps_out), s);
+  stg.done("eval_point");
   h->last_launches = 2;
   FPE_CUDA(cudaGetLastError());
   return FPE_OK;
@@ -278,7 +300,9 @@ fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n
   DeviceGuard g(h->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PolyDev P = h->view();
+  Stager stg(h, s);
   launch_horner(pt_dt, points, n_points, P, values_out, reinterpret_cast<long long*>(exps_out), s);
+  stg.done("horner_full");
   h->last_launches = 1;
   FPE_CUDA(cudaGetLastError());
   return FPE_OK;
@@ -330,6 +354,36 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   for (int b = 0; b < 2; ++b) FPE_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(h->st_streams[b])));
   h->last_launches = launches;
   return FPE_OK;
+}
+
+fpe_status fpe_set_profiling(fpe_poly h, int enable) {
+  if (!h) { set_error("fpe_set_profiling: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  DeviceGuard g(h->device);
+  if (enable && !h->prof_events[0])
+    for (auto& e : h->prof_events) {
+      cudaEvent_t ev;
+      FPE_CUDA(cudaEventCreate(&ev));
+      e = ev;
+    }
+  h->profiling = enable != 0;
+  return FPE_OK;
+}
+
+fpe_status fpe_last_stage_ms(fpe_poly h, float* ms, int cap, int* n) {
+  if (!h || !n || (cap > 0 && !ms)) { set_error("fpe_last_stage_ms: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  *n = h->n_stages;
+  if (!h->profiling) { set_error("fpe_last_stage_ms: profiling is off"); return FPE_ERR_INVALID_ARG; }
+  DeviceGuard g(h->device);
+  FPE_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(h->prof_events[h->n_stages])));
+  for (int i = 0; i < h->n_stages && i < cap; ++i)
+    FPE_CUDA(cudaEventElapsedTime(ms + i, static_cast<cudaEvent_t>(h->prof_events[i]),
+                                  static_cast<cudaEvent_t>(h->prof_events[i + 1])));
+  return FPE_OK;
+}
+
+const char* fpe_stage_name(fpe_poly h, int i) {
+  if (!h || i < 0 || i >= h->n_stages) return nullptr;
+  return h->stage_names[i];
 }
 
 fpe_status fpe_last_stats(fpe_poly h, int64_t* stats4) {

@@ -48,6 +48,12 @@ struct fpe_poly_s {
   std::vector<int32_t> hk, hh;          // host copy of the cover
   unsigned long long* dstats = nullptr; // device counters (hard-to-round lambdas)
   long long last_launches = 0;
+  // per-stage timing (fpe_set_profiling)
+  bool profiling = false;
+  void* prof_events[16] = {};
+  const char* stage_names[16] = {};
+  int n_stages = 0;
+  void* prof_stream = nullptr;
   // staging for fpe_evaluate_host (grown on demand, owned)
   void* st_dev = nullptr; size_t st_bytes = 0;
   void* st_streams[2] = {nullptr, nullptr};

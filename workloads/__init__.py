@@ -37,8 +37,9 @@ def seed(cfg: int, stream: int) -> int:
     return SEED_BASE + 10 * cfg + stream
 
 
-def _rng(cfg: int, stream: int) -> np.random.Generator:
-    return np.random.Generator(np.random.PCG64(seed(cfg, stream)))
+def _rng(cfg: int, stream: int, shard: int = 0) -> np.random.Generator:
+    # shard > 0: an independent batch of the same distribution (weak-scaling ranks)
+    return np.random.Generator(np.random.PCG64(seed(cfg, stream) + 1_000_003 * shard))
 
 
 def _as_complex(re: np.ndarray, im: np.ndarray) -> np.ndarray:
@@ -85,28 +86,28 @@ def sparse_coefficients(cfg: int = 4, d: int | None = None):
     return idx.astype(np.int64), a[idx]
 
 
-def sphere_points(cfg: int, n: int) -> np.ndarray:
+def sphere_points(cfg: int, n: int, shard: int = 0) -> np.ndarray:
     """n points uniform on the Riemann sphere, stereographically projected."""
-    u = _rng(cfg, 2).random(n)
+    u = _rng(cfg, 2, shard).random(n)
     u = np.where(u == 0.0, 0.5, u)  # open interval (0,1); u==0 has probability 2^-53
     r = np.sqrt(u / (1.0 - u))
-    phi = _rng(cfg, 3).uniform(0.0, 2.0 * np.pi, size=n)
+    phi = _rng(cfg, 3, shard).uniform(0.0, 2.0 * np.pi, size=n)
     return _as_complex(r * np.cos(phi), r * np.sin(phi))
 
 
-def points(cfg: int, n: int | None = None) -> np.ndarray:
+def points(cfg: int, n: int | None = None, shard: int = 0) -> np.ndarray:
     """Evaluation points of configuration ``cfg`` (complex128 or float64)."""
     c = CONFIGS[cfg]
     n = c["n_points"] if n is None else int(n)
     if cfg in (1, 3, 5):
-        return sphere_points(cfg, n)
+        return sphere_points(cfg, n, shard)
     if cfg == 2:
-        t = _rng(cfg, 2).uniform(-8.0, 8.0, size=n)
-        sgn = np.where(_rng(cfg, 3).random(n) < 0.5, -1.0, 1.0)
+        t = _rng(cfg, 2, shard).uniform(-8.0, 8.0, size=n)
+        sgn = np.where(_rng(cfg, 3, shard).random(n) < 0.5, -1.0, 1.0)
         return sgn * np.exp2(t)
     if cfg == 4:
-        t = _rng(cfg, 2).uniform(-2.0, 2.0, size=n)
-        phi = _rng(cfg, 3).uniform(0.0, 2.0 * np.pi, size=n)
+        t = _rng(cfg, 2, shard).uniform(-2.0, 2.0, size=n)
+        phi = _rng(cfg, 3, shard).uniform(0.0, 2.0 * np.pi, size=n)
         r = np.exp2(t)
         return _as_complex(r * np.cos(phi), r * np.sin(phi))
     raise KeyError(cfg)
