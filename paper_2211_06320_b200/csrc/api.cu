@@ -8,6 +8,7 @@
 #include <vector>
 #include "fpe_internal.h"
 #include "kernels.cuh"
+#include "eval_tiled.cuh"
 
 namespace fpe {
 
@@ -43,27 +44,29 @@ struct DeviceGuard {
   ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
 };
 
+// internal batch: the radix scan handles up to 2^28 points at a time
+constexpr long long kMaxBatch = 1ll << 28;
+
 static size_t ws_bytes_for(long long n) {
-  return ((size_t)n * sizeof(int2) + 255) & ~size_t(255);
+  long long b = n < kMaxBatch ? n : kMaxBatch;
+  size_t naive = ((size_t)b * sizeof(int2) + 255) & ~size_t(255);
+  size_t tiled = tiled_ws_bytes(b);
+  return naive > tiled ? naive : tiled;
 }
 
-// Records an event before the first stage and after each stage when profiling is on.
-struct Stager {
-  fpe_poly h;
-  cudaStream_t s;
-  Stager(fpe_poly h_, cudaStream_t s_) : h(h_), s(s_) {
-    h->n_stages = 0;
-    h->prof_stream = s;
-    if (h->profiling) cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[0]), s);
+Stage::Stage(fpe_poly h_, void* s_) : h(h_), stream(s_) {
+  h->n_stages = 0;
+  h->prof_stream = s_;
+  if (h->profiling) cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[0]), static_cast<cudaStream_t>(s_));
+}
+void Stage::mark(const char* name) {
+  if (h->n_stages < 15) {
+    h->stage_names[h->n_stages] = name;
+    ++h->n_stages;
+    if (h->profiling)
+      cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[h->n_stages]), static_cast<cudaStream_t>(stream));
   }
-  void done(const char* name) {
-    if (h->n_stages < 15) {
-      h->stage_names[h->n_stages] = name;
-      ++h->n_stages;
-      if (h->profiling) cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[h->n_stages]), s);
-    }
-  }
-};
+}
 
 }  // namespace fpe
 
@@ -281,12 +284,31 @@ fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t
   PolyDev P = h->view();
   int2* lr = static_cast<int2*>(workspace);
   FPE_CUDA(cudaMemsetAsync(h->dstats, 0, sizeof(unsigned long long), s));
-  Stager stg(h, s);
-  launch_classify(pt_dt, points, n_points, P, lr, diag_out, h->dstats, s);
-  stg.done("classify");
-  launch_eval_point(pt_dt, points, n_points, P, lr, values_out, reinterpret_cast<long long*>(exps_out), s);
-  stg.done("eval_point");
-  h->last_launches = 2;
+  Stage stg(h, s);
+  long long launches = 0;
+  for (long long off = 0; off < n_points; off += kMaxBatch) {
+    const long long m = std::min(kMaxBatch, n_points - off);
+    const size_t in_sz = dtype_size(pt_dt);
+    const bool cplx_out = (pt_dt == FPE_C64 || pt_dt == FPE_C32 || h->hdr.dtype == FPE_C64 || h->hdr.dtype == FPE_C32);
+    const size_t out_sz = is_f32(pt_dt) ? (cplx_out ? 8 : 4) : (cplx_out ? 16 : 8);
+    const void* pp = static_cast<const char*>(points) + off * in_sz;
+    void* vv = static_cast<char*>(values_out) + off * out_sz;
+    long long* ee = exps_out ? reinterpret_cast<long long*>(exps_out) + off : nullptr;
+    fpe_diag* dd = diag_out ? diag_out + off : nullptr;
+    if (!P.sparse) {
+      int l = run_tiled(pt_dt, pp, m, P, vv, ee, dd, workspace, h->dstats, stg, s);
+      if (l < 0) { set_error("fpe_evaluate: tiled path rejected the launch"); return FPE_ERR_INVALID_ARG; }
+      launches += l;
+    } else {
+      int2* lr = static_cast<int2*>(workspace);
+      launch_classify(pt_dt, pp, m, P, lr, dd, h->dstats, s);
+      stg.mark("classify");
+      launch_eval_point(pt_dt, pp, m, P, lr, vv, ee, s);
+      stg.mark("eval_point");
+      launches += 2;
+    }
+  }
+  h->last_launches = launches;       // kernels of this library (memsets not counted)
   FPE_CUDA(cudaGetLastError());
   return FPE_OK;
 }
@@ -300,9 +322,9 @@ fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n
   DeviceGuard g(h->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PolyDev P = h->view();
-  Stager stg(h, s);
+  Stage stg(h, s);
   launch_horner(pt_dt, points, n_points, P, values_out, reinterpret_cast<long long*>(exps_out), s);
-  stg.done("horner_full");
+  stg.mark("horner_full");
   h->last_launches = 1;
   FPE_CUDA(cudaGetLastError());
   return FPE_OK;
@@ -342,12 +364,12 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
     void* dp = base;
     void* dv = base + al(chunk * in_sz);
     long long* de = reinterpret_cast<long long*>(base + al(chunk * in_sz) + al(chunk * out_sz));
-    int2* lr = reinterpret_cast<int2*>(base + al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8));
+    void* wsp = base + al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8);
     FPE_CUDA(cudaMemcpyAsync(dp, static_cast<const char*>(points_host) + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s));
-    launch_classify(pt_dt, dp, m, P, lr, nullptr, h->dstats, s);
-    launch_eval_point(pt_dt, dp, m, P, lr, dv, exps_host ? de : nullptr, s);
-    launches += 2;
-    FPE_CUDA(cudaGetLastError());
+    fpe_status est = fpe_evaluate(h, dp, pt_dt, m, dv, exps_host ? reinterpret_cast<int64_t*>(de) : nullptr, nullptr,
+                                  wsp, ws_bytes_for(chunk), s);
+    if (est != FPE_OK) return est;
+    launches += h->last_launches;
     FPE_CUDA(cudaMemcpyAsync(static_cast<char*>(values_host) + off * out_sz, dv, m * out_sz, cudaMemcpyDeviceToHost, s));
     if (exps_host) FPE_CUDA(cudaMemcpyAsync(exps_host + off, de, m * 8, cudaMemcpyDeviceToHost, s));
   }

@@ -62,6 +62,14 @@ struct fpe_poly_s {
 
 namespace fpe {
 void set_error(const char* fmt, ...);
+
+// Per-stage CUDA-event marks on the launching stream (fpe_set_profiling).
+struct Stage {
+  fpe_poly h;
+  void* stream;
+  Stage(fpe_poly h_, void* s_);
+  void mark(const char* name);
+};
 fpe_status precondition_host(const void* coeffs_host, int64_t n, fpe_dtype dt, int32_t p_bits,
                              int32_t drop_override, std::vector<uint8_t>& flat, Header& hdr,
                              std::vector<int32_t>& hk, std::vector<int32_t>& hh);

@@ -231,15 +231,12 @@ __device__ __forceinline__ double lambda_cr(double x, double y, bool cplx, int* 
   return round_checked(lam, fabs(lam.hi) * 0x1p-96, hard);
 }
 
-// Exact sign of lambda*I + J for |I| < 2^53, |J| < 2^53 (R14):
-// lambda*I = P + E exactly (TwoProd), P + J = s + e1 exactly (TwoSum); the sign of
-// s + (e1 + E) rounded is the exact sign (see DESIGN.md for the case analysis).
+// Exact sign of lambda*I + J for integers |I|, |J| < 2^53 (R14): I and J are exact
+// doubles and the fused multiply-add evaluates lambda*I + J exactly before its single rounding,
+// and rounding to nearest preserves the sign; it cannot underflow to zero because a nonzero
+// lambda*I + J is a multiple of min(1, ulp(lambda)) >= 2^-1074.
 __device__ __forceinline__ int sign_lin(double lam, long long I, long long J) {
-  double Id = (double)I, Jd = (double)J;
-  double P = __dmul_rn(lam, Id);
-  double E = __fma_rn(lam, Id, -P);
-  dd_t s = two_sum(P, Jd);
-  double t = __dadd_rn(s.hi, __dadd_rn(s.lo, E));
+  double t = __fma_rn(lam, (double)I, (double)J);
   return (t > 0.0) - (t < 0.0);
 }
 

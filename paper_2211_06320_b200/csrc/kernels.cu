@@ -12,93 +12,10 @@
 #include <cstdint>
 #include "fpe_internal.h"
 #include "fpe_math.cuh"
+#include "device_common.cuh"
 #include "kernels.cuh"
 
 namespace fpe {
-
-// ------------------------------------------------------------------------------------------
-// point / coefficient access
-template <int PK> struct PtTraits;
-template <> struct PtTraits<FPE_R64> { static constexpr bool cplx = false; static constexpr bool f32 = false; };
-template <> struct PtTraits<FPE_C64> { static constexpr bool cplx = true; static constexpr bool f32 = false; };
-template <> struct PtTraits<FPE_R32> { static constexpr bool cplx = false; static constexpr bool f32 = true; };
-template <> struct PtTraits<FPE_C32> { static constexpr bool cplx = true; static constexpr bool f32 = true; };
-
-template <int PK>
-__device__ __forceinline__ void load_point(const void* __restrict__ p, long long i, double& x, double& y) {
-  if constexpr (PK == FPE_R64) { x = __ldg(static_cast<const double*>(p) + i); y = 0.0; }
-  else if constexpr (PK == FPE_C64) { double2 v = __ldg(static_cast<const double2*>(p) + i); x = v.x; y = v.y; }
-  else if constexpr (PK == FPE_R32) { x = (double)__ldg(static_cast<const float*>(p) + i); y = 0.0; }
-  else { float2 v = __ldg(static_cast<const float2*>(p) + i); x = (double)v.x; y = (double)v.y; }
-}
-
-// ------------------------------------------------------------------------------------------
-// classification: exact searches on the cover (fpe_math.cuh sign_lin).
-//
-// f(k) = cover(k) + lambda k - (N - D),  N = hh_i* + lambda hk_i*  (eq:defN, def:LRN).
-// At a vertex j:      f >= 0  <=>  lambda (hk_j - hk_i*) + (hh_j - hh_i* + D) >= 0
-// Inside segment s:   f >= 0  <=>  lambda (k - hk_i*) dk_s + (hh_s - hh_i* + D) dk_s + dh_s (k - hk_s) >= 0
-__device__ __forceinline__ bool band_vertex(const int2* hull, int j, int2 vs, int drop, double lam) {
-  int2 v = hull[j];
-  return sign_lin(lam, (long long)v.x - vs.x, (long long)v.y - vs.y + drop) >= 0;
-}
-__device__ __forceinline__ bool band_seg(int2 a, int2 b, int2 vs, int drop, double lam, long long k) {
-  long long dk = (long long)b.x - a.x, dh = (long long)b.y - a.y;
-  long long J = ((long long)a.y - vs.y + drop) * dk + dh * (k - a.x);
-  long long I = (k - vs.x) * dk;
-  return sign_lin(lam, I, J) >= 0;
-}
-
-__device__ __forceinline__ void classify_lambda(const int2* hull, int nv, int drop, double lam,
-                                                int& istar, int& l, int& r) {
-  if (isnan(lam)) { istar = -1; l = 0; r = -1; return; }
-  if (lam == -INFINITY) { istar = 0; l = r = hull[0].x; return; }
-  const int m = nv - 1;
-  // k_lambda: least i in [0, m) with lambda dk_i + dh_i <= 0 (slopes decreasing), else m.
-  int a = 0, b = m;
-  while (a < b) {
-    int i = (a + b) >> 1;
-    int2 v0 = hull[i], v1 = hull[i + 1];
-    if (sign_lin(lam, (long long)v1.x - v0.x, (long long)v1.y - v0.y) <= 0) b = i; else a = i + 1;
-  }
-  istar = a;
-  const int2 vs = hull[a];
-  // l: least vertex in [0, i*] inside the band, then the least integer in the segment before it.
-  a = 0; b = istar;
-  while (a < b) { int j = (a + b) >> 1; if (band_vertex(hull, j, vs, drop, lam)) b = j; else a = j + 1; }
-  if (a == 0) {
-    l = hull[0].x;
-  } else {
-    int2 A = hull[a - 1], B = hull[a];
-    long long lo = A.x + 1, hi = B.x;   // f(A) < 0 <= f(B)
-    while (lo < hi) { long long k = (lo + hi) >> 1; if (band_seg(A, B, vs, drop, lam, k)) hi = k; else lo = k + 1; }
-    l = (int)lo;
-  }
-  // r: greatest vertex in [i*, m] inside the band, then the greatest integer in the segment after it.
-  a = istar; b = m;
-  while (a < b) { int j = (a + b + 1) >> 1; if (band_vertex(hull, j, vs, drop, lam)) a = j; else b = j - 1; }
-  if (a == m) {
-    r = hull[m].x;
-  } else {
-    int2 A = hull[a], B = hull[a + 1];
-    long long lo = A.x, hi = B.x - 1;   // f(A) >= 0 > f(B)
-    while (lo < hi) { long long k = (lo + hi + 1) >> 1; if (band_seg(A, B, vs, drop, lam, k)) lo = k; else hi = k - 1; }
-    r = (int)lo;
-  }
-}
-
-__device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ a, int n, int key) {
-  int lo = 0, hi = n;
-  while (lo < hi) { int m = (lo + hi) >> 1; if (__ldg(a + m) < key) lo = m + 1; else hi = m; }
-  return lo;
-}
-
-__device__ __forceinline__ int kept_count(const PolyDev& P, int l, int r) {
-  if (r < l) return 0;
-  if (P.sparse) return lower_bound_i32(P.sidx, (int)P.n_good, r + 1) - lower_bound_i32(P.sidx, (int)P.n_good, l);
-  if (P.all_good) return r - l + 1;
-  return __ldg(P.prefix + (r + 1 - P.k_min)) - __ldg(P.prefix + (l - P.k_min));
-}
 
 template <int PK>
 __global__ void __launch_bounds__(256) k_classify(const void* __restrict__ pts, long long n, PolyDev P,
@@ -126,84 +43,6 @@ __global__ void __launch_bounds__(256) k_classify(const void* __restrict__ pts, 
       diag[i] = d;
     }
     if (hard) atomicAdd(hard_ctr, 1ull);
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// output: mantissa normalised to max(|re|,|im|) in [1/2, 1), exponent int64
-template <int OK>   // output kind = fpe_dtype of the values
-__device__ __forceinline__ void store_value(void* __restrict__ vals, long long* __restrict__ exps, long long i,
-                                            double re, double im, long long E) {
-  double m = fmax(fabs(re), fabs(im));
-  if (m == 0.0 || !isfinite(m)) {
-    E = 0;
-  } else {
-    int e = frexp_exp(m);
-    re = ldexp(re, -e); im = ldexp(im, -e);
-    E += e;
-  }
-  if (!exps) {   // plain floats: value * 2^E, saturating
-    int Ec = (int)max(-4000ll, min(4000ll, E));
-    re = ldexp(re, Ec); im = ldexp(im, Ec);
-  } else {
-    exps[i] = E;
-  }
-  if constexpr (OK == FPE_R64) static_cast<double*>(vals)[i] = re;
-  else if constexpr (OK == FPE_C64) static_cast<double2*>(vals)[i] = make_double2(re, im);
-  else if constexpr (OK == FPE_R32) static_cast<float*>(vals)[i] = (float)re;
-  else static_cast<float2*>(vals)[i] = make_float2((float)re, (float)im);
-}
-
-template <int CK> struct Coef;
-template <int CK> __device__ void a0_value(const PolyDev& P, double& re, double& im);
-template <> struct Coef<FPE_C64> {
-  using T = double2;
-  __device__ static void get(const void* c, long long k, double& re, double& im) {
-    double2 v = __ldg(static_cast<const double2*>(c) + k); re = v.x; im = v.y;
-  }
-};
-template <> struct Coef<FPE_R64> {
-  using T = double;
-  __device__ static void get(const void* c, long long k, double& re, double& im) {
-    re = __ldg(static_cast<const double*>(c) + k); im = 0.0;
-  }
-};
-template <> struct Coef<FPE_C32> {
-  using T = float2;
-  __device__ static void get(const void* c, long long k, float& re, float& im) {
-    float2 v = __ldg(static_cast<const float2*>(c) + k); re = v.x; im = v.y;
-  }
-};
-template <> struct Coef<FPE_R32> {
-  using T = float;
-  __device__ static void get(const void* c, long long k, float& re, float& im) {
-    re = __ldg(static_cast<const float*>(c) + k); im = 0.0f;
-  }
-};
-
-// a_0 2^-shift (0 if a_0 = 0): the value at z = 0 (the lambda -> -inf limit).
-template <int CK> __device__ void a0_value(const PolyDev& P, double& re, double& im) {
-  re = 0.0; im = 0.0;
-  if (P.k_min != 0) return;
-  if (P.sparse && __ldg(P.sidx) != 0) return;
-  if constexpr (PtTraits<CK>::f32) { float a, b; Coef<CK>::get(P.coef, 0, a, b); re = a; im = b; }
-  else Coef<CK>::get(P.coef, 0, re, im);
-}
-
-// Q = b * z^n with b in the working precision and z^n extended (fpe_math.cuh xc_pow).
-template <bool CPLX>
-__device__ __forceinline__ void times_zpow(double br, double bi, double x, double y, long long n,
-                                           double& qr, double& qi, long long& E) {
-  if constexpr (CPLX) {
-    xc_t zp = xc_pow(x, y, n);
-    qr = __fma_rn(br, zp.hr, __fma_rn(-bi, zp.hi, __fma_rn(br, zp.er, -bi * zp.ei)));
-    qi = __fma_rn(br, zp.hi, __fma_rn(bi, zp.hr, __fma_rn(br, zp.ei, bi * zp.er)));
-    E = zp.E;
-  } else {
-    xr_t zp = xr_pow(x, n);
-    qr = __fma_rn(br, zp.h, br * zp.e);
-    qi = 0.0;
-    E = zp.E;
   }
 }
 

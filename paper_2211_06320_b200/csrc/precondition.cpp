@@ -137,13 +137,14 @@ fpe_status precondition_host(const void* coeffs, int64_t n, fpe_dtype dt, int32_
   // 5. flat buffer
   const size_t csz = f32 ? (cplx ? 8 : 4) : (cplx ? 16 : 8);
   const int64_t n_coef = sparse ? n_good : d_eff + 1;
+  const int64_t n_coef_alloc = sparse ? n_coef : (n_coef + 127) / 128 * 128;   // TMA chunks (kChunk) read whole
   std::memset(&hdr, 0, sizeof(hdr));
   hdr.magic = kMagic; hdr.version = kVersion; hdr.dtype = dt;
   hdr.n_coeffs = n; hdr.k_min = k_min; hdr.k_max = k_max; hdr.n_hull = nv; hdr.n_good = n_good;
   hdr.p = p; hdr.drop = drop; hdr.shift = shift; hdr.sparse = sparse; hdr.all_good = all_good;
   size_t off = align256(sizeof(Header));
   hdr.off_hull = off; off = align256(off + nv * sizeof(int2));
-  hdr.off_coef = off; off = align256(off + n_coef * csz);
+  hdr.off_coef = off; off = align256(off + n_coef_alloc * csz);
   hdr.off_prefix = 0;
   if (!sparse && !all_good) { hdr.off_prefix = off; off = align256(off + (d_eff + 2) * sizeof(int32_t)); }
   hdr.off_sidx = 0;

@@ -1,0 +1,155 @@
+// sort.cu -- work bucketing (north star subsystem 3).
+//
+// Points carry a 24-bit key that is monotone in lambda (bits 0..22) with bit 23 = "long window";
+// l and r are both non-decreasing in lambda, so points with close keys have nested, nearly equal
+// windows.  Two levels:
+//   global  : one counting-sort scatter by the top kCoarseBits of the key (4096 coarse buckets).
+//             k_classify_bucket (eval_tiled.cu) builds a per-CTA histogram in shared memory and
+//             claims each CTA's slice of every bucket with one global atomicAdd per nonzero bin;
+//             k_bucket_scan turns bucket totals into starts and enumerates work items (chunks of at
+//             most kChunkPts points of one bucket, long buckets first); k_bucket_scatter writes the
+//             permutation (contiguous runs per (CTA, bucket), so L2 merges the partial sectors).
+//   local   : the evaluator sorts each chunk by the remaining low bits in shared memory
+//             (counting sort) before cutting it into warp groups of 32.
+// Order inside a (CTA, bucket) run and inside equal keys is unspecified; every point's arithmetic
+// depends only on its own window, so results do not depend on it (bitwise).
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "sort.cuh"
+
+namespace fpe {
+
+__global__ void __launch_bounds__(1024) k_bucket_scan(const uint32_t* __restrict__ gcount,
+                                                      uint32_t* __restrict__ bstart,
+                                                      uint32_t* __restrict__ istart) {
+  // kBuckets = 4096 = 1024 threads x 4
+  __shared__ uint32_t ws[32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  uint32_t c[4], ch[4];
+  uint32_t s = 0, sc = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    c[j] = gcount[t * 4 + j];
+    s += c[j];
+  }
+  // item order: long buckets (top half) first -> position b' holds bucket (b' + half) % kBuckets
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t b = (uint32_t)((t * 4 + j + kBuckets / 2) % kBuckets);
+    ch[j] = (gcount[b] + kChunkPts - 1) / kChunkPts;
+    sc += ch[j];
+  }
+  // two block scans (bucket starts, item starts)
+  uint32_t v[2] = {s, sc}, ex[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    uint32_t x = v[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t z = ws[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += y;
+      }
+      ws[lane] = z;
+    }
+    __syncthreads();
+    ex[q] = (wid ? ws[wid - 1] : 0) + x - v[q];
+    if (q == 1 && t == 1023) istart[kBuckets] = ws[31];
+    __syncthreads();
+  }
+  uint32_t run = ex[0], runi = ex[1];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    bstart[t * 4 + j] = run;
+    run += c[j];
+    istart[t * 4 + j] = runi;
+    runi += ch[j];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restrict__ keys, long long n,
+                                                        const uint32_t* __restrict__ bstart,
+                                                        const uint32_t* __restrict__ cta_base,
+                                                        uint32_t* __restrict__ perm) {
+  __shared__ uint32_t cnt[kBuckets];
+  __shared__ uint32_t base[kBuckets];
+  for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) {
+    cnt[b] = 0;
+    base[b] = bstart[b] + cta_base[(size_t)blockIdx.x * kBuckets + b];
+  }
+  __syncthreads();
+  const long long beg = (long long)blockIdx.x * kPtsPerCta;
+  const long long end = min(n, beg + kPtsPerCta);
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    const uint32_t c = __ldg(keys + i) >> (24 - kCoarseBits);
+    const uint32_t r = atomicAdd(&cnt[c], 1u);
+    perm[base[c] + r] = (uint32_t)i;
+  }
+}
+
+// In-place counting sort of every chunk of the permutation by key bits [1, 1 + kLocalBits).
+__global__ void __launch_bounds__(256) k_chunk_sort(const uint32_t* __restrict__ keys, uint32_t* __restrict__ perm,
+                                                    const uint32_t* __restrict__ gcount,
+                                                    const uint32_t* __restrict__ bstart,
+                                                    const uint32_t* __restrict__ istart) {
+  __shared__ uint32_t hist[1 << kLocalBits];
+  __shared__ uint32_t sorted[kChunkPts];
+  const int c = blockIdx.x;
+  if (c >= (int)istart[kBuckets]) return;
+  int bucket, npts;
+  uint32_t p0;
+  chunk_of(istart, gcount, bstart, c, bucket, p0, npts);
+  for (int b = threadIdx.x; b < (1 << kLocalBits); b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  constexpr int kPer = kChunkPts / 256;
+  uint32_t my_idx[kPer], my_bin[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int j = threadIdx.x + q * 256;
+    my_idx[q] = 0; my_bin[q] = 0;
+    if (j < npts) {
+      my_idx[q] = perm[p0 + j];
+      my_bin[q] = (__ldg(keys + my_idx[q]) >> 1) & ((1u << kLocalBits) - 1);
+      atomicAdd(&hist[my_bin[q]], 1u);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {   // exclusive scan of the bins (2048 = 32 lanes x 64)
+    const int lane = threadIdx.x;
+    constexpr int kB = (1 << kLocalBits) / 32;
+    uint32_t run = 0;
+    for (int j = 0; j < kB; ++j) run += hist[lane * kB + j];
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { uint32_t y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+    uint32_t off = x - run;
+    for (int j = 0; j < kB; ++j) { uint32_t v = hist[lane * kB + j]; hist[lane * kB + j] = off; off += v; }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int j = threadIdx.x + q * 256;
+    if (j < npts) sorted[atomicAdd(&hist[my_bin[q]], 1u)] = my_idx[q];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < npts; j += 256) perm[p0 + j] = sorted[j];
+}
+
+void bucket_finish(const uint32_t* keys, long long n, const uint32_t* gcount, const uint32_t* cta_base,
+                   uint32_t* bstart, uint32_t* istart, uint32_t* perm, cudaStream_t s) {
+  k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, istart);
+  const int ctas = (int)((n + kPtsPerCta - 1) / kPtsPerCta);
+  k_bucket_scatter<<<ctas, 256, 0, s>>>(keys, n, bstart, cta_base, perm);
+  const int max_chunks = (int)((n + kChunkPts - 1) / kChunkPts) + kBuckets;
+  k_chunk_sort<<<max_chunks, 256, 0, s>>>(keys, perm, gcount, bstart, istart);
+}
+
+}  // namespace fpe
