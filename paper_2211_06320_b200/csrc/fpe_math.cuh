@@ -8,65 +8,66 @@
 //  * z^n in extended range with compensated (dd-accurate) binary powering
 //    ("compute z^l in 2 log2 l steps").
 //
-// All exactness-critical products/sums use __dmul_rn/__dadd_rn so that nvcc's
+// All exactness-critical products/sums use fpe_mul/fpe_add so that nvcc's
 // FMA contraction cannot change them.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "log_table.h"
+#include "fpe_hd.cuh"
 
 namespace fpe {
 
 struct dd_t { double hi, lo; };
 
-__device__ __forceinline__ dd_t two_sum(double a, double b) {
-  double s = __dadd_rn(a, b);
-  double bb = __dsub_rn(s, a);
-  double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+FPE_HD dd_t two_sum(double a, double b) {
+  double s = fpe_add(a, b);
+  double bb = fpe_sub(s, a);
+  double e = fpe_add(fpe_sub(a, fpe_sub(s, bb)), fpe_sub(b, bb));
   return {s, e};
 }
-__device__ __forceinline__ dd_t fast_two_sum(double a, double b) {  // |a| >= |b| or a == 0
-  double s = __dadd_rn(a, b);
-  return {s, __dsub_rn(b, __dsub_rn(s, a))};
+FPE_HD dd_t fast_two_sum(double a, double b) {  // |a| >= |b| or a == 0
+  double s = fpe_add(a, b);
+  return {s, fpe_sub(b, fpe_sub(s, a))};
 }
-__device__ __forceinline__ dd_t two_prod(double a, double b) {
-  double p = __dmul_rn(a, b);
-  return {p, __fma_rn(a, b, -p)};
+FPE_HD dd_t two_prod(double a, double b) {
+  double p = fpe_mul(a, b);
+  return {p, fpe_fma(a, b, -p)};
 }
-__device__ __forceinline__ dd_t dd_add(dd_t a, dd_t b) {
+FPE_HD dd_t dd_add(dd_t a, dd_t b) {
   dd_t s = two_sum(a.hi, b.hi);
   dd_t t = two_sum(a.lo, b.lo);
-  s.lo = __dadd_rn(s.lo, t.hi);
+  s.lo = fpe_add(s.lo, t.hi);
   s = fast_two_sum(s.hi, s.lo);
-  s.lo = __dadd_rn(s.lo, t.lo);
+  s.lo = fpe_add(s.lo, t.lo);
   return fast_two_sum(s.hi, s.lo);
 }
-__device__ __forceinline__ dd_t dd_mul(dd_t a, dd_t b) {
+FPE_HD dd_t dd_mul(dd_t a, dd_t b) {
   dd_t p = two_prod(a.hi, b.hi);
-  p.lo = __fma_rn(a.hi, b.lo, __fma_rn(a.lo, b.hi, p.lo));
+  p.lo = fpe_fma(a.hi, b.lo, fpe_fma(a.lo, b.hi, p.lo));
   return fast_two_sum(p.hi, p.lo);
 }
-__device__ __forceinline__ dd_t dd_mul_d(dd_t a, double b) {
+FPE_HD dd_t dd_mul_d(dd_t a, double b) {
   dd_t p = two_prod(a.hi, b);
-  p.lo = __fma_rn(a.lo, b, p.lo);
+  p.lo = fpe_fma(a.lo, b, p.lo);
   return fast_two_sum(p.hi, p.lo);
 }
-__device__ __forceinline__ dd_t dd_div(dd_t a, dd_t b) {
-  double q1 = __ddiv_rn(a.hi, b.hi);
+FPE_HD dd_t dd_div(dd_t a, dd_t b) {
+  double q1 = fpe_div(a.hi, b.hi);
   dd_t r = dd_add(a, dd_mul_d(b, -q1));
-  double q2 = __ddiv_rn(r.hi, b.hi);
+  double q2 = fpe_div(r.hi, b.hi);
   r = dd_add(r, dd_mul_d(b, -q2));
-  double q3 = __ddiv_rn(r.hi, b.hi);
+  double q3 = fpe_div(r.hi, b.hi);
   dd_t q = fast_two_sum(q1, q2);
   return dd_add(q, dd_t{q3, 0.0});
 }
 
 // 2^e as a double for -1022 <= e <= 1023.
-__device__ __forceinline__ double pow2i(int e) {
-  return __longlong_as_double((long long)(e + 1023) << 52);
+FPE_HD double pow2i(int e) {
+  return fpe_bits2d((long long)(e + 1023) << 52);
 }
 // Exponent e with |x| = m 2^e, m in [1/2, 1), for finite nonzero normal or subnormal x.
-__device__ __forceinline__ int frexp_exp(double x) {
+FPE_HD int frexp_exp(double x) {
   int e;
   (void)frexp(x, &e);
   return e;
@@ -82,12 +83,12 @@ __device__ __forceinline__ int frexp_exp(double x) {
 
 // log1p(u) for |u| <= 2^-7.9, relative error ~2^-104:
 // log1p(u) = 2 atanh(s), s = u/(2+u) = 2s (1 + s^2/3 + s^4/5 + ... + s^12/13).
-__device__ __forceinline__ dd_t log1p_small(dd_t u) {
+FPE_HD dd_t log1p_small(dd_t u) {
   if (u.hi == 0.0) return dd_t{0.0, 0.0};
   dd_t s = dd_div(u, dd_add(dd_t{2.0, 0.0}, u));
   dd_t s2 = dd_mul(s, s);
   double x = s2.hi;
-  double b7 = __fma_rn(x, __fma_rn(x, __fma_rn(x, 1.0 / 13.0, 1.0 / 11.0), 1.0 / 9.0), 1.0 / 7.0);
+  double b7 = fpe_fma(x, fpe_fma(x, fpe_fma(x, 1.0 / 13.0, 1.0 / 11.0), 1.0 / 9.0), 1.0 / 7.0);
   dd_t b5 = dd_add(dd_t{FPE_FIFTH_HI, FPE_FIFTH_LO}, dd_mul_d(s2, b7));
   dd_t b3 = dd_add(dd_t{FPE_THIRD_HI, FPE_THIRD_LO}, dd_mul(s2, b5));
   dd_t R = dd_mul(s2, b3);
@@ -98,23 +99,23 @@ __device__ __forceinline__ dd_t log1p_small(dd_t u) {
 // log2 of w = (whi + wlo), w in (0, inf) finite; returns (j, frac) with
 // log2 w = j + frac*(1/ln2) where frac = ln f is returned as dd and f = w 2^-j in [0.703, 1.414).
 // Table-driven: f r_i = 1 + u, ln f = log1p(u) - ln r_i.
-__device__ __forceinline__ dd_t ln_reduced(double whi, double wlo, int* j_out) {
+FPE_HD dd_t ln_reduced(double whi, double wlo, int* j_out) {
   int j = frexp_exp(whi);
   double f = ldexp(whi, -j);                 // [1/2, 1)
   if (f < FPE_LOGTAB_F0) { f *= 2.0; j -= 1; }
   double flo = ldexp(wlo, -j);
-  int i = __double2int_rn((f - FPE_LOGTAB_F0) * 256.0);
+  int i = fpe_d2i_rn((f - FPE_LOGTAB_F0) * 256.0);
   i = max(0, min(i, FPE_LOGTAB_N - 1));
-  double r = __ldg(&fpe_logtab[i][0]);
-  dd_t L0 = dd_t{__ldg(&fpe_logtab[i][1]), __ldg(&fpe_logtab[i][2])};
+  double r = fpe_logtab(i, 0);
+  dd_t L0 = dd_t{fpe_logtab(i, 1), fpe_logtab(i, 2)};
   dd_t p = two_prod(f, r);
-  dd_t u = fast_two_sum(__dsub_rn(p.hi, 1.0), __fma_rn(flo, r, p.lo));  // p.hi - 1 exact (Sterbenz)
+  dd_t u = fast_two_sum(fpe_sub(p.hi, 1.0), fpe_fma(flo, r, p.lo));  // p.hi - 1 exact (Sterbenz)
   *j_out = j;
   return dd_add(log1p_small(u), L0);
 }
 
 // Exact sum of five doubles as a dd (grow-expansion then compression).
-__device__ __forceinline__ dd_t exact_sum5(double t0, double t1, double t2, double t3, double t4) {
+FPE_HD dd_t exact_sum5(double t0, double t1, double t2, double t3, double t4) {
   double h[5];
   h[0] = t0;
   double in[4] = {t1, t2, t3, t4};
@@ -134,14 +135,14 @@ __device__ __forceinline__ dd_t exact_sum5(double t0, double t1, double t2, doub
   for (int i = 3; i >= 0; --i) {
     dd_t s = two_sum(hi, h[i]);
     hi = s.hi;
-    lo = __dadd_rn(lo, s.lo);
+    lo = fpe_add(lo, s.lo);
   }
   return fast_two_sum(hi, lo);
 }
 
 // Round hi+lo (a normalised dd, |lo| <= ulp(hi)/2) to fp64; flag when within tol of a
 // rounding boundary (midpoint between consecutive doubles).
-__device__ __forceinline__ double round_checked(dd_t v, double tol, int* hard) {
+FPE_HD double round_checked(dd_t v, double tol, int* hard) {
   double h = v.hi;
   if (h == 0.0) return v.lo;  // only arises when the value is exactly representable
   int e = frexp_exp(h);              // |h| in [2^(e-1), 2^e)
@@ -158,17 +159,17 @@ __device__ __forceinline__ double round_checked(dd_t v, double tol, int* hard) {
 // lambda = RN64(log2|z|) for z = x + iy (complex) or x (real, y ignored).
 // Returns -inf for z = 0 and NaN for non-finite z; *hard set on a Ziv failure
 // (|true - boundary| < 2^-96 |lambda|; expected never, R4).
-__device__ __forceinline__ double lambda_cr(double x, double y, bool cplx, int* hard) {
+FPE_HD double lambda_cr(double x, double y, bool cplx, int* hard) {
   *hard = 0;
   if (!cplx) y = 0.0;
-  if (!isfinite(x) || !isfinite(y)) return __longlong_as_double(0x7ff8000000000000LL);
+  if (!isfinite(x) || !isfinite(y)) return fpe_bits2d(0x7ff8000000000000LL);
   double ax = fabs(x), ay = fabs(y);
   if (ay > ax) { double t = ax; ax = ay; ay = t; }
   if (ax == 0.0) return -INFINITY;
   const dd_t INV_LN2 = {FPE_INV_LN2_HI, FPE_INV_LN2_LO};
   dd_t lam;
   if (ay == 0.0) {                                   // |z| = ax
-    double t = __dsub_rn(ax, 1.0);
+    double t = fpe_sub(ax, 1.0);
     if (ax >= 0.5 && ax <= 2.0 && fabs(t) <= 0x1p-8) {   // t exact (Sterbenz); relative accuracy near 1
       lam = dd_mul(log1p_small(dd_t{t, 0.0}), INV_LN2);
     } else {
@@ -177,7 +178,7 @@ __device__ __forceinline__ double lambda_cr(double x, double y, bool cplx, int* 
       lam = dd_add(dd_t{(double)j, 0.0}, dd_mul(L, INV_LN2));
     }
   } else {
-    double v = __fma_rn(ax, ax, ay * ay);
+    double v = fpe_fma(ax, ax, ay * ay);
     if (v >= 0.5 && v <= 2.0) {                      // near |z| = 1: t = x^2 + y^2 - 1 exactly
       if (ay < 0x1p-480) {
         if (ax == 1.0) {
@@ -196,7 +197,7 @@ __device__ __forceinline__ double lambda_cr(double x, double y, bool cplx, int* 
           }
           double A = ldexp(L.hi, 1074 + sc), B = ldexp(L.lo, 1074 + sc);
           double n = rint(A);
-          double fr = __dadd_rn(__dsub_rn(A, n), B);
+          double fr = fpe_add(fpe_sub(A, n), B);
           if (fr > 0.5) n += 1.0; else if (fr < -0.5) n -= 1.0;
           if (fabs(fabs(fr) - 0.5) < 0x1p-40) *hard = 1;
           return ldexp(n, -1074);
@@ -235,8 +236,8 @@ __device__ __forceinline__ double lambda_cr(double x, double y, bool cplx, int* 
 // doubles and the fused multiply-add evaluates lambda*I + J exactly before its single rounding,
 // and rounding to nearest preserves the sign; it cannot underflow to zero because a nonzero
 // lambda*I + J is a multiple of min(1, ulp(lambda)) >= 2^-1074.
-__device__ __forceinline__ int sign_lin(double lam, long long I, long long J) {
-  double t = __fma_rn(lam, (double)I, (double)J);
+FPE_HD int sign_lin(double lam, long long I, long long J) {
+  double t = fpe_fma(lam, (double)I, (double)J);
   return (t > 0.0) - (t < 0.0);
 }
 
@@ -244,7 +245,7 @@ __device__ __forceinline__ int sign_lin(double lam, long long I, long long J) {
 // Extended-range complex value (h + e) 2^E: h the fp64 approximation, e its error term.
 struct xc_t { double hr, hi, er, ei; long long E; };
 
-__device__ __forceinline__ void xc_renorm(xc_t& v) {
+FPE_HD void xc_renorm(xc_t& v) {
   dd_t r = two_sum(v.hr, v.er), i = two_sum(v.hi, v.ei);   // keep |e| <= ulp(h)/2
   v.hr = r.hi; v.er = r.lo; v.hi = i.hi; v.ei = i.lo;
   double m = fmax(fabs(v.hr), fabs(v.hi));
@@ -256,42 +257,42 @@ __device__ __forceinline__ void xc_renorm(xc_t& v) {
 }
 
 // (h+e)^2 with the products of h exact (TwoProd) and the error propagated to first order.
-__device__ __forceinline__ void xc_sqr(xc_t& v) {
+FPE_HD void xc_sqr(xc_t& v) {
   double a = v.hr, b = v.hi, c = v.er, d = v.ei;
   dd_t p1 = two_prod(a, a), p2 = two_prod(b, b);
   dd_t sr = two_sum(p1.hi, -p2.hi);
   double re_err = sr.lo + (p1.lo - p2.lo);
   double a2 = a + a;
   dd_t p3 = two_prod(a2, b);
-  double xr = 2.0 * __fma_rn(a, c, -b * d);
-  double xi = 2.0 * __fma_rn(a, d, b * c);
+  double xr = 2.0 * fpe_fma(a, c, -b * d);
+  double xi = 2.0 * fpe_fma(a, d, b * c);
   v.hr = sr.hi; v.hi = p3.hi;
   v.er = re_err + xr; v.ei = p3.lo + xi;
   v.E *= 2;                               // (h 2^E)^2 = h^2 2^(2E)
 }
 
 // (h+e) * w for an exact w = u + iv.
-__device__ __forceinline__ void xc_mul_exact(xc_t& v, double u, double w) {
+FPE_HD void xc_mul_exact(xc_t& v, double u, double w) {
   double a = v.hr, b = v.hi, c = v.er, d = v.ei;
   dd_t p1 = two_prod(a, u), p2 = two_prod(b, w);
   dd_t sr = two_sum(p1.hi, -p2.hi);
   dd_t p3 = two_prod(a, w), p4 = two_prod(b, u);
   dd_t si = two_sum(p3.hi, p4.hi);
   v.hr = sr.hi; v.hi = si.hi;
-  v.er = sr.lo + (p1.lo - p2.lo) + __fma_rn(c, u, -d * w);
-  v.ei = si.lo + (p3.lo + p4.lo) + __fma_rn(c, w, d * u);
+  v.er = sr.lo + (p1.lo - p2.lo) + fpe_fma(c, u, -d * w);
+  v.ei = si.lo + (p3.lo + p4.lo) + fpe_fma(c, w, d * u);
 }
 
 // z^n (n >= 0) for finite nonzero z = x + iy, relative error ~ n 2^-104 + 2^-53.
 // Left-to-right binary powering on w = z 2^-ez (|w| in [1/2, sqrt 2)).
-__device__ __forceinline__ xc_t xc_pow(double x, double y, long long n) {
+FPE_HD xc_t xc_pow(double x, double y, long long n) {
   xc_t v;
   v.hr = 1.0; v.hi = 0.0; v.er = 0.0; v.ei = 0.0; v.E = 0;
   if (n <= 0) return v;
   int ez = frexp_exp(fmax(fabs(x), fabs(y)));
   double u = ldexp(x, -ez), w = ldexp(y, -ez);
   v.hr = u; v.hi = w;
-  int top = 63 - __clzll(n);
+  int top = 63 - fpe_clzll(n);
   for (int b = top - 1; b >= 0; --b) {
     xc_sqr(v);
     if ((n >> b) & 1) xc_mul_exact(v, u, w);
@@ -303,13 +304,13 @@ __device__ __forceinline__ xc_t xc_pow(double x, double y, long long n) {
 
 // Real version: x^n for finite nonzero real x.
 struct xr_t { double h, e; long long E; };
-__device__ __forceinline__ xr_t xr_pow(double x, long long n) {
+FPE_HD xr_t xr_pow(double x, long long n) {
   xr_t v{1.0, 0.0, 0};
   if (n <= 0) return v;
   int ex = frexp_exp(x);
   double u = ldexp(x, -ex);
   v.h = u;
-  int top = 63 - __clzll(n);
+  int top = 63 - fpe_clzll(n);
   for (int b = top - 1; b >= 0; --b) {
     dd_t p = two_prod(v.h, v.h);
     double e = p.lo + 2.0 * v.h * v.e;
