@@ -1,26 +1,30 @@
 // eval_tiled.cu -- the bucketed, shared-memory-tiled window evaluator (north star subsystems 2-4).
 //
 // Pipeline (all on the caller's stream, no host round trip):
-//   k_classify_bucket lines 5-8 of FPE_p per point (lambda, k_lambda, [l, r]; device_common.cuh) and
-//                    a 24-bit key: bit 23 = "long window" (r - l + 1 > kSegLen), bits 0..22 monotone
-//                    in lambda; per-CTA coarse-bucket histogram and slice claims (sort.cu).  l and r
-//                    are both non-decreasing in lambda (d/dlambda of cover(k) + lambda k - N is
-//                    k - k_lambda), so points with close keys have nested, nearly equal windows.
-//   bucket scan/scatter (sort.cu) -> permutation grouped by coarse bucket, item table.
-//   k_eval_tiled     persistent; items = chunks of one bucket, sorted in shared memory, then:
-//     long group  = 32 consecutive long-window points, one CTA (8 warps): the union window is cut at
-//                   ABSOLUTE multiples of kSegLen (a point's arithmetic depends only on its own window,
-//                   so results stay bitwise independent of the batch); warp w evaluates segment t and
-//                   the CTA combines the per-segment Horner partials top-down with dd-accurate powers
-//                   z^gap (PAPER.md:1621-1622, 2171-2177 generalised to segment gaps).
-//     short group = 32 consecutive short-window points, one warp, the whole union window.
-//   Coefficients are streamed per warp through a 4-stage shared-memory ring filled by 1-D TMA bulk
-//   copies (cp.async.bulk + mbarrier complete_tx) and read as warp-uniform broadcasts; lanes run a
-//   predicated Horner step (fp64 / fp32 FMA) only inside their own window (exact Q_lambda, eq:reducedQlambda).
+//   k_classify_bucket lines 5-8 of FPE_p per point (lambda = RN(log2|z|) via lambda_fast, k_lambda,
+//                    [l, r]; device_common.cuh) and a 24-bit key: bit 23 = "long window"
+//                    (r - l + 1 > kLongWin), bits 0..22 monotone in lambda; per-CTA coarse-bucket
+//                    histogram and slice claims (sort.cu).  l and r are both non-decreasing in lambda
+//                    (d/dlambda of cover(k) + lambda k - N is k - k_lambda), so points with close keys
+//                    have nested, nearly equal windows.
+//   bucket scan/scatter + k_chunk_sort + k_plan (sort.cu): permutation sorted by key (bits 1..23), cut
+//                    into groups of 32*NP consecutive points; per group the union window and the work
+//                    items (one whole group, or one item per kPiece-aligned piece of a long window).
+//   k_eval_tiled     persistent warps.  A warp streams the coefficients of its item's range through a
+//                    private 3-stage shared-memory ring filled by 1-D TMA bulk copies (cp.async.bulk +
+//                    mbarrier complete_tx), reads them as warp-uniform broadcasts (one LDS per
+//                    coefficient for NP points per lane) and runs NP independent Horner chains per lane
+//                    (fp64 / fp32 FMA), masked only at the ragged ends of the windows (exact Q_lambda,
+//                    eq:reducedQlambda).  Windows are cut at absolute multiples of kPiece and the piece
+//                    partials are folded top-down with z^kPiece (compensated powering) and z^gap /
+//                    z^l (polar route, fpe_polar.cuh) -- every point's arithmetic depends only on its
+//                    own window, so results are bitwise independent of the batch and of whether its
+//                    pieces were evaluated by one warp or in parallel (scratch + last-arriver fold).
 #include <cuda_runtime.h>
 #include <cstdint>
 #include "fpe_internal.h"
 #include "fpe_math.cuh"
+#include "fpe_polar.cuh"
 #include "device_common.cuh"
 #include "sort.cuh"
 #include "eval_tiled.cuh"
@@ -29,13 +33,12 @@
 namespace fpe {
 
 constexpr int kWarps = 8;      // warps per CTA of k_eval_tiled
-constexpr int kStages = 4;     // TMA ring depth per warp
-constexpr int kMergeGap = 256; // short-group windows closer than this share one streamed interval
+constexpr int kStages = 3;     // TMA ring depth per warp
 
 // ------------------------------------------------------------------------------------------------
 // classification + sort key + first radix upsweep
 __device__ __forceinline__ uint32_t lambda_key(double lam, int l, int r) {
-  uint32_t longw = (r - l + 1 > kSegLen) ? 1u : 0u;
+  uint32_t longw = (r - l + 1 > kLongWin) ? 1u : 0u;
   uint32_t u;
   if (!(lam == lam) || lam == -INFINITY) {
     u = 0;
@@ -75,7 +78,7 @@ __global__ void __launch_bounds__(256) k_classify_bucket(const void* __restrict_
     double x, y;
     load_point<PK>(pts, i, x, y);
     int hard;
-    double lam = lambda_cr(x, y, PtTraits<PK>::cplx, &hard);
+    double lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
     int istar, l, r;
     classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
     lr[i] = make_int2(l, r);
@@ -170,63 +173,128 @@ __device__ __forceinline__ void horner_step(typename Step<CK>::W& br, typename S
   else Step<CK>::template apply_t<CPLX>(br, bi, zr, zi, a);
 }
 
-template <int CK>
-struct WarpRing {
+template <int CK> struct Ring {
   using CT = typename Step<CK>::CT;
-  CT* buf;            // kStages * kChunk
-  uint64_t* bar;      // kStages
+  CT* buf;            // kStages * kChunk coefficients of this warp
+  uint64_t* bar;      // kStages mbarriers
   const CT* coef;     // padded dense coefficient array (relative to k_min)
-  uint32_t g;         // chunks consumed so far by this warp (uniform)
+  uint32_t g;         // chunks consumed (warp-uniform)
+  uint32_t gi;        // chunks issued (warp-uniform)
+  int q_next, q_end;  // next chunk to issue (descending) and the last chunk of the current range
 };
 
 template <int CK>
-__device__ __forceinline__ void ring_issue(WarpRing<CK>& R, uint32_t g, int q) {
+__device__ __forceinline__ void ring_issue_n(Ring<CK>& R, int n) {
   using CT = typename Step<CK>::CT;
-  const int s = g % kStages;
-  fence_proxy_async();
-  mbar_expect_tx(R.bar + s, kChunk * sizeof(CT));
-  tma_load_1d(R.buf + s * kChunk, R.coef + (size_t)q * kChunk, kChunk * sizeof(CT), R.bar + s);
+  if ((threadIdx.x & 31) == 0) {
+    for (int i = 0; i < n; ++i) {
+      const int s = (int)((R.gi + i) % kStages);
+      fence_proxy_async();
+      mbar_expect_tx(R.bar + s, kChunk * sizeof(CT));
+      tma_load_1d(R.buf + s * kChunk, R.coef + (size_t)(R.q_next - i) * kChunk, kChunk * sizeof(CT), R.bar + s);
+    }
+  }
+  R.gi += n;
+  R.q_next -= n;
+}
+// Start streaming the chunks that cover [lo, hi] (relative indices, lo <= hi), highest chunk first.
+template <int CK>
+__device__ __forceinline__ void ring_begin(Ring<CK>& R, int lo, int hi) {
+  R.q_next = hi / kChunk;
+  R.q_end = lo / kChunk;
+  ring_issue_n(R, min(kStages - (int)(R.gi - R.g), R.q_next - R.q_end + 1));
+}
+template <int CK>
+__device__ __forceinline__ const typename Step<CK>::CT* ring_wait(Ring<CK>& R) {
+  const int s = (int)(R.g % kStages);
+  mbar_wait(R.bar + s, (R.g / kStages) & 1u);
+  return R.buf + s * kChunk;
+}
+template <int CK>
+__device__ __forceinline__ void ring_release(Ring<CK>& R) {
+  __syncwarp();
+  ++R.g;
+  if (R.q_next >= R.q_end) ring_issue_n(R, 1);
 }
 
-// Horner over the coefficient range [lo, hi] (relative indices, descending) for the warp; each lane
-// updates (br, bi) only for k in its own window [wl, wr] (empty if wl > wr).
-template <int CK, bool CPLX>
-__device__ __forceinline__ void stream_window(WarpRing<CK>& R, int lo, int hi, int wl, int wr,
-                                              typename Step<CK>::W zr, typename Step<CK>::W zi,
-                                              typename Step<CK>::W& br, typename Step<CK>::W& bi) {
+// Horner over the coefficient range [lo, hi] (relative, descending) for the NP points of every lane:
+// point j updates b_j = b_j z_j + a_k only for k in its own window [wl_j, wr_j] (b_j must be 0 on
+// entry).  Inside [F_lo, F_hi], common to all points whose window meets [lo, hi], the steps are
+// unmasked (8 coefficients loaded ahead, then NP independent Horner chains per coefficient); outside
+// it a masked step zeroes the coefficient above a window (b stays exactly 0) and freezes b below it.
+// Points whose window misses [lo, hi] compute garbage that the caller discards.
+template <int CK, int NP, bool CPLX>
+__device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const int (&wl)[NP], const int (&wr)[NP],
+                                             const typename Step<CK>::W (&zr)[NP],
+                                             const typename Step<CK>::W (&zi)[NP],
+                                             typename Step<CK>::W (&br)[NP], typename Step<CK>::W (&bi)[NP]) {
   using CT = typename Step<CK>::CT;
-  const int lane = threadIdx.x & 31;
-  if (lo > hi) return;
-  // warp-uniform range where every lane is active (empty if some lane is idle)
-  const bool nonempty = wl <= wr;
-  const bool all = __all_sync(0xffffffffu, nonempty);
-  int F_lo = __reduce_max_sync(0xffffffffu, (unsigned)(nonempty ? wl : 0));
-  int F_hi = (int)__reduce_min_sync(0xffffffffu, (unsigned)(nonempty ? wr : 0x7fffffff));
-  if (!all) { F_lo = 1; F_hi = 0; }
-  const int q_hi = hi / kChunk, q_lo = lo / kChunk;
-  const int nq = q_hi - q_lo + 1;
-  if (lane == 0)
-    for (int j = 0; j < nq && j < kStages; ++j) ring_issue<CK>(R, R.g + j, q_hi - j);
-  for (int j = 0; j < nq; ++j) {
-    const uint32_t g = R.g + j;
-    const int s = g % kStages;
-    mbar_wait(R.bar + s, (g / kStages) & 1u);
-    const int q = q_hi - j;
-    const CT* cb = R.buf + s * kChunk - q * kChunk;   // cb[k] for k in chunk q
-    const int klo = max(lo, q * kChunk), khi = min(hi, q * kChunk + kChunk - 1);
-    const int a = max(klo, F_lo), b = min(khi, F_hi);
-    int k = khi;
-    if (a <= b) {
-      for (; k > b; --k) if (k >= wl && k <= wr) horner_step<CK, CPLX>(br, bi, zr, zi, cb[k]);
-#pragma unroll 8
-      for (; k >= a; --k) horner_step<CK, CPLX>(br, bi, zr, zi, cb[k]);
+  using W = typename Step<CK>::W;
+  int mx = lo, mn = hi;
+  bool any = false;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    if (wl[j] <= wr[j] && wl[j] <= hi && wr[j] >= lo) {
+      mx = max(mx, wl[j]);
+      mn = min(mn, wr[j]);
+      any = true;
     }
-    for (; k >= klo; --k) if (k >= wl && k <= wr) horner_step<CK, CPLX>(br, bi, zr, zi, cb[k]);
-    __syncwarp();
-    if (lane == 0 && j + kStages < nq) ring_issue<CK>(R, g + kStages, q - kStages);
   }
-  R.g += nq;
+  int F_lo = __reduce_max_sync(0xffffffffu, mx);
+  int F_hi = __reduce_min_sync(0xffffffffu, mn);
+  if (!__any_sync(0xffffffffu, any) || F_lo > F_hi) { F_lo = lo; F_hi = lo - 1; }
+  const CT zero = CT{};
+  for (int q = hi / kChunk; q >= lo / kChunk; --q) {
+    const CT* cb = ring_wait(R) - q * kChunk;
+    const int k1 = min(hi, q * kChunk + kChunk - 1), k0 = max(lo, q * kChunk);
+    int k = k1;
+    for (const int m1 = max(k0, F_hi + 1); k >= m1; --k) {
+      const CT a = cb[k];
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        W nr = br[j], ni = bi[j];
+        horner_step<CK, CPLX>(nr, ni, zr[j], zi[j], k <= wr[j] ? a : zero);
+        if (k >= wl[j]) { br[j] = nr; bi[j] = ni; }
+      }
+    }
+    const int f0 = max(k0, F_lo);
+    for (; k - 7 >= f0; k -= 8) {
+      CT a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = cb[k - u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) horner_step<CK, CPLX>(br[j], bi[j], zr[j], zi[j], a[u]);
+      }
+    }
+    for (; k >= f0; --k) {
+      const CT a = cb[k];
+#pragma unroll
+      for (int j = 0; j < NP; ++j) horner_step<CK, CPLX>(br[j], bi[j], zr[j], zi[j], a);
+    }
+    for (; k >= k0; --k) {
+      const CT a = cb[k];
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        W nr = br[j], ni = bi[j];
+        horner_step<CK, CPLX>(nr, ni, zr[j], zi[j], k <= wr[j] ? a : zero);
+        if (k >= wl[j]) { br[j] = nr; bi[j] = ni; }
+      }
+    }
+    ring_release(R);
+  }
 }
+
+// ------------------------------------------------------------------------------------------------
+// combining piece partials (top-down Horner over the pieces, PAPER.md:1621-1622 generalised) and the
+// epilogue Q = acc z^l.  Shared by the serial and the parallel path, so that a point's
+// result does not depend on which one evaluated it.
+struct Acc {
+  double r, i;
+  int base;        // relative index of the lowest coefficient folded in so far
+  bool started;
+};
 
 // (re, im) * (h + e) 2^E, scaled into range (the product is bounded by the cover argument).
 __device__ __forceinline__ void mul_ext(double& re, double& im, const xc_t& p) {
@@ -236,137 +304,182 @@ __device__ __forceinline__ void mul_ext(double& re, double& im, const xc_t& p) {
   re = ldexp(r, sc); im = ldexp(i, sc);
 }
 
+template <bool CPLX>
+__device__ __forceinline__ xc_t power_piece(double x, double y) {   // z^kPiece, compensated powering
+  if constexpr (CPLX) return xc_pow(x, y, kPiece);
+  else { xr_t v = xr_pow(x, kPiece); return xc_t{v.h, 0.0, v.e, 0.0, v.E}; }
+}
+template <bool CPLX>
+__device__ __forceinline__ xc_t power_polar(double x, double y, long long n) {   // z^n by the polar route
+  polar_t p = polar_of<CPLX>(x, y);
+  if constexpr (CPLX) return pow_polar(p.lam, p.tau, n);
+  else { xr_t v = pow_polar_real(p.lam, p.neg, n); return xc_t{v.h, 0.0, 0.0, 0.0, v.E}; }
+}
+
+template <bool CPLX>
+__device__ __forceinline__ void acc_fold(Acc& A, double hr, double hi, int pbase, double x, double y) {
+  if (!A.started) { A.r = hr; A.i = hi; A.base = pbase; A.started = true; return; }
+  const int gap = A.base - pbase;
+  const xc_t m = (gap == kPiece) ? power_piece<CPLX>(x, y) : power_polar<CPLX>(x, y, gap);
+  mul_ext(A.r, A.i, m);
+  A.r += hr; A.i += hi;
+  A.base = pbase;
+}
+
 template <int OK, bool CPLX>
-__device__ __forceinline__ void finalize_point(void* vals, long long* exps, long long idx, double x, double y,
-                                               double br, double bi, long long l_abs, const PolyDev& P) {
-  if (x == 0.0 && y == 0.0) {   // z = 0: P(0) = a_0 (window {k_min})
-    if (P.k_min != 0) { br = 0.0; bi = 0.0; }
-    store_value<OK>(vals, exps, idx, br, bi, (br == 0.0 && bi == 0.0) ? 0 : P.shift);
+__device__ __forceinline__ void finalize(void* vals, long long* exps, long long idx, double x, double y,
+                                         const Acc& A, const PolyDev& P) {
+  if (!isfinite(x) || !isfinite(y)) {
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    store_value<OK>(vals, exps, idx, nan, CPLX ? nan : 0.0, 0);
     return;
   }
-  double qr, qi;
-  long long E;
-  times_zpow<CPLX>(br, bi, x, y, l_abs, qr, qi, E);
+  double qr = A.started ? A.r : 0.0, qi = A.started ? A.i : 0.0;
+  if (x == 0.0 && y == 0.0) {   // z = 0: P(0) = a_0 (window {k_min})
+    if (P.k_min != 0) { qr = 0.0; qi = 0.0; }
+    store_value<OK>(vals, exps, idx, qr, qi, (qr == 0.0 && qi == 0.0) ? 0 : P.shift);
+    return;
+  }
+  long long E = 0;
+  const long long n = A.started ? (long long)A.base + P.k_min : 0;
+  if (n > 0) {
+    const xc_t p = power_polar<CPLX>(x, y, n);
+    const double r = __fma_rn(qr, p.hr, -qi * p.hi);
+    const double i = __fma_rn(qr, p.hi, qi * p.hr);
+    qr = r; qi = i; E = p.E;
+  }
   store_value<OK>(vals, exps, idx, qr, qi, E + P.shift);
 }
 
-struct LongShared {
-  double hr[kWarps][32], hi[kWarps][32];
-  int base[kWarps][32];
+// The NP points of each lane of a group: sorted position j*32 + lane.
+template <int NP>
+struct Pts {
+  long long idx[NP];
+  double x[NP], y[NP];
+  int wl[NP], wr[NP];   // relative window; empty (wl > wr) for padding and non-finite points
+  bool valid[NP];
 };
 
-struct ItemShared {
-  const uint32_t* gidx;
-  int count, done;
-};
-
-// Long group (32 long-window points, all 8 warps): absolute segments, combined top-down by warp 0.
-template <int PK, int CK, int OK>
-__device__ __forceinline__ void long_group(WarpRing<CK>& R, LongShared* LS, const uint32_t* gidx, int gcount,
-                                           const void* __restrict__ pts, const int2* __restrict__ lr,
-                                           const PolyDev& P, void* vals, long long* exps) {
-  constexpr bool CPLX = PtTraits<OK>::cplx;
-  using W = typename Step<CK>::W;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int kmin = (int)P.k_min;
-  const bool valid = lane < gcount;
-  long long idx = 0;
-  double x = 0.0, y = 0.0;
-  int wl = 1, wr = 0;
-  if (valid) {
-    idx = __ldg(gidx + lane);
-    load_point<PK>(pts, idx, x, y);
-    int2 w2 = __ldg(lr + idx);
-    wl = w2.x - kmin; wr = w2.y - kmin;
+// Group g holds the sorted positions [g*32*NP, min(n, (g+1)*32*NP)) (k_plan), so its permutation
+// entries are loaded without waiting for the descriptor.
+template <int NP>
+__device__ __forceinline__ void load_group_idx(Pts<NP>& S, uint32_t g, long long n, const uint32_t* __restrict__ perm) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    const long long pos = (long long)g * (32 * NP) + j * 32 + lane;
+    S.valid[j] = pos < n;
+    S.idx[j] = S.valid[j] ? (long long)__ldg(perm + pos) : 0;
   }
-  const int lo = (int)__reduce_min_sync(0xffffffffu, (unsigned)(valid ? wl : 0x7fffffff));
-  const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)(valid ? wr : 0));
-  const int T_lo = lo / kSegLen, T_hi = hi / kSegLen;
-  double acc_r = 0.0, acc_i = 0.0;
-  int last_base = 0;
-  bool started = false;
-  xc_t zL;
-  if (wib == 0 && valid) zL = xc_pow(x, y, kSegLen);
-  for (int tb = T_hi; tb >= T_lo; tb -= kWarps) {
-    const int t = tb - wib;
-    if (t >= T_lo) {
-      const int s_lo = t * kSegLen, s_hi = s_lo + kSegLen - 1;
-      const int swl = max(wl, s_lo), swr = min(wr, s_hi);
-      W br = 0, bi = 0;
-      stream_window<CK, CPLX>(R, max(lo, s_lo), min(hi, s_hi), swl, swr, (W)x, (W)y, br, bi);
-      LS->hr[wib][lane] = (double)br;
-      LS->hi[wib][lane] = (double)bi;
-      LS->base[wib][lane] = (swl <= swr) ? swl : -1;
+}
+template <int PK, int NP>
+__device__ __forceinline__ void load_group_pts(Pts<NP>& S, const void* __restrict__ pts, const int2* __restrict__ lr,
+                                               int kmin) {
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    S.x[j] = 0.0; S.y[j] = 0.0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
+    if (S.valid[j]) {
+      load_point<PK>(pts, S.idx[j], S.x[j], S.y[j]);
+      const int2 w = __ldg(lr + S.idx[j]);
+      if (w.y >= w.x) { S.wl[j] = w.x - kmin; S.wr[j] = w.y - kmin; }
     }
-    __syncthreads();
-    if (wib == 0 && valid) {
-      for (int ww = 0; ww < kWarps && tb - ww >= T_lo; ++ww) {
-        const int base = LS->base[ww][lane];
-        if (base < 0) continue;
-        const double hr = LS->hr[ww][lane], hi_ = LS->hi[ww][lane];
-        if (!started) {
-          acc_r = hr; acc_i = hi_; started = true;
-        } else {
-          const int gap = last_base - base;
-          if (gap == kSegLen) mul_ext(acc_r, acc_i, zL);
-          else { xc_t zg = xc_pow(x, y, gap); mul_ext(acc_r, acc_i, zg); }
-          acc_r += hr; acc_i += hi_;
-        }
-        last_base = base;
-      }
-    }
-    __syncthreads();
   }
-  if (wib == 0 && valid)
-    finalize_point<OK, CPLX>(vals, exps, idx, x, y, acc_r, acc_i, (long long)last_base + kmin, P);
 }
 
-// Short group (32 short-window points, one warp): the union processed as merged intervals (windows
-// closer than kMergeGap share one streamed interval; several intervals only where the key order
-// jumps, e.g. across the lambda range of the long windows).
-template <int PK, int CK, int OK>
-__device__ __forceinline__ void short_group(WarpRing<CK>& R, const uint32_t* gidx, int gcount,
-                                            const void* __restrict__ pts, const int2* __restrict__ lr,
-                                            const PolyDev& P, void* vals, long long* exps) {
+template <int CK, int NP, bool CPLX>
+__device__ __forceinline__ void eval_piece(Ring<CK>& R, const Pts<NP>& S, int rlo, int rhi,
+                                           typename Step<CK>::W (&br)[NP], typename Step<CK>::W (&bi)[NP]) {
+  using W = typename Step<CK>::W;
+  W zr[NP], zi[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) { zr[j] = (W)S.x[j]; zi[j] = (W)S.y[j]; br[j] = 0; bi[j] = 0; }
+  stream_range<CK, NP, CPLX>(R, rlo, rhi, S.wl, S.wr, zr, zi, br, bi);
+}
+
+// One warp evaluates a whole group: the pieces of its union window top-down, folding as it goes.
+template <int PK, int CK, int OK, int NP>
+__device__ __forceinline__ void single_group(Ring<CK>& R, uint32_t g, long long n, const Plan& plan,
+                                             const uint32_t* __restrict__ perm, const void* __restrict__ pts,
+                                             const int2* __restrict__ lr, const PolyDev& P, void* vals,
+                                             long long* exps) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
-  const int lane = threadIdx.x & 31;
   const int kmin = (int)P.k_min;
-  const bool valid = lane < gcount;
-  long long idx = 0;
-  double x = 0.0, y = 0.0;
-  int wl = 1, wr = 0, l_abs = 0;
-  if (valid) {
-    idx = __ldg(gidx + lane);
-    load_point<PK>(pts, idx, x, y);
-    int2 w2 = __ldg(lr + idx);
-    l_abs = w2.x;
-    wl = w2.x - kmin; wr = w2.y - kmin;
-  }
-  W br = 0, bi = 0;
-  const bool act = valid && wl <= wr;
-  unsigned pending = __ballot_sync(0xffffffffu, act);
-  while (pending) {
-    const bool pend = (pending >> lane) & 1u;
-    const int top = (int)__reduce_max_sync(0xffffffffu, pend ? (unsigned)wr : 0u);
-    int lo = (int)__reduce_min_sync(0xffffffffu, (pend && wr == top) ? (unsigned)wl : 0x7fffffffu);
-    for (;;) {
-      const bool in = pend && wr >= lo - kMergeGap;
-      const int lo2 = (int)__reduce_min_sync(0xffffffffu, in ? (unsigned)wl : 0x7fffffffu);
-      if (lo2 >= lo) break;
-      lo = lo2;
+  Pts<NP> S;
+  load_group_idx<NP>(S, g, n, perm);
+  const GroupDesc d = plan.desc[g];
+  const bool nonempty = d.hi >= d.lo;
+  const int p_hi = nonempty ? d.hi / kPiece : 0, p_lo = nonempty ? d.lo / kPiece : 0;
+  if (nonempty) ring_begin(R, max(d.lo, p_hi * kPiece), d.hi);   // coefficients in flight during the loads
+  load_group_pts<PK, NP>(S, pts, lr, kmin);
+  Acc A[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) A[j] = Acc{0.0, 0.0, 0, false};
+  if (nonempty) {
+    for (int p = p_hi; p >= p_lo; --p) {
+      const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
+      if (p != p_hi) ring_begin(R, rlo, rhi);
+      W br[NP], bi[NP];
+      eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, br, bi);
+#pragma unroll
+      for (int j = 0; j < NP; ++j)
+        if (S.wl[j] <= S.wr[j] && S.wl[j] <= p * kPiece + kPiece - 1 && S.wr[j] >= p * kPiece)
+          acc_fold<CPLX>(A[j], (double)br[j], (double)bi[j], max(S.wl[j], p * kPiece), S.x[j], S.y[j]);
     }
-    const bool mine = pend && wr >= lo - kMergeGap;
-    stream_window<CK, CPLX>(R, lo, top, mine ? wl : 1, mine ? wr : 0, (W)x, (W)y, br, bi);
-    pending &= ~__ballot_sync(0xffffffffu, mine);
   }
-  if (valid) {
-    if (wl > wr) {   // non-finite point
-      double nan = __longlong_as_double(0x7ff8000000000000LL);
-      store_value<OK>(vals, exps, idx, nan, CPLX ? nan : 0.0, 0);
-    } else {
-      finalize_point<OK, CPLX>(vals, exps, idx, x, y, (double)br, (double)bi, l_abs, P);
+#pragma unroll
+  for (int j = 0; j < NP; ++j)
+    if (S.valid[j]) finalize<OK, CPLX>(vals, exps, S.idx[j], S.x[j], S.y[j], A[j], P);
+}
+
+// One warp evaluates piece p of a multi-piece group into its scratch slot; the warp that completes
+// the group's last piece folds all partials in order and finalises.
+template <int PK, int CK, int OK, int NP>
+__device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long long n, const Plan& plan,
+                                            const uint32_t* __restrict__ perm, const void* __restrict__ pts,
+                                            const int2* __restrict__ lr, const PolyDev& P, void* vals,
+                                            long long* exps) {
+  constexpr bool CPLX = PtTraits<OK>::cplx;
+  using W = typename Step<CK>::W;
+  using W2 = typename std::conditional<std::is_same<W, float>::value, float2, double2>::type;
+  constexpr int G = 32 * NP;
+  const int lane = threadIdx.x & 31;
+  const GroupDesc d = plan.desc[g];
+  const int kmin = (int)P.k_min;
+  const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
+  ring_begin(R, rlo, rhi);
+  Pts<NP> S;
+  load_group_idx<NP>(S, g, n, perm);
+  load_group_pts<PK, NP>(S, pts, lr, kmin);
+  W br[NP], bi[NP];
+  eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, br, bi);
+  const int p0 = d.lo / kPiece;
+  W2* scr = static_cast<W2*>(plan.scratch);
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    W2 v; v.x = br[j]; v.y = bi[j];
+    scr[(size_t)(d.slot + (p - p0)) * G + j * 32 + lane] = v;
+  }
+  __threadfence();
+  __syncwarp();
+  uint32_t done = 0;
+  if (lane == 0) done = atomicAdd(plan.gcnt + g, 1u);
+  done = __shfl_sync(0xffffffffu, done, 0);
+  if (done != (uint32_t)d.npieces - 1) return;
+  __threadfence();
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    if (!S.valid[j]) continue;
+    Acc A{0.0, 0.0, 0, false};
+    if (S.wl[j] <= S.wr[j]) {
+      for (int pp = d.hi / kPiece; pp >= p0; --pp) {
+        if (S.wl[j] <= pp * kPiece + kPiece - 1 && S.wr[j] >= pp * kPiece) {
+          const W2 v = __ldcg(scr + (size_t)(d.slot + (pp - p0)) * G + j * 32 + lane);
+          acc_fold<CPLX>(A, (double)v.x, (double)v.y, max(S.wl[j], pp * kPiece), S.x[j], S.y[j]);
+        }
+      }
     }
+    finalize<OK, CPLX>(vals, exps, S.idx[j], S.x[j], S.y[j], A, P);
   }
 }
 
@@ -375,69 +488,41 @@ constexpr size_t ring_bytes() {
   return (size_t)kWarps * kStages * kChunk * sizeof(typename Step<CK>::CT);
 }
 
-// Persistent evaluator.  Work items are the 32-point group slots of the sorted chunks (64 per
-// chunk): long-bucket slots first, each taken by a whole CTA (long_group), then short-bucket slots,
-// each taken by one warp (short_group); both fetched with global atomic counters.
-template <int PK, int CK, int OK>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(const void* __restrict__ pts, long long n, PolyDev P,
+// Persistent evaluator: every warp first takes parallel pieces of long windows, then whole groups,
+// both from global atomic counters (largest work first; the tail is at most one group).
+template <int PK, int CK, int OK, int NP>
+__global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const void* __restrict__ pts, long long n, PolyDev P,
                                                                const int2* __restrict__ lr,
-                                                               const uint32_t* __restrict__ perm,
-                                                               const uint32_t* __restrict__ gcount,
-                                                               const uint32_t* __restrict__ bstart,
-                                                               const uint32_t* __restrict__ istart,
-                                                               uint32_t* __restrict__ ctrs, void* __restrict__ vals,
-                                                               long long* __restrict__ exps) {
+                                                               const uint32_t* __restrict__ perm, Plan plan,
+                                                               void* __restrict__ vals, long long* __restrict__ exps) {
   using CT = typename Step<CK>::CT;
-  constexpr int kSlots = kChunkPts / 32;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   CT* ring_buf = reinterpret_cast<CT*>(smem) + (size_t)wib * kStages * kChunk;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes<CK>()) + wib * kStages;
-  LongShared* LS = reinterpret_cast<LongShared*>(smem + ring_bytes<CK>() + kWarps * kStages * sizeof(uint64_t));
-  ItemShared* IS = reinterpret_cast<ItemShared*>(reinterpret_cast<unsigned char*>(LS) + sizeof(LongShared));
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  WarpRing<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u};
-  const int n_long_chunks = (int)istart[kBuckets / 2];
-  const int n_chunks = (int)istart[kBuckets];
-  const long long n_long_items = (long long)n_long_chunks * kSlots;
-  const long long n_short_items = (long long)(n_chunks - n_long_chunks) * kSlots;
-
-  for (;;) {   // long-window groups: whole CTA
-    if (threadIdx.x == 0) {
-      const long long it = atomicAdd(ctrs + 0, 1u);
-      IS->done = it >= n_long_items;
-      IS->count = 0;
-      if (!IS->done) {
-        int bucket, npts;
-        uint32_t p0;
-        chunk_of(istart, gcount, bstart, (int)(it / kSlots), bucket, p0, npts);
-        const int slot = (int)(it % kSlots);
-        IS->count = max(0, min(32, npts - 32 * slot));
-        IS->gidx = perm + p0 + 32 * slot;
-      }
-    }
-    __syncthreads();
-    const int done = IS->done, count = IS->count;
-    const uint32_t* gidx = IS->gidx;
-    __syncthreads();
-    if (done) break;
-    if (count > 0) long_group<PK, CK, OK>(R, LS, gidx, count, pts, lr, P, vals, exps);
-  }
-  for (;;) {   // short-window groups: one warp each
-    long long it = 0;
-    if (lane == 0) it = atomicAdd(ctrs + 1, 1u);
+  __syncwarp();
+  Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0};
+  const uint32_t n_multi = min(plan.ctrs[2], plan.cap);
+  const uint32_t n_single = plan.ctrs[3];
+  for (;;) {
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(plan.ctrs + 0, 1u);
     it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= n_short_items) break;
-    int bucket, npts;
-    uint32_t p0;
-    chunk_of(istart, gcount, bstart, n_long_chunks + (int)(it / kSlots), bucket, p0, npts);
-    const int slot = (int)(it % kSlots);
-    const int count = min(32, npts - 32 * slot);
-    if (count > 0) short_group<PK, CK, OK>(R, perm + p0 + 32 * slot, count, pts, lr, P, vals, exps);
+    if (it >= n_multi) break;
+    const uint2 item = plan.items[it];
+    if (item.x == ~0u) continue;
+    multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, perm, pts, lr, P, vals, exps);
+  }
+  for (;;) {
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(plan.ctrs + 1, 1u);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= n_single) break;
+    single_group<PK, CK, OK, NP>(R, plan.singles[it], n, plan, perm, pts, lr, P, vals, exps);
   }
 }
 
@@ -446,43 +531,53 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(const void* __res
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static size_t n_ctas(long long n) { return (size_t)((n + kPtsPerCta - 1) / kPtsPerCta); }
+// scratch for parallel pieces: 2 bytes per point (at least 1 MiB), in slots of 1 KiB (64 double2)
+static size_t scratch_slots(long long n) {
+  size_t bytes = max((size_t)n * 2, (size_t)1 << 20);
+  return bytes / 1024;
+}
 
 size_t tiled_ws_bytes(long long n) {
   return al256(n * sizeof(int2)) + 2 * al256(n * sizeof(uint32_t)) +
-         al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 3 * al256((kBuckets + 1) * sizeof(uint32_t)) + 256;
+         al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 3 * al256((kBuckets + 1) * sizeof(uint32_t)) +
+         al256(max_groups(n) * sizeof(GroupDesc)) + 2 * al256(max_groups(n) * sizeof(uint32_t)) +
+         al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
 }
 
 template <int CK>
 static size_t eval_smem() {
-  return ring_bytes<CK>() + kWarps * kStages * sizeof(uint64_t) + sizeof(LongShared) + sizeof(ItemShared);
+  return ring_bytes<CK>() + kWarps * kStages * sizeof(uint64_t);
 }
 
-template <int PK, int CK, int OK>
-static int launch_eval_tiled_t(const void* pts, long long n, const PolyDev& P, const int2* lr,
-                               const uint32_t* perm, const uint32_t* gcount, const uint32_t* bstart,
-                               const uint32_t* istart, uint32_t* ctrs, void* vals, long long* exps, cudaStream_t s) {
+template <int PK, int CK, int OK, int NP>
+static int launch_eval_tiled_t(const void* pts, long long n, const PolyDev& P, const int2* lr, const uint32_t* perm,
+                               const Plan& plan, void* vals, long long* exps, cudaStream_t s) {
   static int grid = 0;
   const size_t smem = eval_smem<CK>();
   if (grid == 0) {
-    cudaFuncSetAttribute(k_eval_tiled<PK, CK, OK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_eval_tiled<PK, CK, OK, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_tiled<PK, CK, OK>, kWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_tiled<PK, CK, OK, NP>, kWarps * 32, smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid = max(1, per_sm) * sms;
   }
-  k_eval_tiled<PK, CK, OK><<<grid, kWarps * 32, smem, s>>>(pts, n, P, lr, perm, gcount, bstart, istart,
-                                                             ctrs, vals, exps);
+  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(pts, n, P, lr, perm, plan, vals, exps);
   return 1;
 }
 
+// points per lane: complex steps (4 FMAs per coefficient) share a coefficient load between 2 points,
+// real steps (1 FMA) between 4 (shared-memory wavefronts per FMA)
 template <int PK, int CK>
-static int dispatch_eval(const void* pts, long long n, const PolyDev& P, const int2* lr,
-                         const uint32_t* perm, const uint32_t* gcount, const uint32_t* bstart, const uint32_t* istart,
-                         uint32_t* ctrs, void* vals, long long* exps, cudaStream_t s) {
-  constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
-  constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
-  return launch_eval_tiled_t<PK, CK, OK>(pts, n, P, lr, perm, gcount, bstart, istart, ctrs, vals, exps, s);
+struct NPFor {
+  static constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
+  static constexpr int value = cplx ? 2 : 4;
+  static constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
+};
+
+static int np_for(int pk, int cdt) {
+  const bool cplx = (pk == FPE_C64 || pk == FPE_C32 || cdt == FPE_C64 || cdt == FPE_C32);
+  return cplx ? 2 : 4;
 }
 
 template <int PK>
@@ -503,9 +598,20 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   uint32_t* gcount = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   uint32_t* bstart = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   uint32_t* istart = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
-  uint32_t* ctrs = reinterpret_cast<uint32_t*>(p);
+  Plan plan;
+  plan.desc = reinterpret_cast<GroupDesc*>(p); p += al256(max_groups(n) * sizeof(GroupDesc));
+  plan.gcnt = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
+  plan.singles = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
+  plan.items = reinterpret_cast<uint2*>(p); p += al256(scratch_slots(n) * sizeof(uint2));
+  plan.scratch = p; p += al256(scratch_slots(n) * 1024);
+  plan.ctrs = reinterpret_cast<uint32_t*>(p);
+  const int np = np_for(pk, P.cdt);
+  plan.gsize = 32 * np;
+  const bool f32 = (P.cdt == FPE_R32 || P.cdt == FPE_C32);
+  const size_t slot_bytes = (size_t)plan.gsize * (f32 ? sizeof(float2) : sizeof(double2));
+  plan.cap = (uint32_t)(scratch_slots(n) * 1024 / slot_bytes);
   cudaMemsetAsync(gcount, 0, (kBuckets + 1) * 4, s);
-  cudaMemsetAsync(ctrs, 0, 16, s);
+  cudaMemsetAsync(plan.ctrs, 0, 16, s);
   switch (pk) {
     case FPE_R64: launch_classify_bucket_t<FPE_R64>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
     case FPE_C64: launch_classify_bucket_t<FPE_C64>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
@@ -513,11 +619,11 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     default: launch_classify_bucket_t<FPE_C32>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
   }
   st.mark("classify");
-  bucket_finish(keys, n, gcount, cta_base, bstart, istart, perm, s);
+  bucket_finish(keys, n, gcount, cta_base, bstart, istart, perm, lr, P.k_min, plan, s);
   st.mark("bucket");
   int le = 0;
 #define FPE_EV(PKV, CKV) \
-  le = dispatch_eval<PKV, CKV>(pts, n, P, lr, perm, gcount, bstart, istart, ctrs, vals, exps, s)
+  le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(pts, n, P, lr, perm, plan, vals, exps, s)
   switch (pk * 4 + P.cdt) {
     case FPE_R64 * 4 + FPE_R64: FPE_EV(FPE_R64, FPE_R64); break;
     case FPE_R64 * 4 + FPE_C64: FPE_EV(FPE_R64, FPE_C64); break;
@@ -531,7 +637,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   }
 #undef FPE_EV
   st.mark("eval_tiled");
-  return 4 + le;
+  return 5 + le;
 }
 
 }  // namespace fpe

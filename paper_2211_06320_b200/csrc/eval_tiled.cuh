@@ -4,11 +4,11 @@
 #include "fpe_internal.h"
 
 namespace fpe {
-constexpr int kChunk = 128;     // coefficients per TMA bulk copy / ring stage (dense array padded to this)
-constexpr int kSegLen = 4096;   // windows longer than this are split at absolute multiples of kSegLen
+constexpr int kChunk = kCoefPad;   // coefficients per TMA bulk copy / ring stage (dense array padded to this)
+constexpr int kLongWin = 4096;     // windows longer than this sort into the "long" half of the key space
 
 size_t tiled_ws_bytes(long long n);
-// classify + sort + evaluate (dense handles).  Returns the number of kernel launches or -1.
+// classify + sort + plan + evaluate (dense handles).  Returns the number of kernel launches or -1.
 int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
               fpe_diag* diag, void* ws, unsigned long long* hard, Stage& st, cudaStream_t s);
 }  // namespace fpe

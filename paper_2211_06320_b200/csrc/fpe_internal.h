@@ -9,12 +9,14 @@
 namespace fpe {
 
 constexpr uint64_t kMagic = 0x4650453230304232ull;  // "FPE200B2"
-constexpr uint32_t kVersion = 1;
+constexpr uint32_t kVersion = 2;
+constexpr int kCoefPad = 256;   // dense coefficient arrays are padded to whole evaluator chunks
 
 // First 256 bytes of the flat device buffer (also kept on the host in the handle).
 // Sections follow, each 256-byte aligned:
 //   hull   int2[n_hull]                (k, s(a_k)) of the canonical cover vertices
 //   coef   dense : CT[d_eff + 1]        a_k 2^-shift for k in [k_min, k_max], 0 where k not in G_p
+//                                       (zero-padded to a multiple of kCoefPad)
 //          sparse: CT[n_good]           a_k 2^-shift for the good indices
 //   prefix int32[d_eff + 2]             dense & not all_good: #G_p below k (k - k_min)
 //   sidx   int32[n_good]                sparse: the good indices, increasing

@@ -137,7 +137,7 @@ fpe_status precondition_host(const void* coeffs, int64_t n, fpe_dtype dt, int32_
   // 5. flat buffer
   const size_t csz = f32 ? (cplx ? 8 : 4) : (cplx ? 16 : 8);
   const int64_t n_coef = sparse ? n_good : d_eff + 1;
-  const int64_t n_coef_alloc = sparse ? n_coef : (n_coef + 127) / 128 * 128;   // TMA chunks (kChunk) read whole
+  const int64_t n_coef_alloc = sparse ? n_coef : (n_coef + kCoefPad - 1) / kCoefPad * kCoefPad;   // TMA chunks read whole
   std::memset(&hdr, 0, sizeof(hdr));
   hdr.magic = kMagic; hdr.version = kVersion; hdr.dtype = dt;
   hdr.n_coeffs = n; hdr.k_min = k_min; hdr.k_max = k_max; hdr.n_hull = nv; hdr.n_good = n_good;

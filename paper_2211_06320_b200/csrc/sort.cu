@@ -9,8 +9,9 @@
 //             k_bucket_scan turns bucket totals into starts and enumerates work items (chunks of at
 //             most kChunkPts points of one bucket, long buckets first); k_bucket_scatter writes the
 //             permutation (contiguous runs per (CTA, bucket), so L2 merges the partial sectors).
-//   local   : the evaluator sorts each chunk by the remaining low bits in shared memory
-//             (counting sort) before cutting it into warp groups of 32.
+//   local   : k_chunk_sort sorts each chunk by the remaining low bits in shared memory (counting
+//             sort); k_plan cuts the sorted permutation into groups of 32*NP points and plans their
+//             work items.
 // Order inside a (CTA, bucket) run and inside equal keys is unspecified; every point's arithmetic
 // depends only on its own window, so results do not depend on it (bitwise).
 #include <cuda_runtime.h>
@@ -95,7 +96,8 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restri
   }
 }
 
-// In-place counting sort of every chunk of the permutation by key bits [1, 1 + kLocalBits).
+// In-place counting sort of every chunk of the permutation by key bits [1, 1 + kLocalBits): afterwards
+// the whole permutation is ordered by key bits 1..23 (buckets are laid out in key order).
 __global__ void __launch_bounds__(256) k_chunk_sort(const uint32_t* __restrict__ keys, uint32_t* __restrict__ perm,
                                                     const uint32_t* __restrict__ gcount,
                                                     const uint32_t* __restrict__ bstart,
@@ -143,13 +145,59 @@ __global__ void __launch_bounds__(256) k_chunk_sort(const uint32_t* __restrict__
   for (int j = threadIdx.x; j < npts; j += 256) perm[p0 + j] = sorted[j];
 }
 
+// The evaluator's work plan: groups of gsize consecutive points of the sorted permutation (across
+// bucket boundaries: neighbouring buckets hold neighbouring lambdas), one warp per group: the union
+// of the windows and either one single item (one warp, pieces in order) or npieces parallel items
+// with scratch slots for their partials (windows longer than kPiece).
+__global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ perm, long long n,
+                                              const int2* __restrict__ lr, long long k_min, Plan plan) {
+  const int lane = threadIdx.x & 31;
+  const long long g = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int gs = plan.gsize;
+  const long long first = g * gs;
+  if (first >= n) return;
+  const int count = (int)min((long long)gs, n - first);
+  int lo = 0x7fffffff, hi = -1;
+  for (int j = lane; j < count; j += 32) {
+    const int2 w2 = __ldg(lr + __ldg(perm + first + j));
+    if (w2.y >= w2.x) {
+      lo = min(lo, (int)(w2.x - k_min));
+      hi = max(hi, (int)(w2.y - k_min));
+    }
+  }
+  lo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if (lane != 0) return;
+  GroupDesc d;
+  d.p0 = (uint32_t)first;
+  d.count = count;
+  d.lo = lo; d.hi = hi; d.slot = 0; d.npieces = 1;
+  bool single = true;
+  if (hi >= lo && hi - lo + 1 > kPiece) {
+    const int np = hi / kPiece - lo / kPiece + 1;
+    const uint32_t base = atomicAdd(plan.ctrs + 2, (uint32_t)np);
+    if ((unsigned long long)base + np <= plan.cap) {
+      d.slot = base; d.npieces = np;
+      plan.gcnt[g] = 0;
+      for (int i = 0; i < np; ++i) plan.items[base + i] = make_uint2((uint32_t)g, (uint32_t)(lo / kPiece + i));
+      single = false;
+    } else {   // scratch exhausted: evaluated serially by one warp (bitwise the same result)
+      for (uint32_t i = base; i < plan.cap && i < base + (uint32_t)np; ++i) plan.items[i] = make_uint2(~0u, 0u);
+    }
+  }
+  plan.desc[g] = d;
+  if (single) plan.singles[atomicAdd(plan.ctrs + 3, 1u)] = (uint32_t)g;
+}
+
 void bucket_finish(const uint32_t* keys, long long n, const uint32_t* gcount, const uint32_t* cta_base,
-                   uint32_t* bstart, uint32_t* istart, uint32_t* perm, cudaStream_t s) {
+                   uint32_t* bstart, uint32_t* istart, uint32_t* perm, const int2* lr, long long k_min,
+                   const Plan& plan, cudaStream_t s) {
   k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, istart);
   const int ctas = (int)((n + kPtsPerCta - 1) / kPtsPerCta);
   k_bucket_scatter<<<ctas, 256, 0, s>>>(keys, n, bstart, cta_base, perm);
-  const int max_chunks = (int)((n + kChunkPts - 1) / kChunkPts) + kBuckets;
-  k_chunk_sort<<<max_chunks, 256, 0, s>>>(keys, perm, gcount, bstart, istart);
+  k_chunk_sort<<<(int)max_chunks(n), 256, 0, s>>>(keys, perm, gcount, bstart, istart);
+  const long long groups = (n + plan.gsize - 1) / plan.gsize;
+  k_plan<<<(int)((groups + 7) / 8), 256, 0, s>>>(perm, n, lr, k_min, plan);
 }
 
 }  // namespace fpe

@@ -9,6 +9,31 @@ constexpr int kBuckets = 1 << kCoarseBits;
 constexpr int kPtsPerCta = 32768;               // points per CTA of classify / scatter
 constexpr int kChunkPts = 2048;                 // points per evaluator work item (one bucket's slice)
 constexpr int kLocalBits = 11;                  // in-chunk counting sort on key bits [1, 12)
+constexpr int kPiece = 16384;                   // absolute coefficient pieces: a window is cut at multiples
+                                                // of kPiece (relative to k_min) and the piece partials are
+                                                // combined top-down, so results never depend on the batch
+
+// A group: 32*NP consecutive points of the sorted permutation, evaluated by one warp (NP points per
+// lane) over the union [lo, hi] of their windows (relative to k_min; hi < lo: no finite point).
+struct GroupDesc {
+  uint32_t p0;      // first position in the permutation
+  int32_t count;    // points in the group
+  int32_t lo, hi;   // union of the windows
+  uint32_t slot;    // first scratch slot (multi-piece groups evaluated in parallel)
+  int32_t npieces;  // > 1: the pieces lo/kPiece .. hi/kPiece are separate work items
+};
+
+// Planner outputs (k_plan) consumed by the evaluator.
+struct Plan {
+  GroupDesc* desc;        // [max_groups]
+  uint32_t* gcnt;         // [max_groups] finished pieces of a multi-piece group
+  uint2* items;           // [cap] (group, piece) of the parallel pieces; group = ~0u: unused slot
+  uint32_t* singles;      // [max_groups] groups evaluated by one warp (all their pieces in order)
+  uint32_t* ctrs;         // [0] multi fetch, [1] single fetch, [2] slots reserved, [3] singles
+  void* scratch;          // [cap][32*NP] piece partials (working complex type)
+  uint32_t cap;           // scratch slots
+  int gsize;              // points per group (32*NP)
+};
 
 // Locate work-item chunk c (item order, long buckets first): its bucket, first position in the
 // permutation and its number of points.
@@ -21,8 +46,11 @@ __device__ __forceinline__ void chunk_of(const uint32_t* istart, const uint32_t*
   p0 = bstart[bucket] + off;
   npts = (int)min((uint32_t)kChunkPts, gcount[bucket] - off);
 }
-// bucket starts + item table (k_bucket_scan), the permutation (k_bucket_scatter) and the in-chunk
-// order (k_chunk_sort)
+// bucket starts + item table (k_bucket_scan), the permutation (k_bucket_scatter), the in-chunk
+// order (k_chunk_sort) and the evaluator's work plan (k_plan)
 void bucket_finish(const uint32_t* keys, long long n, const uint32_t* gcount, const uint32_t* cta_base,
-                   uint32_t* bstart, uint32_t* istart, uint32_t* perm, cudaStream_t s);
+                   uint32_t* bstart, uint32_t* istart, uint32_t* perm, const int2* lr, long long k_min,
+                   const Plan& plan, cudaStream_t s);
+inline long long max_chunks(long long n) { return (n + kChunkPts - 1) / kChunkPts + kBuckets; }
+inline long long max_groups(long long n) { return (n + 63) / 64; }   // groups of >= 64 points
 }  // namespace fpe
