@@ -7,10 +7,10 @@
 //                    histogram and slice claims (sort.cu).  l and r are both non-decreasing in lambda
 //                    (d/dlambda of cover(k) + lambda k - N is k - k_lambda), so points with close keys
 //                    have nested, nearly equal windows.
-//   bucket scan/scatter + k_chunk_sort + k_plan (sort.cu): permutation sorted by key (bits 1..23), cut
-//                    into groups of 32*NP consecutive points; per group the union window and the work
+//   bucket scan/scatter + k_chunk_sort + k_plan (sort.cu): permutation and windows sorted by key (bits
+//                    1..23), cut into groups of 32*NP consecutive points; per group the union window and the work
 //                    items (one whole group, or one item per kPiece-aligned piece of a long window).
-//   k_eval_tiled     persistent warps.  A warp streams the coefficients of its item's range through a
+//   k_eval_tiled     persistent warps: first the parallel pieces, then every other group in order.  A warp streams the coefficients of its item's range through a
 //                    private 3-stage shared-memory ring filled by 1-D TMA bulk copies (cp.async.bulk +
 //                    mbarrier complete_tx), reads them as warp-uniform broadcasts (one LDS per
 //                    coefficient for NP points per lane) and runs NP independent Horner chains per lane
@@ -363,26 +363,27 @@ struct Pts {
 // Group g holds the sorted positions [g*32*NP, min(n, (g+1)*32*NP)) (k_plan), so its permutation
 // entries are loaded without waiting for the descriptor.
 template <int NP>
-__device__ __forceinline__ void load_group_idx(Pts<NP>& S, uint32_t g, long long n, const uint32_t* __restrict__ perm) {
+__device__ __forceinline__ void load_group_idx(Pts<NP>& S, uint32_t g, long long n, const uint32_t* __restrict__ perm,
+                                               const int2* __restrict__ slr, int kmin) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
     const long long pos = (long long)g * (32 * NP) + j * 32 + lane;
     S.valid[j] = pos < n;
-    S.idx[j] = S.valid[j] ? (long long)__ldg(perm + pos) : 0;
+    S.idx[j] = 0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
+    if (S.valid[j]) {
+      S.idx[j] = (long long)__ldg(perm + pos);
+      const int2 w = __ldg(slr + pos);
+      if (w.y >= w.x) { S.wl[j] = w.x - kmin; S.wr[j] = w.y - kmin; }
+    }
   }
 }
 template <int PK, int NP>
-__device__ __forceinline__ void load_group_pts(Pts<NP>& S, const void* __restrict__ pts, const int2* __restrict__ lr,
-                                               int kmin) {
+__device__ __forceinline__ void load_group_pts(Pts<NP>& S, const void* __restrict__ pts) {
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
-    S.x[j] = 0.0; S.y[j] = 0.0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
-    if (S.valid[j]) {
-      load_point<PK>(pts, S.idx[j], S.x[j], S.y[j]);
-      const int2 w = __ldg(lr + S.idx[j]);
-      if (w.y >= w.x) { S.wl[j] = w.x - kmin; S.wr[j] = w.y - kmin; }
-    }
+    S.x[j] = 0.0; S.y[j] = 0.0;
+    if (S.valid[j]) load_point<PK>(pts, S.idx[j], S.x[j], S.y[j]);
   }
 }
 
@@ -405,13 +406,14 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, uint32_t g, long long 
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
   const int kmin = (int)P.k_min;
-  Pts<NP> S;
-  load_group_idx<NP>(S, g, n, perm);
   const GroupDesc d = plan.desc[g];
+  if (d.npieces > 1) return;   // evaluated as parallel pieces (multi_piece)
+  Pts<NP> S;
+  load_group_idx<NP>(S, g, n, perm, lr, kmin);
   const bool nonempty = d.hi >= d.lo;
   const int p_hi = nonempty ? d.hi / kPiece : 0, p_lo = nonempty ? d.lo / kPiece : 0;
   if (nonempty) ring_begin(R, max(d.lo, p_hi * kPiece), d.hi);   // coefficients in flight during the loads
-  load_group_pts<PK, NP>(S, pts, lr, kmin);
+  load_group_pts<PK, NP>(S, pts);
   Acc A[NP];
 #pragma unroll
   for (int j = 0; j < NP; ++j) A[j] = Acc{0.0, 0.0, 0, false};
@@ -449,8 +451,8 @@ __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long
   const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
   ring_begin(R, rlo, rhi);
   Pts<NP> S;
-  load_group_idx<NP>(S, g, n, perm);
-  load_group_pts<PK, NP>(S, pts, lr, kmin);
+  load_group_idx<NP>(S, g, n, perm, lr, kmin);
+  load_group_pts<PK, NP>(S, pts);
   W br[NP], bi[NP];
   eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, br, bi);
   const int p0 = d.lo / kPiece;
@@ -492,7 +494,7 @@ constexpr size_t ring_bytes() {
 // both from global atomic counters (largest work first; the tail is at most one group).
 template <int PK, int CK, int OK, int NP>
 __global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const void* __restrict__ pts, long long n, PolyDev P,
-                                                               const int2* __restrict__ lr,
+                                                               const int2* __restrict__ lr,   // sorted windows
                                                                const uint32_t* __restrict__ perm, Plan plan,
                                                                void* __restrict__ vals, long long* __restrict__ exps) {
   using CT = typename Step<CK>::CT;
@@ -507,22 +509,23 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const void* __res
   __syncwarp();
   Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0};
   const uint32_t n_multi = min(plan.ctrs[2], plan.cap);
-  const uint32_t n_single = plan.ctrs[3];
+  // the next item index is fetched one item ahead, so the atomic's latency hides behind the work
+  uint32_t nxt = 0;
+  if (lane == 0) nxt = atomicAdd(plan.ctrs + 0, 1u);
   for (;;) {
-    uint32_t it = 0;
-    if (lane == 0) it = atomicAdd(plan.ctrs + 0, 1u);
-    it = __shfl_sync(0xffffffffu, it, 0);
+    const uint32_t it = __shfl_sync(0xffffffffu, nxt, 0);
     if (it >= n_multi) break;
+    if (lane == 0) nxt = atomicAdd(plan.ctrs + 0, 1u);
     const uint2 item = plan.items[it];
     if (item.x == ~0u) continue;
     multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, perm, pts, lr, P, vals, exps);
   }
+  if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
   for (;;) {
-    uint32_t it = 0;
-    if (lane == 0) it = atomicAdd(plan.ctrs + 1, 1u);
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= n_single) break;
-    single_group<PK, CK, OK, NP>(R, plan.singles[it], n, plan, perm, pts, lr, P, vals, exps);
+    const uint32_t g = __shfl_sync(0xffffffffu, nxt, 0);
+    if (g >= plan.ngroups) break;
+    if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
+    single_group<PK, CK, OK, NP>(R, g, n, plan, perm, pts, lr, P, vals, exps);
   }
 }
 
@@ -538,9 +541,9 @@ static size_t scratch_slots(long long n) {
 }
 
 size_t tiled_ws_bytes(long long n) {
-  return al256(n * sizeof(int2)) + 2 * al256(n * sizeof(uint32_t)) +
+  return al256(n * sizeof(int2)) + al256(n * sizeof(uint32_t)) + al256(n * sizeof(int4)) +
          al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 3 * al256((kBuckets + 1) * sizeof(uint32_t)) +
-         al256(max_groups(n) * sizeof(GroupDesc)) + 2 * al256(max_groups(n) * sizeof(uint32_t)) +
+         al256(max_groups(n) * sizeof(GroupDesc)) + al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
 }
 
@@ -591,9 +594,10 @@ static void launch_classify_bucket_t(const void* pts, long long n, const PolyDev
 int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
               fpe_diag* diag, void* ws, unsigned long long* hard, Stage& st, cudaStream_t s) {
   char* p = static_cast<char*>(ws);
-  int2* lr = reinterpret_cast<int2*>(p); p += al256(n * sizeof(int2));
-  uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += al256(n * 4);
-  uint32_t* perm = reinterpret_cast<uint32_t*>(p); p += al256(n * 4);
+  int2* lr = reinterpret_cast<int2*>(p); p += al256(n * sizeof(int2));          // later: sorted windows
+  uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += al256(n * 4);           // later: permutation
+  int4* rec = reinterpret_cast<int4*>(p); p += al256(n * sizeof(int4));
+  uint32_t* perm = keys;
   uint32_t* cta_base = reinterpret_cast<uint32_t*>(p); p += al256(n_ctas(n) * kBuckets * 4);
   uint32_t* gcount = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   uint32_t* bstart = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
@@ -601,12 +605,12 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   Plan plan;
   plan.desc = reinterpret_cast<GroupDesc*>(p); p += al256(max_groups(n) * sizeof(GroupDesc));
   plan.gcnt = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
-  plan.singles = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
   plan.items = reinterpret_cast<uint2*>(p); p += al256(scratch_slots(n) * sizeof(uint2));
   plan.scratch = p; p += al256(scratch_slots(n) * 1024);
   plan.ctrs = reinterpret_cast<uint32_t*>(p);
   const int np = np_for(pk, P.cdt);
   plan.gsize = 32 * np;
+  plan.ngroups = (uint32_t)((n + plan.gsize - 1) / plan.gsize);
   const bool f32 = (P.cdt == FPE_R32 || P.cdt == FPE_C32);
   const size_t slot_bytes = (size_t)plan.gsize * (f32 ? sizeof(float2) : sizeof(double2));
   plan.cap = (uint32_t)(scratch_slots(n) * 1024 / slot_bytes);
@@ -619,7 +623,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     default: launch_classify_bucket_t<FPE_C32>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
   }
   st.mark("classify");
-  bucket_finish(keys, n, gcount, cta_base, bstart, istart, perm, lr, P.k_min, plan, s);
+  bucket_finish(keys, lr, n, gcount, cta_base, bstart, istart, rec, perm, P.k_min, plan, s);
   st.mark("bucket");
   int le = 0;
 #define FPE_EV(PKV, CKV) \

@@ -8,7 +8,8 @@
 //             claims each CTA's slice of every bucket with one global atomicAdd per nonzero bin;
 //             k_bucket_scan turns bucket totals into starts and enumerates work items (chunks of at
 //             most kChunkPts points of one bucket, long buckets first); k_bucket_scatter writes the
-//             permutation (contiguous runs per (CTA, bucket), so L2 merges the partial sectors).
+//             records {index, key, l, r} in bucket order (contiguous runs per (CTA, bucket), so L2
+//             merges the partial sectors).
 //   local   : k_chunk_sort sorts each chunk by the remaining low bits in shared memory (counting
 //             sort); k_plan cuts the sorted permutation into groups of 32*NP points and plans their
 //             work items.
@@ -76,10 +77,11 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(const uint32_t* __restrict
   }
 }
 
-__global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restrict__ keys, long long n,
+__global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restrict__ keys,
+                                                        const int2* __restrict__ lr, long long n,
                                                         const uint32_t* __restrict__ bstart,
                                                         const uint32_t* __restrict__ cta_base,
-                                                        uint32_t* __restrict__ perm) {
+                                                        int4* __restrict__ rec) {
   __shared__ uint32_t cnt[kBuckets];
   __shared__ uint32_t base[kBuckets];
   for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) {
@@ -90,20 +92,25 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restri
   const long long beg = (long long)blockIdx.x * kPtsPerCta;
   const long long end = min(n, beg + kPtsPerCta);
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    const uint32_t c = __ldg(keys + i) >> (24 - kCoarseBits);
+    const uint32_t key = __ldg(keys + i);
+    const int2 w = __ldg(lr + i);
+    const uint32_t c = key >> (24 - kCoarseBits);
     const uint32_t r = atomicAdd(&cnt[c], 1u);
-    perm[base[c] + r] = (uint32_t)i;
+    rec[base[c] + r] = make_int4((int)i, (int)key, w.x, w.y);
   }
 }
 
-// In-place counting sort of every chunk of the permutation by key bits [1, 1 + kLocalBits): afterwards
-// the whole permutation is ordered by key bits 1..23 (buckets are laid out in key order).
-__global__ void __launch_bounds__(256) k_chunk_sort(const uint32_t* __restrict__ keys, uint32_t* __restrict__ perm,
+// Counting sort of every chunk of the records by key bits [1, 1 + kLocalBits): afterwards the point
+// indices (perm) and their windows (slr) are ordered by key bits 1..23 (buckets are laid out in key
+// order), and every later pass reads them coalesced.
+__global__ void __launch_bounds__(256) k_chunk_sort(const int4* __restrict__ rec, uint32_t* __restrict__ perm,
+                                                    int2* __restrict__ slr,
                                                     const uint32_t* __restrict__ gcount,
                                                     const uint32_t* __restrict__ bstart,
                                                     const uint32_t* __restrict__ istart) {
   __shared__ uint32_t hist[1 << kLocalBits];
-  __shared__ uint32_t sorted[kChunkPts];
+  __shared__ uint32_t s_idx[kChunkPts];
+  __shared__ int2 s_lr[kChunkPts];
   const int c = blockIdx.x;
   if (c >= (int)istart[kBuckets]) return;
   int bucket, npts;
@@ -112,14 +119,15 @@ __global__ void __launch_bounds__(256) k_chunk_sort(const uint32_t* __restrict__
   for (int b = threadIdx.x; b < (1 << kLocalBits); b += blockDim.x) hist[b] = 0;
   __syncthreads();
   constexpr int kPer = kChunkPts / 256;
-  uint32_t my_idx[kPer], my_bin[kPer];
+  int4 my[kPer];
+  uint32_t my_bin[kPer];
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
     const int j = threadIdx.x + q * 256;
-    my_idx[q] = 0; my_bin[q] = 0;
+    my_bin[q] = 0;
     if (j < npts) {
-      my_idx[q] = perm[p0 + j];
-      my_bin[q] = (__ldg(keys + my_idx[q]) >> 1) & ((1u << kLocalBits) - 1);
+      my[q] = __ldg(rec + p0 + j);
+      my_bin[q] = ((uint32_t)my[q].y >> 1) & ((1u << kLocalBits) - 1);
       atomicAdd(&hist[my_bin[q]], 1u);
     }
   }
@@ -139,18 +147,25 @@ __global__ void __launch_bounds__(256) k_chunk_sort(const uint32_t* __restrict__
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
     const int j = threadIdx.x + q * 256;
-    if (j < npts) sorted[atomicAdd(&hist[my_bin[q]], 1u)] = my_idx[q];
+    if (j < npts) {
+      const uint32_t d = atomicAdd(&hist[my_bin[q]], 1u);
+      s_idx[d] = (uint32_t)my[q].x;
+      s_lr[d] = make_int2(my[q].z, my[q].w);
+    }
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < npts; j += 256) perm[p0 + j] = sorted[j];
+  for (int j = threadIdx.x; j < npts; j += 256) {
+    perm[p0 + j] = s_idx[j];
+    slr[p0 + j] = s_lr[j];
+  }
 }
 
 // The evaluator's work plan: groups of gsize consecutive points of the sorted permutation (across
 // bucket boundaries: neighbouring buckets hold neighbouring lambdas), one warp per group: the union
 // of the windows and either one single item (one warp, pieces in order) or npieces parallel items
 // with scratch slots for their partials (windows longer than kPiece).
-__global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ perm, long long n,
-                                              const int2* __restrict__ lr, long long k_min, Plan plan) {
+__global__ void __launch_bounds__(256) k_plan(long long n, const int2* __restrict__ slr, long long k_min,
+                                              Plan plan) {
   const int lane = threadIdx.x & 31;
   const long long g = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int gs = plan.gsize;
@@ -159,7 +174,7 @@ __global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ perm,
   const int count = (int)min((long long)gs, n - first);
   int lo = 0x7fffffff, hi = -1;
   for (int j = lane; j < count; j += 32) {
-    const int2 w2 = __ldg(lr + __ldg(perm + first + j));
+    const int2 w2 = __ldg(slr + first + j);
     if (w2.y >= w2.x) {
       lo = min(lo, (int)(w2.x - k_min));
       hi = max(hi, (int)(w2.y - k_min));
@@ -186,18 +201,19 @@ __global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ perm,
     }
   }
   plan.desc[g] = d;
-  if (single) plan.singles[atomicAdd(plan.ctrs + 3, 1u)] = (uint32_t)g;
+  (void)single;
 }
 
-void bucket_finish(const uint32_t* keys, long long n, const uint32_t* gcount, const uint32_t* cta_base,
-                   uint32_t* bstart, uint32_t* istart, uint32_t* perm, const int2* lr, long long k_min,
+void bucket_finish(const uint32_t* keys, int2* lr, long long n, const uint32_t* gcount, const uint32_t* cta_base,
+                   uint32_t* bstart, uint32_t* istart, int4* rec, uint32_t* perm, long long k_min,
                    const Plan& plan, cudaStream_t s) {
   k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, istart);
   const int ctas = (int)((n + kPtsPerCta - 1) / kPtsPerCta);
-  k_bucket_scatter<<<ctas, 256, 0, s>>>(keys, n, bstart, cta_base, perm);
-  k_chunk_sort<<<(int)max_chunks(n), 256, 0, s>>>(keys, perm, gcount, bstart, istart);
+  k_bucket_scatter<<<ctas, 256, 0, s>>>(keys, lr, n, bstart, cta_base, rec);
+  // perm and slr may alias keys and lr: k_chunk_sort reads only the records
+  k_chunk_sort<<<(int)max_chunks(n), 256, 0, s>>>(rec, perm, lr, gcount, bstart, istart);
   const long long groups = (n + plan.gsize - 1) / plan.gsize;
-  k_plan<<<(int)((groups + 7) / 8), 256, 0, s>>>(perm, n, lr, k_min, plan);
+  k_plan<<<(int)((groups + 7) / 8), 256, 0, s>>>(n, lr, k_min, plan);
 }
 
 }  // namespace fpe

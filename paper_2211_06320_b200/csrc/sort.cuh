@@ -28,11 +28,11 @@ struct Plan {
   GroupDesc* desc;        // [max_groups]
   uint32_t* gcnt;         // [max_groups] finished pieces of a multi-piece group
   uint2* items;           // [cap] (group, piece) of the parallel pieces; group = ~0u: unused slot
-  uint32_t* singles;      // [max_groups] groups evaluated by one warp (all their pieces in order)
-  uint32_t* ctrs;         // [0] multi fetch, [1] single fetch, [2] slots reserved, [3] singles
+  uint32_t* ctrs;         // [0] multi fetch, [1] group fetch, [2] slots reserved
   void* scratch;          // [cap][32*NP] piece partials (working complex type)
   uint32_t cap;           // scratch slots
   int gsize;              // points per group (32*NP)
+  uint32_t ngroups;       // ceil(n / gsize)
 };
 
 // Locate work-item chunk c (item order, long buckets first): its bucket, first position in the
@@ -46,10 +46,10 @@ __device__ __forceinline__ void chunk_of(const uint32_t* istart, const uint32_t*
   p0 = bstart[bucket] + off;
   npts = (int)min((uint32_t)kChunkPts, gcount[bucket] - off);
 }
-// bucket starts + item table (k_bucket_scan), the permutation (k_bucket_scatter), the in-chunk
-// order (k_chunk_sort) and the evaluator's work plan (k_plan)
-void bucket_finish(const uint32_t* keys, long long n, const uint32_t* gcount, const uint32_t* cta_base,
-                   uint32_t* bstart, uint32_t* istart, uint32_t* perm, const int2* lr, long long k_min,
+// bucket starts + item table (k_bucket_scan), records in bucket order (k_bucket_scatter), the sorted
+// permutation perm and windows (k_chunk_sort; written over keys and lr) and the work plan (k_plan)
+void bucket_finish(const uint32_t* keys, int2* lr, long long n, const uint32_t* gcount, const uint32_t* cta_base,
+                   uint32_t* bstart, uint32_t* istart, int4* rec, uint32_t* perm, long long k_min,
                    const Plan& plan, cudaStream_t s);
 inline long long max_chunks(long long n) { return (n + kChunkPts - 1) / kChunkPts + kBuckets; }
 inline long long max_groups(long long n) { return (n + 63) / 64; }   // groups of >= 64 points
