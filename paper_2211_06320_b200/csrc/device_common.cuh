@@ -131,6 +131,50 @@ __device__ __forceinline__ void classify_lambda(const int2* hull, int nv, int dr
   }
 }
 
+// The same searches with the cover vertices also staged as doubles hv[i] = (hk_i, hh_i): every vertex
+// predicate is then one fused multiply-add on exactly representable operands (|hk|, |hh| < 2^31), whose
+// single rounding preserves the sign of lambda I + J -- no integer products or conversions in the loops.
+__device__ __forceinline__ void classify_lambda_v(const int2* hull, const double2* hv, int nv, int drop, double lam,
+                                                  int& istar, int& l, int& r) {
+  if (isnan(lam)) { istar = -1; l = 0; r = -1; return; }
+  if (lam == -INFINITY) { istar = 0; l = r = hull[0].x; return; }
+  const int m = nv - 1;
+  int a = 0, b = m;
+  while (a < b) {
+    const int i = (a + b) >> 1;
+    const double2 v0 = hv[i], v1 = hv[i + 1];
+    if (__fma_rn(lam, v1.x - v0.x, v1.y - v0.y) <= 0.0) b = i; else a = i + 1;
+  }
+  istar = a;
+  const double2 vs = hv[a];
+  const double Dd = (double)drop;
+  a = 0; b = istar;
+  while (a < b) {
+    const int j = (a + b) >> 1;
+    const double2 v = hv[j];
+    if (__fma_rn(lam, v.x - vs.x, (v.y - vs.y) + Dd) >= 0.0) b = j; else a = j + 1;
+  }
+  const int2 vsi = hull[istar];
+  if (a == 0) {
+    l = hull[0].x;
+  } else {
+    const int2 A = hull[a - 1], B = hull[a];
+    l = (int)seg_first_true(A, B, vsi, drop, lam, (long long)A.x + 1, (long long)B.x);
+  }
+  a = istar; b = m;
+  while (a < b) {
+    const int j = (a + b + 1) >> 1;
+    const double2 v = hv[j];
+    if (__fma_rn(lam, v.x - vs.x, (v.y - vs.y) + Dd) >= 0.0) a = j; else b = j - 1;
+  }
+  if (a == m) {
+    r = hull[m].x;
+  } else {
+    const int2 A = hull[a], B = hull[a + 1];
+    r = (int)seg_last_true(A, B, vsi, drop, lam, (long long)A.x, (long long)B.x - 1);
+  }
+}
+
 __device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ a, int n, int key) {
   int lo = 0, hi = n;
   while (lo < hi) { int m = (lo + hi) >> 1; if (__ldg(a + m) < key) lo = m + 1; else hi = m; }

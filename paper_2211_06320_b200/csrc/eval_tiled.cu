@@ -64,34 +64,51 @@ __global__ void __launch_bounds__(256) k_classify_bucket(const void* __restrict_
                                                          uint32_t* __restrict__ cta_base,
                                                          fpe_diag* __restrict__ diag,
                                                          unsigned long long* __restrict__ hard_ctr) {
-  extern __shared__ int2 s_hull[];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
   __shared__ uint32_t hist[kBuckets];
   const int2* hull = P.hull;
-  if (P.nv <= kSmemHullMax) {
-    for (int i = threadIdx.x; i < P.nv; i += blockDim.x) s_hull[i] = P.hull[i];
-    hull = s_hull;
+  double2* hv = reinterpret_cast<double2*>(s_dyn);
+  const bool staged = P.nv <= kSmemHullDbl;
+  if (staged) {
+    int2* sh = reinterpret_cast<int2*>(s_dyn + (size_t)P.nv * sizeof(double2));
+    for (int i = threadIdx.x; i < P.nv; i += blockDim.x) {
+      const int2 v = P.hull[i];
+      sh[i] = v;
+      hv[i] = make_double2((double)v.x, (double)v.y);
+    }
+    hull = sh;
   }
   for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) hist[b] = 0;
   __syncthreads();
+  const int lane = threadIdx.x & 31;
   const long long beg = (long long)blockIdx.x * kPtsPerCta, end = min(n, beg + kPtsPerCta);
-  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    double x, y;
-    load_point<PK>(pts, i, x, y);
-    int hard;
-    double lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
-    int istar, l, r;
-    classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
-    lr[i] = make_int2(l, r);
-    uint32_t key = lambda_key(lam, l, r);
-    keys[i] = key;
-    atomicAdd(&hist[key >> (24 - kCoarseBits)], 1u);
-    if (diag) {
-      fpe_diag dg;
-      dg.lambda = lam; dg.region = istar; dg.l = l; dg.r = r;
-      dg.kept = kept_count(P, l, r); dg.hard = hard; dg.pad = 0;
-      diag[i] = dg;
+  for (long long i0 = beg + threadIdx.x; i0 - lane < end; i0 += blockDim.x) {
+    const long long i = i0;
+    const bool ok = i < end;
+    uint32_t key = 0xffffffffu;
+    if (ok) {
+      double x, y;
+      load_point<PK>(pts, i, x, y);
+      int hard;
+      double lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
+      int istar, l, r;
+      if (staged) classify_lambda_v(hull, hv, P.nv, P.drop, lam, istar, l, r);
+      else classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
+      lr[i] = make_int2(l, r);
+      key = lambda_key(lam, l, r);
+      keys[i] = key;
+      if (diag) {
+        fpe_diag dg;
+        dg.lambda = lam; dg.region = istar; dg.l = l; dg.r = r;
+        dg.kept = kept_count(P, l, r); dg.hard = hard; dg.pad = 0;
+        diag[i] = dg;
+      }
+      if (hard) atomicAdd(hard_ctr, 1ull);
     }
-    if (hard) atomicAdd(hard_ctr, 1ull);
+    // one shared-memory atomic per distinct bucket in the warp
+    const uint32_t c = ok ? key >> (24 - kCoarseBits) : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, c);
+    if (ok && lane == __ffs(peers) - 1) atomicAdd(&hist[c], (uint32_t)__popc(peers));
   }
   __syncthreads();
   // claim this CTA's slice of every bucket
@@ -360,30 +377,23 @@ struct Pts {
   bool valid[NP];
 };
 
-// Group g holds the sorted positions [g*32*NP, min(n, (g+1)*32*NP)) (k_plan), so its permutation
-// entries are loaded without waiting for the descriptor.
-template <int NP>
-__device__ __forceinline__ void load_group_idx(Pts<NP>& S, uint32_t g, long long n, const uint32_t* __restrict__ perm,
-                                               const int2* __restrict__ slr, int kmin) {
+// Group g holds the sorted positions [g*32*NP, min(n, (g+1)*32*NP)) (k_plan); its records (index,
+// window) are read coalesced and without waiting for the descriptor, then the points themselves.
+template <int PK, int NP>
+__device__ __forceinline__ void load_group(Pts<NP>& S, uint32_t g, long long n, const PtRec* __restrict__ rec,
+                                           const double2* __restrict__ zs, int kmin) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
     const long long pos = (long long)g * (32 * NP) + j * 32 + lane;
     S.valid[j] = pos < n;
-    S.idx[j] = 0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
+    S.idx[j] = 0; S.x[j] = 0.0; S.y[j] = 0.0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
     if (S.valid[j]) {
-      S.idx[j] = (long long)__ldg(perm + pos);
-      const int2 w = __ldg(slr + pos);
-      if (w.y >= w.x) { S.wl[j] = w.x - kmin; S.wr[j] = w.y - kmin; }
+      const int4 h = __ldg(reinterpret_cast<const int4*>(rec + pos));
+      const double2 z = __ldg(zs + pos);
+      S.idx[j] = h.x; S.x[j] = z.x; S.y[j] = z.y;
+      if (h.w >= h.z) { S.wl[j] = h.z - kmin; S.wr[j] = h.w - kmin; }
     }
-  }
-}
-template <int PK, int NP>
-__device__ __forceinline__ void load_group_pts(Pts<NP>& S, const void* __restrict__ pts) {
-#pragma unroll
-  for (int j = 0; j < NP; ++j) {
-    S.x[j] = 0.0; S.y[j] = 0.0;
-    if (S.valid[j]) load_point<PK>(pts, S.idx[j], S.x[j], S.y[j]);
   }
 }
 
@@ -398,29 +408,42 @@ __device__ __forceinline__ void eval_piece(Ring<CK>& R, const Pts<NP>& S, int rl
 }
 
 // One warp evaluates a whole group: the pieces of its union window top-down, folding as it goes.
-template <int PK, int CK, int OK, int NP>
-__device__ __forceinline__ void single_group(Ring<CK>& R, uint32_t g, long long n, const Plan& plan,
-                                             const uint32_t* __restrict__ perm, const void* __restrict__ pts,
-                                             const int2* __restrict__ lr, const PolyDev& P, void* vals,
-                                             long long* exps) {
+// The group's records and descriptor were loaded by the caller (one group ahead, so that their latency
+// hides behind the previous group's epilogue); `prefetch` is called once the coefficient stream is done
+// and before the epilogue, to issue the loads of the next group.
+template <int NP>
+struct GroupCtx {
+  uint32_t g;
+  GroupDesc d;
+  Pts<NP> S;
+};
+
+template <int PK, int NP>
+__device__ __forceinline__ void group_load(GroupCtx<NP>& c, uint32_t g, long long n, const Plan& plan,
+                                           const PtRec* __restrict__ rec, const double2* __restrict__ zs, int kmin) {
+  c.g = g;
+  if (g < plan.ngroups) {
+    c.d = plan.desc[g];
+    load_group<PK, NP>(c.S, g, n, rec, zs, kmin);
+  }
+}
+
+template <int PK, int CK, int OK, int NP, typename Prefetch>
+__device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c, const PolyDev& P, void* vals,
+                                             long long* exps, Prefetch prefetch) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
-  const int kmin = (int)P.k_min;
-  const GroupDesc d = plan.desc[g];
-  if (d.npieces > 1) return;   // evaluated as parallel pieces (multi_piece)
-  Pts<NP> S;
-  load_group_idx<NP>(S, g, n, perm, lr, kmin);
+  const GroupDesc& d = c.d;
+  const Pts<NP>& S = c.S;
   const bool nonempty = d.hi >= d.lo;
   const int p_hi = nonempty ? d.hi / kPiece : 0, p_lo = nonempty ? d.lo / kPiece : 0;
-  if (nonempty) ring_begin(R, max(d.lo, p_hi * kPiece), d.hi);   // coefficients in flight during the loads
-  load_group_pts<PK, NP>(S, pts);
   Acc A[NP];
 #pragma unroll
   for (int j = 0; j < NP; ++j) A[j] = Acc{0.0, 0.0, 0, false};
   if (nonempty) {
     for (int p = p_hi; p >= p_lo; --p) {
       const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
-      if (p != p_hi) ring_begin(R, rlo, rhi);
+      ring_begin(R, rlo, rhi);
       W br[NP], bi[NP];
       eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, br, bi);
 #pragma unroll
@@ -429,6 +452,7 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, uint32_t g, long long 
           acc_fold<CPLX>(A[j], (double)br[j], (double)bi[j], max(S.wl[j], p * kPiece), S.x[j], S.y[j]);
     }
   }
+  prefetch();
 #pragma unroll
   for (int j = 0; j < NP; ++j)
     if (S.valid[j]) finalize<OK, CPLX>(vals, exps, S.idx[j], S.x[j], S.y[j], A[j], P);
@@ -438,8 +462,8 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, uint32_t g, long long 
 // the group's last piece folds all partials in order and finalises.
 template <int PK, int CK, int OK, int NP>
 __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long long n, const Plan& plan,
-                                            const uint32_t* __restrict__ perm, const void* __restrict__ pts,
-                                            const int2* __restrict__ lr, const PolyDev& P, void* vals,
+                                            const PtRec* __restrict__ rec, const double2* __restrict__ zs,
+                                            const PolyDev& P, void* vals,
                                             long long* exps) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
@@ -451,8 +475,7 @@ __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long
   const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
   ring_begin(R, rlo, rhi);
   Pts<NP> S;
-  load_group_idx<NP>(S, g, n, perm, lr, kmin);
-  load_group_pts<PK, NP>(S, pts);
+  load_group<PK, NP>(S, g, n, rec, zs, kmin);
   W br[NP], bi[NP];
   eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, br, bi);
   const int p0 = d.lo / kPiece;
@@ -493,9 +516,8 @@ constexpr size_t ring_bytes() {
 // Persistent evaluator: every warp first takes parallel pieces of long windows, then whole groups,
 // both from global atomic counters (largest work first; the tail is at most one group).
 template <int PK, int CK, int OK, int NP>
-__global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const void* __restrict__ pts, long long n, PolyDev P,
-                                                               const int2* __restrict__ lr,   // sorted windows
-                                                               const uint32_t* __restrict__ perm, Plan plan,
+__global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const double2* __restrict__ zs, long long n, PolyDev P,
+                                                               const PtRec* __restrict__ rec, Plan plan,
                                                                void* __restrict__ vals, long long* __restrict__ exps) {
   using CT = typename Step<CK>::CT;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -518,14 +540,23 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const void* __res
     if (lane == 0) nxt = atomicAdd(plan.ctrs + 0, 1u);
     const uint2 item = plan.items[it];
     if (item.x == ~0u) continue;
-    multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, perm, pts, lr, P, vals, exps);
+    multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, rec, zs, P, vals, exps);
   }
+  // groups: software-pipelined one group ahead (the next group's records load during this epilogue)
+  const int kmin = (int)P.k_min;
   if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
-  for (;;) {
-    const uint32_t g = __shfl_sync(0xffffffffu, nxt, 0);
-    if (g >= plan.ngroups) break;
-    if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
-    single_group<PK, CK, OK, NP>(R, g, n, plan, perm, pts, lr, P, vals, exps);
+  GroupCtx<NP> cur;
+  group_load<PK, NP>(cur, __shfl_sync(0xffffffffu, nxt, 0), n, plan, rec, zs, kmin);
+  if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
+  while (cur.g < plan.ngroups) {
+    GroupCtx<NP> nx;
+    auto fetch_next = [&]() {
+      group_load<PK, NP>(nx, __shfl_sync(0xffffffffu, nxt, 0), n, plan, rec, zs, kmin);
+      if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
+    };
+    if (cur.d.npieces > 1) fetch_next();   // evaluated as parallel pieces (multi_piece)
+    else single_group<PK, CK, OK, NP>(R, cur, P, vals, exps, fetch_next);
+    cur = nx;
   }
 }
 
@@ -541,7 +572,7 @@ static size_t scratch_slots(long long n) {
 }
 
 size_t tiled_ws_bytes(long long n) {
-  return al256(n * sizeof(int2)) + al256(n * sizeof(uint32_t)) + al256(n * sizeof(int4)) +
+  return al256(n * sizeof(int2)) + al256(n * sizeof(uint32_t)) + al256(n * sizeof(PtRec)) + al256(n * sizeof(double2)) +
          al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 3 * al256((kBuckets + 1) * sizeof(uint32_t)) +
          al256(max_groups(n) * sizeof(GroupDesc)) + al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
@@ -553,8 +584,8 @@ static size_t eval_smem() {
 }
 
 template <int PK, int CK, int OK, int NP>
-static int launch_eval_tiled_t(const void* pts, long long n, const PolyDev& P, const int2* lr, const uint32_t* perm,
-                               const Plan& plan, void* vals, long long* exps, cudaStream_t s) {
+static int launch_eval_tiled_t(const double2* zs, long long n, const PolyDev& P, const PtRec* rec, const Plan& plan, void* vals,
+                               long long* exps, cudaStream_t s) {
   static int grid = 0;
   const size_t smem = eval_smem<CK>();
   if (grid == 0) {
@@ -565,7 +596,7 @@ static int launch_eval_tiled_t(const void* pts, long long n, const PolyDev& P, c
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid = max(1, per_sm) * sms;
   }
-  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(pts, n, P, lr, perm, plan, vals, exps);
+  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(zs, n, P, rec, plan, vals, exps);
   return 1;
 }
 
@@ -587,7 +618,7 @@ template <int PK>
 static void launch_classify_bucket_t(const void* pts, long long n, const PolyDev& P, int2* lr, uint32_t* keys,
                                      uint32_t* gcount, uint32_t* cta_base, fpe_diag* diag, unsigned long long* hard,
                                      cudaStream_t s) {
-  size_t smem = P.nv <= kSmemHullMax ? P.nv * sizeof(int2) : 0;
+  size_t smem = P.nv <= kSmemHullDbl ? P.nv * (sizeof(int2) + sizeof(double2)) : 0;
   k_classify_bucket<PK><<<(int)n_ctas(n), 256, smem, s>>>(pts, n, P, lr, keys, gcount, cta_base, diag, hard);
 }
 
@@ -595,9 +626,9 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
               fpe_diag* diag, void* ws, unsigned long long* hard, Stage& st, cudaStream_t s) {
   char* p = static_cast<char*>(ws);
   int2* lr = reinterpret_cast<int2*>(p); p += al256(n * sizeof(int2));          // later: sorted windows
-  uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += al256(n * 4);           // later: permutation
-  int4* rec = reinterpret_cast<int4*>(p); p += al256(n * sizeof(int4));
-  uint32_t* perm = keys;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += al256(n * 4);
+  PtRec* rec = reinterpret_cast<PtRec*>(p); p += al256(n * sizeof(PtRec));
+  double2* zs = reinterpret_cast<double2*>(p); p += al256(n * sizeof(double2));   // points in sorted order
   uint32_t* cta_base = reinterpret_cast<uint32_t*>(p); p += al256(n_ctas(n) * kBuckets * 4);
   uint32_t* gcount = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   uint32_t* bstart = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
@@ -623,11 +654,11 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     default: launch_classify_bucket_t<FPE_C32>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
   }
   st.mark("classify");
-  bucket_finish(keys, lr, n, gcount, cta_base, bstart, istart, rec, perm, P.k_min, plan, s);
+  bucket_finish(keys, lr, n, gcount, cta_base, bstart, istart, rec, pk, pts, zs, P.k_min, plan, s);
   st.mark("bucket");
   int le = 0;
 #define FPE_EV(PKV, CKV) \
-  le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(pts, n, P, lr, perm, plan, vals, exps, s)
+  le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(zs, n, P, rec, plan, vals, exps, s)
   switch (pk * 4 + P.cdt) {
     case FPE_R64 * 4 + FPE_R64: FPE_EV(FPE_R64, FPE_R64); break;
     case FPE_R64 * 4 + FPE_C64: FPE_EV(FPE_R64, FPE_C64); break;

@@ -5,6 +5,7 @@
 
 namespace fpe {
 constexpr int kSmemHullMax = 6144;   // cover vertices staged in shared memory (48 KiB)
+constexpr int kSmemHullDbl = 1536;   // ... also as doubles (36 KiB) by the bucketing classifier
 
 void launch_classify(int pk, const void* pts, long long n, const PolyDev& P, int2* lr, fpe_diag* diag,
                      unsigned long long* hard, cudaStream_t s);

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include "sort.cuh"
+#include "fpe_internal.h"
 
 namespace fpe {
 
@@ -77,11 +78,13 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(const uint32_t* __restrict
   }
 }
 
+// Records to bucket positions.  Lanes of a warp that hit the same bucket are aggregated
+// (__match_any_sync) so that each distinct bucket costs one shared-memory atomic per warp.
 __global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restrict__ keys,
                                                         const int2* __restrict__ lr, long long n,
                                                         const uint32_t* __restrict__ bstart,
                                                         const uint32_t* __restrict__ cta_base,
-                                                        int4* __restrict__ rec) {
+                                                        PtRec* __restrict__ rec) {
   __shared__ uint32_t cnt[kBuckets];
   __shared__ uint32_t base[kBuckets];
   for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) {
@@ -89,28 +92,57 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restri
     base[b] = bstart[b] + cta_base[(size_t)blockIdx.x * kBuckets + b];
   }
   __syncthreads();
+  const int lane = threadIdx.x & 31;
   const long long beg = (long long)blockIdx.x * kPtsPerCta;
   const long long end = min(n, beg + kPtsPerCta);
-  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    const uint32_t key = __ldg(keys + i);
-    const int2 w = __ldg(lr + i);
-    const uint32_t c = key >> (24 - kCoarseBits);
-    const uint32_t r = atomicAdd(&cnt[c], 1u);
-    rec[base[c] + r] = make_int4((int)i, (int)key, w.x, w.y);
+  constexpr int U = 4;   // independent loads in flight per thread
+  for (long long i0 = beg + threadIdx.x; i0 - lane < end; i0 += (long long)U * blockDim.x) {
+    uint32_t key[U];
+    int2 w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + (long long)u * blockDim.x;
+      key[u] = 0xffffffffu;
+      if (i < end) { key[u] = __ldg(keys + i); w[u] = __ldg(lr + i); }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + (long long)u * blockDim.x;
+      const bool ok = i < end;
+      const uint32_t c = ok ? key[u] >> (24 - kCoarseBits) : 0xffffffffu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, c);
+      const int leader = __ffs(peers) - 1;
+      const uint32_t rank = __popc(peers & ((1u << lane) - 1));
+      uint32_t r0 = 0;
+      if (ok && lane == leader) r0 = atomicAdd(&cnt[c], (uint32_t)__popc(peers));
+      r0 = __shfl_sync(0xffffffffu, r0, leader);
+      if (ok) rec[base[c] + r0 + rank] = PtRec{(int32_t)i, key[u], w[u].x, w[u].y};
+    }
   }
 }
 
-// Counting sort of every chunk of the records by key bits [1, 1 + kLocalBits): afterwards the point
-// indices (perm) and their windows (slr) are ordered by key bits 1..23 (buckets are laid out in key
-// order), and every later pass reads them coalesced.
-__global__ void __launch_bounds__(256) k_chunk_sort(const int4* __restrict__ rec, uint32_t* __restrict__ perm,
-                                                    int2* __restrict__ slr,
+__device__ __forceinline__ double2 load_point_any(int pk, const void* __restrict__ p, long long i) {
+  switch (pk) {
+    case FPE_R64: return make_double2(__ldg(static_cast<const double*>(p) + i), 0.0);
+    case FPE_C64: return __ldg(static_cast<const double2*>(p) + i);
+    case FPE_R32: return make_double2((double)__ldg(static_cast<const float*>(p) + i), 0.0);
+    default: { const float2 v = __ldg(static_cast<const float2*>(p) + i); return make_double2(v.x, v.y); }
+  }
+}
+
+// Counting sort of every chunk of the records by key bits [1, 1 + kLocalBits), in place: afterwards the
+// records (and the windows slr, for the planner) are ordered by key bits 1..23 (buckets are laid out in
+// key order); the points are gathered into the same order (zs, as doubles), so that every later pass
+// reads them coalesced.
+constexpr size_t kChunkSortSmem = (size_t)kChunkPts * sizeof(PtRec) + (1u << kLocalBits) * sizeof(uint32_t);
+__global__ void __launch_bounds__(256) k_chunk_sort(PtRec* __restrict__ rec, int2* __restrict__ slr,
+                                                    int pk, const void* __restrict__ pts, double2* __restrict__ zs,
                                                     const uint32_t* __restrict__ gcount,
                                                     const uint32_t* __restrict__ bstart,
                                                     const uint32_t* __restrict__ istart) {
-  __shared__ uint32_t hist[1 << kLocalBits];
-  __shared__ uint32_t s_idx[kChunkPts];
-  __shared__ int2 s_lr[kChunkPts];
+  extern __shared__ __align__(16) unsigned char sm[];
+  PtRec* s_rec = reinterpret_cast<PtRec*>(sm);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sm + (size_t)kChunkPts * sizeof(PtRec));
   const int c = blockIdx.x;
   if (c >= (int)istart[kBuckets]) return;
   int bucket, npts;
@@ -119,15 +151,15 @@ __global__ void __launch_bounds__(256) k_chunk_sort(const int4* __restrict__ rec
   for (int b = threadIdx.x; b < (1 << kLocalBits); b += blockDim.x) hist[b] = 0;
   __syncthreads();
   constexpr int kPer = kChunkPts / 256;
-  int4 my[kPer];
   uint32_t my_bin[kPer];
+  int4 my_h[kPer];
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
     const int j = threadIdx.x + q * 256;
     my_bin[q] = 0;
     if (j < npts) {
-      my[q] = __ldg(rec + p0 + j);
-      my_bin[q] = ((uint32_t)my[q].y >> 1) & ((1u << kLocalBits) - 1);
+      my_h[q] = __ldg(reinterpret_cast<const int4*>(rec + p0 + j));
+      my_bin[q] = ((uint32_t)my_h[q].y >> 1) & ((1u << kLocalBits) - 1);
       atomicAdd(&hist[my_bin[q]], 1u);
     }
   }
@@ -149,14 +181,24 @@ __global__ void __launch_bounds__(256) k_chunk_sort(const int4* __restrict__ rec
     const int j = threadIdx.x + q * 256;
     if (j < npts) {
       const uint32_t d = atomicAdd(&hist[my_bin[q]], 1u);
-      s_idx[d] = (uint32_t)my[q].x;
-      s_lr[d] = make_int2(my[q].z, my[q].w);
+      reinterpret_cast<int4*>(s_rec + d)[0] = my_h[q];
     }
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < npts; j += 256) {
-    perm[p0 + j] = s_idx[j];
-    slr[p0 + j] = s_lr[j];
+  double2 z[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {   // gathers issued together (independent random loads)
+    const int j = threadIdx.x + q * 256;
+    if (j < npts) z[q] = load_point_any(pk, pts, s_rec[j].idx);
+  }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int j = threadIdx.x + q * 256;
+    if (j < npts) {
+      rec[p0 + j] = s_rec[j];
+      slr[p0 + j] = make_int2(s_rec[j].l, s_rec[j].r);
+      zs[p0 + j] = z[q];
+    }
   }
 }
 
@@ -204,14 +246,19 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const int2* __restric
   (void)single;
 }
 
-void bucket_finish(const uint32_t* keys, int2* lr, long long n, const uint32_t* gcount, const uint32_t* cta_base,
-                   uint32_t* bstart, uint32_t* istart, int4* rec, uint32_t* perm, long long k_min,
-                   const Plan& plan, cudaStream_t s) {
+void bucket_finish(const uint32_t* keys, int2* lr, long long n, const uint32_t* gcount,
+                   const uint32_t* cta_base, uint32_t* bstart, uint32_t* istart, PtRec* rec, int pk,
+                   const void* pts, double2* zs, long long k_min, const Plan& plan, cudaStream_t s) {
   k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, istart);
   const int ctas = (int)((n + kPtsPerCta - 1) / kPtsPerCta);
   k_bucket_scatter<<<ctas, 256, 0, s>>>(keys, lr, n, bstart, cta_base, rec);
-  // perm and slr may alias keys and lr: k_chunk_sort reads only the records
-  k_chunk_sort<<<(int)max_chunks(n), 256, 0, s>>>(rec, perm, lr, gcount, bstart, istart);
+  // the sorted windows are written over lr: k_chunk_sort reads only the records
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_chunk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChunkSortSmem);
+    attr = true;
+  }
+  k_chunk_sort<<<(int)max_chunks(n), 256, kChunkSortSmem, s>>>(rec, lr, pk, pts, zs, gcount, bstart, istart);
   const long long groups = (n + plan.gsize - 1) / plan.gsize;
   k_plan<<<(int)((groups + 7) / 8), 256, 0, s>>>(n, lr, k_min, plan);
 }

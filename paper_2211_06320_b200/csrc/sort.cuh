@@ -13,6 +13,13 @@ constexpr int kPiece = 16384;                   // absolute coefficient pieces: 
                                                 // of kPiece (relative to k_min) and the piece partials are
                                                 // combined top-down, so results never depend on the batch
 
+// A point's record in bucket / sorted order: index, sort key, window [l, r] (absolute).
+struct __align__(16) PtRec {
+  int32_t idx;
+  uint32_t key;
+  int32_t l, r;
+};
+
 // A group: 32*NP consecutive points of the sorted permutation, evaluated by one warp (NP points per
 // lane) over the union [lo, hi] of their windows (relative to k_min; hi < lo: no finite point).
 struct GroupDesc {
@@ -46,11 +53,12 @@ __device__ __forceinline__ void chunk_of(const uint32_t* istart, const uint32_t*
   p0 = bstart[bucket] + off;
   npts = (int)min((uint32_t)kChunkPts, gcount[bucket] - off);
 }
-// bucket starts + item table (k_bucket_scan), records in bucket order (k_bucket_scatter), the sorted
-// permutation perm and windows (k_chunk_sort; written over keys and lr) and the work plan (k_plan)
-void bucket_finish(const uint32_t* keys, int2* lr, long long n, const uint32_t* gcount, const uint32_t* cta_base,
-                   uint32_t* bstart, uint32_t* istart, int4* rec, uint32_t* perm, long long k_min,
-                   const Plan& plan, cudaStream_t s);
+// bucket starts + item table (k_bucket_scan), records in bucket order (k_bucket_scatter), the records
+// sorted in place, their windows (written over lr) and points (zs) in sorted order (k_chunk_sort), and the
+// work plan (k_plan)
+void bucket_finish(const uint32_t* keys, int2* lr, long long n, const uint32_t* gcount,
+                   const uint32_t* cta_base, uint32_t* bstart, uint32_t* istart, PtRec* rec, int pk,
+                   const void* pts, double2* zs, long long k_min, const Plan& plan, cudaStream_t s);
 inline long long max_chunks(long long n) { return (n + kChunkPts - 1) / kChunkPts + kBuckets; }
 inline long long max_groups(long long n) { return (n + 63) / 64; }   // groups of >= 64 points
 }  // namespace fpe
