@@ -80,6 +80,13 @@ fpe::PolyDev fpe_poly_s::view() const {
   P.k_min = hdr.k_min; P.k_max = hdr.k_max; P.n_good = hdr.n_good;
   P.nv = (int)hdr.n_hull; P.drop = hdr.drop; P.shift = hdr.shift;
   P.sparse = hdr.sparse; P.all_good = hdr.all_good; P.cdt = hdr.dtype;
+  long long hmin = 0, hmax = 0;
+  for (size_t i = 0; i < hh.size(); ++i) {
+    hmin = i ? std::min<long long>(hmin, hh[i]) : hh[i];
+    hmax = i ? std::max<long long>(hmax, hh[i]) : hh[i];
+  }
+  const long long deff = hdr.k_max - hdr.k_min;
+  P.dbl_ok = deff < (1ll << 26) && (2 * (hmax - hmin) + hdr.drop) * (deff + 1) < (1ll << 52);
   return P;
 }
 

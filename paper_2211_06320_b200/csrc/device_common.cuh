@@ -35,6 +35,14 @@ __device__ __forceinline__ bool band_vertex(const int2* hull, int j, int2 vs, in
   int2 v = hull[j];
   return sign_lin(lam, (long long)v.x - vs.x, (long long)v.y - vs.y + drop) >= 0;
 }
+// The same predicate in doubles: exact when every |I|, |J| < 2^53 (PolyDev::dbl_ok, checked per polynomial):
+// the products are exact integers and the fused multiply-add rounds lambda I + J once.
+__device__ __forceinline__ bool band_seg_d(int2 a, int2 b, int2 vs, int drop, double lam, long long k) {
+  const double dk = (double)(b.x - a.x), dh = (double)(b.y - a.y);
+  const double J = __fma_rn(dh, (double)(k - a.x), (double)(a.y - vs.y + drop) * dk);
+  const double I = (double)(k - vs.x) * dk;
+  return __fma_rn(lam, I, J) >= 0.0;
+}
 __device__ __forceinline__ bool band_seg(int2 a, int2 b, int2 vs, int drop, double lam, long long k) {
   long long dk = (long long)b.x - a.x, dh = (long long)b.y - a.y;
   long long J = ((long long)a.y - vs.y + drop) * dk + dh * (k - a.x);
@@ -45,6 +53,7 @@ __device__ __forceinline__ bool band_seg(int2 a, int2 b, int2 vs, int drop, doub
 // Least k in [lo, hi] with band_seg(A, B, ...) true, given that it holds at hi and the predicate
 // is monotone on the segment (left branch: increasing).  The sheared cover is affine on the
 // segment, F(k) = c0 + c1 k, so the crossing is estimated in fp64 and then verified exactly.
+template <bool DBL = false>
 __device__ __forceinline__ long long seg_first_true(int2 A, int2 B, int2 vs, int drop, double lam,
                                                     long long lo, long long hi) {
   // F(A.x + t) = dk g + t c1,  g = (A.y - vs.y + D) + lambda (A.x - vs.x),  c1 = dh + lambda dk
@@ -59,19 +68,20 @@ __device__ __forceinline__ long long seg_first_true(int2 A, int2 B, int2 vs, int
   }
   // exact adjustment; a bounded number of steps, else bisection
   for (int it = 0; it < 4; ++it) {
-    const bool t = band_seg(A, B, vs, drop, lam, k);
+    const bool t = (DBL ? band_seg_d(A, B, vs, drop, lam, k) : band_seg(A, B, vs, drop, lam, k));
     if (t) {
-      if (k == lo || !band_seg(A, B, vs, drop, lam, k - 1)) return k;
+      if (k == lo || !(DBL ? band_seg_d(A, B, vs, drop, lam, k - 1) : band_seg(A, B, vs, drop, lam, k - 1))) return k;
       --k;
     } else {
       ++k;
     }
   }
   long long a = lo, b = hi;
-  while (a < b) { long long m = (a + b) >> 1; if (band_seg(A, B, vs, drop, lam, m)) b = m; else a = m + 1; }
+  while (a < b) { long long m = (a + b) >> 1; if ((DBL ? band_seg_d(A, B, vs, drop, lam, m) : band_seg(A, B, vs, drop, lam, m))) b = m; else a = m + 1; }
   return a;
 }
 // Greatest k in [lo, hi] with the predicate true, given that it holds at lo (right branch: decreasing).
+template <bool DBL = false>
 __device__ __forceinline__ long long seg_last_true(int2 A, int2 B, int2 vs, int drop, double lam,
                                                    long long lo, long long hi) {
   const double dk = (double)(B.x - A.x), dh = (double)(B.y - A.y);
@@ -84,16 +94,16 @@ __device__ __forceinline__ long long seg_last_true(int2 A, int2 B, int2 vs, int 
     else if (e > (double)hi) k = hi;
   }
   for (int it = 0; it < 4; ++it) {
-    const bool t = band_seg(A, B, vs, drop, lam, k);
+    const bool t = (DBL ? band_seg_d(A, B, vs, drop, lam, k) : band_seg(A, B, vs, drop, lam, k));
     if (t) {
-      if (k == hi || !band_seg(A, B, vs, drop, lam, k + 1)) return k;
+      if (k == hi || !(DBL ? band_seg_d(A, B, vs, drop, lam, k + 1) : band_seg(A, B, vs, drop, lam, k + 1))) return k;
       ++k;
     } else {
       --k;
     }
   }
   long long a = lo, b = hi;
-  while (a < b) { long long m = (a + b + 1) >> 1; if (band_seg(A, B, vs, drop, lam, m)) a = m; else b = m - 1; }
+  while (a < b) { long long m = (a + b + 1) >> 1; if ((DBL ? band_seg_d(A, B, vs, drop, lam, m) : band_seg(A, B, vs, drop, lam, m))) a = m; else b = m - 1; }
   return a;
 }
 
@@ -134,6 +144,7 @@ __device__ __forceinline__ void classify_lambda(const int2* hull, int nv, int dr
 // The same searches with the cover vertices also staged as doubles hv[i] = (hk_i, hh_i): every vertex
 // predicate is then one fused multiply-add on exactly representable operands (|hk|, |hh| < 2^31), whose
 // single rounding preserves the sign of lambda I + J -- no integer products or conversions in the loops.
+template <bool DBL>
 __device__ __forceinline__ void classify_lambda_v(const int2* hull, const double2* hv, int nv, int drop, double lam,
                                                   int& istar, int& l, int& r) {
   if (isnan(lam)) { istar = -1; l = 0; r = -1; return; }
@@ -159,7 +170,7 @@ __device__ __forceinline__ void classify_lambda_v(const int2* hull, const double
     l = hull[0].x;
   } else {
     const int2 A = hull[a - 1], B = hull[a];
-    l = (int)seg_first_true(A, B, vsi, drop, lam, (long long)A.x + 1, (long long)B.x);
+    l = (int)seg_first_true<DBL>(A, B, vsi, drop, lam, (long long)A.x + 1, (long long)B.x);
   }
   a = istar; b = m;
   while (a < b) {
@@ -171,7 +182,7 @@ __device__ __forceinline__ void classify_lambda_v(const int2* hull, const double
     r = hull[m].x;
   } else {
     const int2 A = hull[a], B = hull[a + 1];
-    r = (int)seg_last_true(A, B, vsi, drop, lam, (long long)A.x, (long long)B.x - 1);
+    r = (int)seg_last_true<DBL>(A, B, vsi, drop, lam, (long long)A.x, (long long)B.x - 1);
   }
 }
 

@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(256) k_classify_bucket(const void* __restrict_
       int hard;
       double lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
       int istar, l, r;
-      if (staged) classify_lambda_v(hull, hv, P.nv, P.drop, lam, istar, l, r);
+      if (staged && P.dbl_ok) classify_lambda_v<true>(hull, hv, P.nv, P.drop, lam, istar, l, r);
+      else if (staged) classify_lambda_v<false>(hull, hv, P.nv, P.drop, lam, istar, l, r);
       else classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
       lr[i] = make_int2(l, r);
       key = lambda_key(lam, l, r);
@@ -412,29 +413,54 @@ __device__ __forceinline__ void eval_piece(Ring<CK>& R, const Pts<NP>& S, int rl
 // hides behind the previous group's epilogue); `prefetch` is called once the coefficient stream is done
 // and before the epilogue, to issue the loads of the next group.
 template <int NP>
-struct GroupCtx {
+struct GroupCtx {   // raw loads of a group, consumed only when the group is evaluated
   uint32_t g;
   GroupDesc d;
-  Pts<NP> S;
+  int4 h[NP];
+  double2 z[NP];
 };
 
 template <int PK, int NP>
 __device__ __forceinline__ void group_load(GroupCtx<NP>& c, uint32_t g, long long n, const Plan& plan,
                                            const PtRec* __restrict__ rec, const double2* __restrict__ zs, int kmin) {
+  const int lane = threadIdx.x & 31;
   c.g = g;
   if (g < plan.ngroups) {
     c.d = plan.desc[g];
-    load_group<PK, NP>(c.S, g, n, rec, zs, kmin);
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const long long pos = (long long)g * (32 * NP) + j * 32 + lane;
+      if (pos < n) {
+        c.h[j] = __ldg(reinterpret_cast<const int4*>(rec + pos));
+        c.z[j] = __ldg(zs + pos);
+      }
+    }
+  }
+}
+
+template <int NP>
+__device__ __forceinline__ void group_unpack(Pts<NP>& S, const GroupCtx<NP>& c, long long n, int kmin) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    const long long pos = (long long)c.g * (32 * NP) + j * 32 + lane;
+    S.valid[j] = pos < n;
+    S.idx[j] = 0; S.x[j] = 0.0; S.y[j] = 0.0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
+    if (S.valid[j]) {
+      S.idx[j] = c.h[j].x; S.x[j] = c.z[j].x; S.y[j] = c.z[j].y;
+      if (c.h[j].w >= c.h[j].z) { S.wl[j] = c.h[j].z - kmin; S.wr[j] = c.h[j].w - kmin; }
+    }
   }
 }
 
 template <int PK, int CK, int OK, int NP, typename Prefetch>
-__device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c, const PolyDev& P, void* vals,
-                                             long long* exps, Prefetch prefetch) {
+__device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c, long long n, const PolyDev& P,
+                                             void* vals, long long* exps, Prefetch prefetch) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
-  const GroupDesc& d = c.d;
-  const Pts<NP>& S = c.S;
+  const GroupDesc d = c.d;
+  Pts<NP> S;
+  group_unpack<NP>(S, c, n, (int)P.k_min);
   const bool nonempty = d.hi >= d.lo;
   const int p_hi = nonempty ? d.hi / kPiece : 0, p_lo = nonempty ? d.lo / kPiece : 0;
   Acc A[NP];
@@ -555,7 +581,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const double2* __
       if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
     };
     if (cur.d.npieces > 1) fetch_next();   // evaluated as parallel pieces (multi_piece)
-    else single_group<PK, CK, OK, NP>(R, cur, P, vals, exps, fetch_next);
+    else single_group<PK, CK, OK, NP>(R, cur, n, P, vals, exps, fetch_next);
     cur = nx;
   }
 }

@@ -39,6 +39,7 @@ struct PolyDev {
   const int32_t* sidx;
   long long k_min, k_max, n_good;
   int nv, drop, shift, sparse, all_good, cdt;
+  int dbl_ok;   // band predicates exact in doubles: d_eff < 2^26 and (2 H + D) d_eff < 2^52
 };
 
 }  // namespace fpe
