@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the context measurements (full Horner, the other BASELINE configs)")
     return ap.parse_args()
 
 
@@ -157,6 +159,83 @@ def cpu_baseline(cfg: int, sample: int):
             "sample": f"{sample} points of cfg{cfg} (same distribution, shard 977): binary128 classify + "
                       f"Q_lambda; preconditioning {t_pre:.2f}s not included",
             "seconds": dt}
+
+
+def _time_ms(fn, steps: int, warmup: int) -> float:
+    """Mean device time of fn() in ms (CUDA events on the current stream, synchronised)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def extra_context(device: int, steps: int = 3):
+    """Context numbers on 1 GPU (north_star): the full-Horner kernel on the headline workload, and the
+    other BASELINE configs (evals/s through fpe_evaluate, algorithmic fp64/fp32 FMA rate from a
+    2^20-point diagnostic subsample).  Each entry is independent; a failure is recorded, not raised."""
+    import numpy as np
+    import torch
+
+    import paper_2211_06320_b200 as fpe
+    import workloads
+    dev = torch.device("cuda", device)
+    out = {}
+    try:   # full Horner, cfg3 polynomial (d = 2^20 - 1), 2^14 sphere points
+        poly = fpe.precondition(workloads.coefficients(3), device=device)
+        pts = torch.from_numpy(workloads.points(3, 1 << 14, shard=5)).to(dev)
+        ms = _time_ms(lambda: poly.horner(pts), steps, 1)
+        fma = 4.0 * (poly.info["k_max"] - poly.info["k_min"] + 1) * pts.numel()
+        out["full_horner_cfg3"] = {"evals_per_s": pts.numel() / (ms * 1e-3), "ms": ms, "points": pts.numel(),
+                                   "fma_per_s": fma / (ms * 1e-3)}
+        del poly, pts
+    except Exception as e:  # noqa: BLE001
+        out["full_horner_cfg3"] = {"error": repr(e)[:200]}
+    specs = [(1, None, False), (2, None, False), (4, None, False), (5, None, False), (5, None, True)]
+    for cfg, n, fp32 in specs:
+        name = f"cfg{cfg}" + ("_fp32" if fp32 else "")
+        try:
+            c = workloads.CONFIGS[cfg]
+            n = n or c["n_points"]
+            a = workloads.coefficients(cfg)
+            p = workloads.points(cfg, n)
+            if fp32:
+                a, p = workloads.to_fp32(a), workloads.to_fp32(p)
+            poly = fpe.precondition(a, device=device)
+            pts = torch.from_numpy(p).to(dev)
+            del p
+            sub = pts[: min(n, 1 << 20)]
+            _, _, dg = poly.evaluate(sub, exps=True, diag=True)
+            D = fpe.diag_fields(dg)
+            cplx = np.iscomplexobj(a)
+            work_pt = algorithmic_fma(D, cplx) / sub.numel()
+            meanK = float(D["kept"].double().mean())
+            del dg, D
+            vals = torch.empty(n, dtype=(torch.complex64 if cplx else torch.float32) if fp32 else
+                               (torch.complex128 if cplx else torch.float64), device=dev)
+            ms = _time_ms(lambda: poly.evaluate(pts, exps=True, out=vals), steps, 2)
+            poly.set_profiling(True)
+            poly.evaluate(pts, exps=True, out=vals)
+            stages = dict(poly.last_stage_ms())
+            poly.set_profiling(False)
+            peak = FP64_FMA_PEAK * (2 if fp32 else 1)
+            ev_ms = max(stages.values())
+            out[name] = {"workload": c["name"], "points": n, "evals_per_s": n / (ms * 1e-3), "ms_per_step": ms,
+                         "mean_kept_terms": meanK, "stages_ms": stages,
+                         "eval_kernel_fma_frac": work_pt * n / (ev_ms * 1e-3) / peak,
+                         "sparse": bool(poly.info["sparse"]), "dtype": "f32" if fp32 else "f64"}
+            del poly, pts, vals
+            torch.cuda.empty_cache()
+        except Exception as e:  # noqa: BLE001
+            out[name] = {"error": repr(e)[:200]}
+    return out
 
 
 def run_reference(args):
@@ -288,6 +367,11 @@ def run_fpe(args):
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_baseline(cfg, args.cpu_sample or 65536)
+    context = None
+    if not args.no_extra and world == 1:
+        del pts, vals, exps
+        torch.cuda.empty_cache()
+        context = extra_context(local)
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -303,6 +387,7 @@ def run_fpe(args):
         "e2e": e2e,
         "gpu_launches": int(launches * args.steps),
         "clocks": clk.summary(),
+        "context": context,
     }
     print(json.dumps(line), flush=True)
 
