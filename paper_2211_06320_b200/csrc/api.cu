@@ -310,8 +310,8 @@ fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t
       int2* lr = static_cast<int2*>(workspace);
       launch_classify(pt_dt, pp, m, P, lr, dd, h->dstats, s);
       stg.mark("classify");
-      launch_eval_point(pt_dt, pp, m, P, lr, vv, ee, s);
-      stg.mark("eval_point");
+      launch_eval_sparse(pt_dt, pp, m, P, lr, vv, ee, s);
+      stg.mark("eval_sparse");
       launches += 2;
     }
   }

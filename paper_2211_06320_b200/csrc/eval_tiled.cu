@@ -58,7 +58,7 @@ __device__ __forceinline__ uint32_t lambda_key(double lam, int l, int r) {
 }
 
 template <int PK>
-__global__ void __launch_bounds__(256) k_classify_bucket(const void* __restrict__ pts, long long n, PolyDev P,
+__global__ void __launch_bounds__(256) k_classify_bucket(const void* __restrict__ pts, long long n, int ppc, PolyDev P,
                                                          int2* __restrict__ lr, uint32_t* __restrict__ keys,
                                                          uint32_t* __restrict__ gcount,
                                                          uint32_t* __restrict__ cta_base,
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) k_classify_bucket(const void* __restrict_
   for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) hist[b] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const long long beg = (long long)blockIdx.x * kPtsPerCta, end = min(n, beg + kPtsPerCta);
+  const long long beg = (long long)blockIdx.x * ppc, end = min(n, beg + ppc);
   for (long long i0 = beg + threadIdx.x; i0 - lane < end; i0 += blockDim.x) {
     const long long i = i0;
     const bool ok = i < end;
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const double2* __
 // host side
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-static size_t n_ctas(long long n) { return (size_t)((n + kPtsPerCta - 1) / kPtsPerCta); }
+static size_t n_ctas(long long n) { const int p = pts_per_cta(n); return (size_t)((n + p - 1) / p); }
 // scratch for parallel pieces: 2 bytes per point (at least 1 MiB), in slots of 1 KiB (64 double2)
 static size_t scratch_slots(long long n) {
   size_t bytes = max((size_t)n * 2, (size_t)1 << 20);
@@ -645,7 +645,8 @@ static void launch_classify_bucket_t(const void* pts, long long n, const PolyDev
                                      uint32_t* gcount, uint32_t* cta_base, fpe_diag* diag, unsigned long long* hard,
                                      cudaStream_t s) {
   size_t smem = P.nv <= kSmemHullDbl ? P.nv * (sizeof(int2) + sizeof(double2)) : 0;
-  k_classify_bucket<PK><<<(int)n_ctas(n), 256, smem, s>>>(pts, n, P, lr, keys, gcount, cta_base, diag, hard);
+  k_classify_bucket<PK><<<(int)n_ctas(n), 256, smem, s>>>(pts, n, pts_per_cta(n), P, lr, keys, gcount, cta_base,
+                                                          diag, hard);
 }
 
 int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
@@ -680,7 +681,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     default: launch_classify_bucket_t<FPE_C32>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
   }
   st.mark("classify");
-  bucket_finish(keys, lr, n, gcount, cta_base, bstart, istart, rec, pk, pts, zs, P.k_min, plan, s);
+  bucket_finish(keys, lr, n, pts_per_cta(n), gcount, cta_base, bstart, istart, rec, pk, pts, zs, P.k_min, plan, s);
   st.mark("bucket");
   int le = 0;
 #define FPE_EV(PKV, CKV) \

@@ -12,6 +12,7 @@
 #include <cstdint>
 #include "fpe_internal.h"
 #include "fpe_math.cuh"
+#include "fpe_polar.cuh"
 #include "device_common.cuh"
 #include "kernels.cuh"
 
@@ -32,7 +33,7 @@ __global__ void __launch_bounds__(256) k_classify(const void* __restrict__ pts, 
     double x, y;
     load_point<PK>(pts, i, x, y);
     int hard;
-    double lam = lambda_cr(x, y, PtTraits<PK>::cplx, &hard);
+    double lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
     int istar, l, r;
     classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
     lr[i] = make_int2(l, r);
@@ -112,6 +113,82 @@ __global__ void __launch_bounds__(128) k_eval_point(const void* __restrict__ pts
     long long E;
     times_zpow<CPLX>((double)br, (double)bi, x, y, base, qr, qi, E);
     store_value<OK>(vals, exps, i, qr, qi, E + P.shift);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Sparse handles (compact good-index list): the kept terms of a window are few
+// (cfg4: K ~ 1), so every term a_k z^k is formed directly with z^k by the polar route (one
+// log2|z| / arg z per point, then ~one exp2 + sincospi per term; fpe_polar.cuh) and the terms are
+// summed in extended range in increasing k.  The good indices are binary-searched in shared memory.
+__device__ __forceinline__ void xadd(double& sr, double& si, long long& se, double tr, double ti, long long te) {
+  if (tr == 0.0 && ti == 0.0) return;
+  if (sr == 0.0 && si == 0.0) { sr = tr; si = ti; se = te; return; }
+  if (te > se) { const long long d = te - se; const int s = (int)min(d, 2000ll); sr = ldexp(sr, -s); si = ldexp(si, -s); se = te; }
+  else if (te < se) { const long long d = se - te; const int s = (int)min(d, 2000ll); tr = ldexp(tr, -s); ti = ldexp(ti, -s); }
+  sr += tr; si += ti;
+  const double m = fmax(fabs(sr), fabs(si));
+  if (m != 0.0) { const int e = frexp_exp(m); sr = ldexp(sr, -e); si = ldexp(si, -e); se += e; }
+}
+
+constexpr int kSparseSmemIdx = 8192;   // good indices staged in shared memory (32 KiB)
+
+template <int PK, int CK, int OK>
+__global__ void __launch_bounds__(256) k_eval_sparse(const void* __restrict__ pts, long long n, PolyDev P,
+                                                     const int2* __restrict__ lr, void* __restrict__ vals,
+                                                     long long* __restrict__ exps) {
+  constexpr bool CPLX = PtTraits<OK>::cplx;
+  extern __shared__ int32_t s_idx[];
+  const int32_t* sidx = P.sidx;
+  const int ng = (int)P.n_good;
+  if (ng <= kSparseSmemIdx) {
+    for (int i = threadIdx.x; i < ng; i += blockDim.x) s_idx[i] = P.sidx[i];
+    __syncthreads();
+    sidx = s_idx;
+  }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double x, y;
+    load_point<PK>(pts, i, x, y);
+    const int2 w = lr[i];
+    if (w.y < w.x) {
+      const double nan = __longlong_as_double(0x7ff8000000000000LL);
+      store_value<OK>(vals, exps, i, nan, CPLX ? nan : 0.0, 0);
+      continue;
+    }
+    if (x == 0.0 && y == 0.0) {
+      double cr, ci;
+      a0_value<CK>(P, cr, ci);
+      store_value<OK>(vals, exps, i, cr, ci, cr == 0 && ci == 0 ? 0 : P.shift);
+      continue;
+    }
+    int lo = 0, hi = ng;   // first good index >= l
+    while (lo < hi) { const int m = (lo + hi) >> 1; if (sidx[m] < w.x) lo = m + 1; else hi = m; }
+    double sr = 0.0, si = 0.0;
+    long long se = 0;
+    if (lo < ng && sidx[lo] <= w.y) {
+      const polar_t pz = polar_of<CPLX>(x, y);
+      for (int j = lo; j < ng; ++j) {
+        const int k = sidx[j];
+        if (k > w.y) break;
+        double cr, ci;
+        if constexpr (PtTraits<CK>::f32) { float a, b; Coef<CK>::get(P.coef, j, a, b); cr = a; ci = b; }
+        else Coef<CK>::get(P.coef, j, cr, ci);
+        double tr, ti;
+        long long te = 0;
+        if (k == 0) { tr = cr; ti = ci; }
+        else if constexpr (CPLX) {
+          const xc_t p = pow_polar(pz.lam, pz.tau, k);
+          tr = __fma_rn(cr, p.hr, -ci * p.hi);
+          ti = __fma_rn(cr, p.hi, ci * p.hr);
+          te = p.E;
+        } else {
+          const xr_t p = pow_polar_real(pz.lam, pz.neg, k);
+          tr = cr * p.h; ti = 0.0; te = p.E;
+        }
+        xadd(sr, si, se, tr, ti, te);
+      }
+    }
+    store_value<OK>(vals, exps, i, sr, si, se + P.shift);
   }
 }
 
@@ -231,6 +308,21 @@ static void launch_horner_t(const void* pts, long long n, const PolyDev& P, void
 bool launch_eval_point(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
                        long long* exps, cudaStream_t s) {
   FPE_DISPATCH_PC(launch_eval_point_t, pts, n, P, lr, vals, exps, s)
+  return true;
+}
+
+template <int PK, int CK>
+static void launch_eval_sparse_t(const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
+                                 long long* exps, cudaStream_t s) {
+  constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
+  constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
+  const size_t smem = P.n_good <= kSparseSmemIdx ? (size_t)P.n_good * sizeof(int32_t) : 0;
+  k_eval_sparse<PK, CK, OK><<<grid_for(n, 256), 256, smem, s>>>(pts, n, P, lr, vals, exps);
+}
+
+bool launch_eval_sparse(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
+                        long long* exps, cudaStream_t s) {
+  FPE_DISPATCH_PC(launch_eval_sparse_t, pts, n, P, lr, vals, exps, s)
   return true;
 }
 

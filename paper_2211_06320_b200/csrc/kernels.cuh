@@ -11,6 +11,8 @@ void launch_classify(int pk, const void* pts, long long n, const PolyDev& P, int
                      unsigned long long* hard, cudaStream_t s);
 bool launch_eval_point(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
                        long long* exps, cudaStream_t s);
+bool launch_eval_sparse(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
+                        long long* exps, cudaStream_t s);
 bool launch_horner(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
                    cudaStream_t s);
 }  // namespace fpe

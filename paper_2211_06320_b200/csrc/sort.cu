@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(const uint32_t* __restrict
 // Records to bucket positions.  Lanes of a warp that hit the same bucket are aggregated
 // (__match_any_sync) so that each distinct bucket costs one shared-memory atomic per warp.
 __global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restrict__ keys,
-                                                        const int2* __restrict__ lr, long long n,
+                                                        const int2* __restrict__ lr, long long n, int ppc,
                                                         const uint32_t* __restrict__ bstart,
                                                         const uint32_t* __restrict__ cta_base,
                                                         PtRec* __restrict__ rec) {
@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restri
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const long long beg = (long long)blockIdx.x * kPtsPerCta;
-  const long long end = min(n, beg + kPtsPerCta);
+  const long long beg = (long long)blockIdx.x * ppc;
+  const long long end = min(n, beg + ppc);
   constexpr int U = 4;   // independent loads in flight per thread
   for (long long i0 = beg + threadIdx.x; i0 - lane < end; i0 += (long long)U * blockDim.x) {
     uint32_t key[U];
@@ -246,12 +246,12 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const int2* __restric
   (void)single;
 }
 
-void bucket_finish(const uint32_t* keys, int2* lr, long long n, const uint32_t* gcount,
+void bucket_finish(const uint32_t* keys, int2* lr, long long n, int ppc, const uint32_t* gcount,
                    const uint32_t* cta_base, uint32_t* bstart, uint32_t* istart, PtRec* rec, int pk,
                    const void* pts, double2* zs, long long k_min, const Plan& plan, cudaStream_t s) {
   k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, istart);
-  const int ctas = (int)((n + kPtsPerCta - 1) / kPtsPerCta);
-  k_bucket_scatter<<<ctas, 256, 0, s>>>(keys, lr, n, bstart, cta_base, rec);
+  const int ctas = (int)((n + ppc - 1) / ppc);
+  k_bucket_scatter<<<ctas, 256, 0, s>>>(keys, lr, n, ppc, bstart, cta_base, rec);
   // the sorted windows are written over lr: k_chunk_sort reads only the records
   static bool attr = false;
   if (!attr) {

@@ -6,7 +6,13 @@
 namespace fpe {
 constexpr int kCoarseBits = 12;                 // global buckets: top 12 of the 24 key bits
 constexpr int kBuckets = 1 << kCoarseBits;
-constexpr int kPtsPerCta = 32768;               // points per CTA of classify / scatter
+constexpr int kPtsPerCta = 32768;               // points per CTA of classify / scatter (at most)
+// points per classify / scatter CTA for a batch of n: enough CTAs to fill the GPU for small batches
+inline int pts_per_cta(long long n) {
+  long long p = (n + 148 * 8 - 1) / (148 * 8);
+  p = (p + 255) / 256 * 256;
+  return (int)(p < 2048 ? 2048 : (p > kPtsPerCta ? kPtsPerCta : p));
+}
 constexpr int kChunkPts = 2048;                 // points per evaluator work item (one bucket's slice)
 constexpr int kLocalBits = 11;                  // in-chunk counting sort on key bits [1, 12)
 constexpr int kPiece = 16384;                   // absolute coefficient pieces: a window is cut at multiples
@@ -56,7 +62,7 @@ __device__ __forceinline__ void chunk_of(const uint32_t* istart, const uint32_t*
 // bucket starts + item table (k_bucket_scan), records in bucket order (k_bucket_scatter), the records
 // sorted in place, their windows (written over lr) and points (zs) in sorted order (k_chunk_sort), and the
 // work plan (k_plan)
-void bucket_finish(const uint32_t* keys, int2* lr, long long n, const uint32_t* gcount,
+void bucket_finish(const uint32_t* keys, int2* lr, long long n, int ppc, const uint32_t* gcount,
                    const uint32_t* cta_base, uint32_t* bstart, uint32_t* istart, PtRec* rec, int pk,
                    const void* pts, double2* zs, long long k_min, const Plan& plan, cudaStream_t s);
 inline long long max_chunks(long long n) { return (n + kChunkPts - 1) / kChunkPts + kBuckets; }
