@@ -122,6 +122,7 @@ void fpe_destroy(fpe_poly h) {
   if (h->dstats) cudaFree(h->dstats);
   if (h->st_dev) cudaFree(h->st_dev);
   for (void* s : h->st_streams) if (s) cudaStreamDestroy(static_cast<cudaStream_t>(s));
+  for (void* e : h->st_events) if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (void* e : h->prof_events) if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   delete h;
 }
@@ -349,38 +350,54 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   const size_t out_sz = is_f32(pt_dt) ? (cplx_out ? 8 : 4) : (cplx_out ? 16 : 8);
   const long long chunk = std::min<long long>(n_points, 1ll << 22);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  constexpr int kSlots = 3;
   const size_t per = al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8) + ws_bytes_for(chunk);
-  if (h->st_bytes < 2 * per) {
+  if (h->st_bytes < kSlots * per) {
     if (h->st_dev) { cudaFree(h->st_dev); h->st_dev = nullptr; h->st_bytes = 0; }
-    if (cudaMalloc(&h->st_dev, 2 * per) != cudaSuccess) { cudaGetLastError(); set_error("staging cudaMalloc failed"); return FPE_ERR_OOM; }
-    h->st_bytes = 2 * per;
+    if (cudaMalloc(&h->st_dev, kSlots * per) != cudaSuccess) { cudaGetLastError(); set_error("staging cudaMalloc failed"); return FPE_ERR_OOM; }
+    h->st_bytes = kSlots * per;
   }
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < 3; ++b)
     if (!h->st_streams[b]) {
       cudaStream_t ns;
       FPE_CUDA(cudaStreamCreateWithFlags(&ns, cudaStreamNonBlocking));
       h->st_streams[b] = ns;
     }
-  PolyDev P = h->view();
+  for (auto& e : h->st_events)
+    if (!e) {
+      cudaEvent_t ev;
+      FPE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      e = ev;
+    }
+  // three-stage pipeline over staging slots: H2D of chunk c+1 || kernels of chunk c || D2H of chunk c-1
+  cudaStream_t s_in = static_cast<cudaStream_t>(h->st_streams[0]);
+  cudaStream_t s_ev = static_cast<cudaStream_t>(h->st_streams[1]);
+  cudaStream_t s_out = static_cast<cudaStream_t>(h->st_streams[2]);
+  auto ev = [&](int slot, int kind) { return static_cast<cudaEvent_t>(h->st_events[slot * 3 + kind]); };
   long long launches = 0;
   for (long long off = 0, c = 0; off < n_points; off += chunk, ++c) {
     const long long m = std::min(chunk, n_points - off);
-    const int b = (int)(c & 1);
-    cudaStream_t s = static_cast<cudaStream_t>(h->st_streams[b]);
+    const int b = (int)(c % kSlots);
     char* base = static_cast<char*>(h->st_dev) + b * per;
     void* dp = base;
     void* dv = base + al(chunk * in_sz);
     long long* de = reinterpret_cast<long long*>(base + al(chunk * in_sz) + al(chunk * out_sz));
     void* wsp = base + al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8);
-    FPE_CUDA(cudaMemcpyAsync(dp, static_cast<const char*>(points_host) + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s));
+    if (c >= kSlots) FPE_CUDA(cudaStreamWaitEvent(s_in, ev(b, 2), 0));   // slot's previous results copied out
+    FPE_CUDA(cudaMemcpyAsync(dp, static_cast<const char*>(points_host) + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
+    FPE_CUDA(cudaEventRecord(ev(b, 0), s_in));
+    FPE_CUDA(cudaStreamWaitEvent(s_ev, ev(b, 0), 0));
     fpe_status est = fpe_evaluate(h, dp, pt_dt, m, dv, exps_host ? reinterpret_cast<int64_t*>(de) : nullptr, nullptr,
-                                  wsp, ws_bytes_for(chunk), s);
+                                  wsp, ws_bytes_for(chunk), s_ev);
     if (est != FPE_OK) return est;
     launches += h->last_launches;
-    FPE_CUDA(cudaMemcpyAsync(static_cast<char*>(values_host) + off * out_sz, dv, m * out_sz, cudaMemcpyDeviceToHost, s));
-    if (exps_host) FPE_CUDA(cudaMemcpyAsync(exps_host + off, de, m * 8, cudaMemcpyDeviceToHost, s));
+    FPE_CUDA(cudaEventRecord(ev(b, 1), s_ev));
+    FPE_CUDA(cudaStreamWaitEvent(s_out, ev(b, 1), 0));
+    FPE_CUDA(cudaMemcpyAsync(static_cast<char*>(values_host) + off * out_sz, dv, m * out_sz, cudaMemcpyDeviceToHost, s_out));
+    if (exps_host) FPE_CUDA(cudaMemcpyAsync(exps_host + off, de, m * 8, cudaMemcpyDeviceToHost, s_out));
+    FPE_CUDA(cudaEventRecord(ev(b, 2), s_out));
   }
-  for (int b = 0; b < 2; ++b) FPE_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(h->st_streams[b])));
+  FPE_CUDA(cudaStreamSynchronize(s_out));
   h->last_launches = launches;
   return FPE_OK;
 }

@@ -59,7 +59,8 @@ struct fpe_poly_s {
   void* prof_stream = nullptr;
   // staging for fpe_evaluate_host (grown on demand, owned)
   void* st_dev = nullptr; size_t st_bytes = 0;
-  void* st_streams[2] = {nullptr, nullptr};
+  void* st_streams[3] = {nullptr, nullptr, nullptr};   // H2D copies, kernels, D2H copies
+  void* st_events[9] = {};                            // per staging slot: h2d done, eval done, d2h done
   fpe::PolyDev view() const;
 };
 
