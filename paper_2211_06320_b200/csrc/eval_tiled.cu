@@ -475,8 +475,8 @@ __device__ __forceinline__ void group_unpack(Pts<NP>& S, const GroupCtx<NP>& c, 
 }
 
 template <int PK, int CK, int OK, int NP, typename Prefetch>
-__device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c, long long n, const PolyDev& P,
-                                             void* vals, long long* exps, Prefetch prefetch) {
+__device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c, bool begun, long long n,
+                                             const PolyDev& P, void* vals, long long* exps, Prefetch prefetch) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
   const GroupDesc d = c.d;
@@ -490,7 +490,7 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c,
   if (nonempty) {
     for (int p = p_hi; p >= p_lo; --p) {
       const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
-      ring_begin(R, rlo, rhi);
+      if (p != p_hi || !begun) ring_begin(R, rlo, rhi);
       W br[NP], bi[NP];
       eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, br, bi);
 #pragma unroll
@@ -589,21 +589,32 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const double2* __
     if (item.x == ~0u) continue;
     multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, rec, zs, P, vals, exps);
   }
-  // groups: software-pipelined one group ahead (the next group's records load during this epilogue)
+  // groups, software-pipelined: the next group's descriptor and records are loaded while this group
+  // streams its coefficients, and the next group's first coefficient chunks are requested (TMA) before
+  // this group's epilogue, so neither latency is exposed.
   const int kmin = (int)P.k_min;
+  auto begin_first = [&](const GroupCtx<NP>& c) -> bool {
+    if (c.g >= plan.ngroups || c.d.npieces > 1 || c.d.hi < c.d.lo) return false;
+    ring_begin(R, max(c.d.lo, (c.d.hi / kPiece) * kPiece), c.d.hi);
+    return true;
+  };
   if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
   GroupCtx<NP> cur;
   group_load<PK, NP>(cur, __shfl_sync(0xffffffffu, nxt, 0), n, plan, rec, zs, kmin);
   if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
+  bool cur_begun = begin_first(cur);
   while (cur.g < plan.ngroups) {
     GroupCtx<NP> nx;
-    auto fetch_next = [&]() {
-      group_load<PK, NP>(nx, __shfl_sync(0xffffffffu, nxt, 0), n, plan, rec, zs, kmin);
-      if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
-    };
-    if (cur.d.npieces > 1) fetch_next();   // evaluated as parallel pieces (multi_piece)
-    else single_group<PK, CK, OK, NP>(R, cur, n, P, vals, exps, fetch_next);
+    group_load<PK, NP>(nx, __shfl_sync(0xffffffffu, nxt, 0), n, plan, rec, zs, kmin);
+    if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
+    bool nx_begun = false;
+    if (cur.d.npieces > 1) {   // evaluated as parallel pieces (multi_piece)
+      nx_begun = begin_first(nx);
+    } else {
+      single_group<PK, CK, OK, NP>(R, cur, cur_begun, n, P, vals, exps, [&]() { nx_begun = begin_first(nx); });
+    }
     cur = nx;
+    cur_begun = nx_begun;
   }
 }
 
