@@ -32,7 +32,7 @@
 
 namespace fpe {
 
-constexpr int kWarps = 8;      // warps per CTA of k_eval_tiled
+constexpr int kWarps = 4;      // warps per CTA of k_eval_tiled
 constexpr int kStages = 3;     // TMA ring depth per warp
 
 // ------------------------------------------------------------------------------------------------
@@ -299,8 +299,10 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
       for (int u = 0; u < 8; ++u) a[u] = cb[k - u];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if constexpr (NP == 2 && CK == FPE_C64) {
-          horner_step2_c64(br[0], bi[0], br[1], bi[1], zr[0], zi[0], zr[1], zi[1], a[u]);
+        if constexpr (NP % 2 == 0 && CK == FPE_C64) {
+#pragma unroll
+          for (int j = 0; j < NP; j += 2)
+            horner_step2_c64(br[j], bi[j], br[j + 1], bi[j + 1], zr[j], zi[j], zr[j + 1], zi[j + 1], a[u]);
         } else {
 #pragma unroll
           for (int j = 0; j < NP; ++j) horner_step<CK, CPLX>(br[j], bi[j], zr[j], zi[j], a[u]);
@@ -475,8 +477,8 @@ __device__ __forceinline__ void group_unpack(Pts<NP>& S, const GroupCtx<NP>& c, 
 }
 
 template <int PK, int CK, int OK, int NP, typename Prefetch>
-__device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c, bool begun, long long n,
-                                             const PolyDev& P, void* vals, long long* exps, Prefetch prefetch) {
+__device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c, long long n, const PolyDev& P,
+                                             void* vals, long long* exps, Prefetch prefetch) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
   const GroupDesc d = c.d;
@@ -490,7 +492,7 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c,
   if (nonempty) {
     for (int p = p_hi; p >= p_lo; --p) {
       const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
-      if (p != p_hi || !begun) ring_begin(R, rlo, rhi);
+      ring_begin(R, rlo, rhi);
       W br[NP], bi[NP];
       eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, br, bi);
 #pragma unroll
@@ -563,7 +565,7 @@ constexpr size_t ring_bytes() {
 // Persistent evaluator: every warp first takes parallel pieces of long windows, then whole groups,
 // both from global atomic counters (largest work first; the tail is at most one group).
 template <int PK, int CK, int OK, int NP>
-__global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const double2* __restrict__ zs, long long n, PolyDev P,
+__global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(const double2* __restrict__ zs, long long n, PolyDev P,
                                                                const PtRec* __restrict__ rec, Plan plan,
                                                                void* __restrict__ vals, long long* __restrict__ exps) {
   using CT = typename Step<CK>::CT;
@@ -589,32 +591,22 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_eval_tiled(const double2* __
     if (item.x == ~0u) continue;
     multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, rec, zs, P, vals, exps);
   }
-  // groups, software-pipelined: the next group's descriptor and records are loaded while this group
-  // streams its coefficients, and the next group's first coefficient chunks are requested (TMA) before
-  // this group's epilogue, so neither latency is exposed.
+  // groups: software-pipelined one group ahead (the next group's records load during this epilogue)
   const int kmin = (int)P.k_min;
-  auto begin_first = [&](const GroupCtx<NP>& c) -> bool {
-    if (c.g >= plan.ngroups || c.d.npieces > 1 || c.d.hi < c.d.lo) return false;
-    ring_begin(R, max(c.d.lo, (c.d.hi / kPiece) * kPiece), c.d.hi);
-    return true;
-  };
   if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
   GroupCtx<NP> cur;
-  group_load<PK, NP>(cur, __shfl_sync(0xffffffffu, nxt, 0), n, plan, rec, zs, kmin);
+  auto gid = [&](uint32_t it) { return it; };
+  group_load<PK, NP>(cur, gid(__shfl_sync(0xffffffffu, nxt, 0)), n, plan, rec, zs, kmin);
   if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
-  bool cur_begun = begin_first(cur);
   while (cur.g < plan.ngroups) {
     GroupCtx<NP> nx;
-    group_load<PK, NP>(nx, __shfl_sync(0xffffffffu, nxt, 0), n, plan, rec, zs, kmin);
-    if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
-    bool nx_begun = false;
-    if (cur.d.npieces > 1) {   // evaluated as parallel pieces (multi_piece)
-      nx_begun = begin_first(nx);
-    } else {
-      single_group<PK, CK, OK, NP>(R, cur, cur_begun, n, P, vals, exps, [&]() { nx_begun = begin_first(nx); });
-    }
+    auto fetch_next = [&]() {
+      group_load<PK, NP>(nx, gid(__shfl_sync(0xffffffffu, nxt, 0)), n, plan, rec, zs, kmin);
+      if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
+    };
+    if (cur.d.npieces > 1) fetch_next();   // evaluated as parallel pieces (multi_piece)
+    else single_group<PK, CK, OK, NP>(R, cur, n, P, vals, exps, fetch_next);
     cur = nx;
-    cur_begun = nx_begun;
   }
 }
 
@@ -659,7 +651,8 @@ static int launch_eval_tiled_t(const double2* zs, long long n, const PolyDev& P,
 }
 
 // points per lane: complex steps (4 FMAs per coefficient) share a coefficient load between 2 points,
-// real steps (1 FMA) between 4 (shared-memory wavefronts per FMA)
+// real steps (1 FMA) between 4 (shared-memory wavefronts per FMA); 4 complex points per
+// lane measured slower (register spills in the epilogue)
 template <int PK, int CK>
 struct NPFor {
   static constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
