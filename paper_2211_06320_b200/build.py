@@ -13,9 +13,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 SO = os.path.join(HERE, "libfpe.so")
+# experiments only: extra nvcc flags (e.g. -DFPE_EXP_NO_ZPOW) into a separately named library
+EXTRA = os.environ.get("FPE_EXTRA_FLAGS", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+CUFLAGS = EXTRA + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
            "--expt-relaxed-constexpr", "-I", os.path.join(HERE, "..", "include")]
 SOURCES = ["api.cu", "kernels.cu", "sort.cu", "eval_tiled.cu", "precondition.cpp"]
 HEADERS = ["fpe_internal.h", "fpe_hd.cuh", "fpe_polar.cuh", "fpe_math.cuh", "kernels.cuh", "log_table.h", "device_common.cuh", "sort.cuh", "eval_tiled.cuh"]

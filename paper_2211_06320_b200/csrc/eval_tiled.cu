@@ -235,6 +235,9 @@ __device__ __forceinline__ void ring_issue_n(Ring<CK>& R, int n) {
 // Start streaming the chunks that cover [lo, hi] (relative indices, lo <= hi), highest chunk first.
 template <int CK>
 __device__ __forceinline__ void ring_begin(Ring<CK>& R, int lo, int hi) {
+#ifdef FPE_EXP_NO_STREAM
+  return;
+#endif
   R.q_next = hi / kChunk;
   R.q_end = lo / kChunk;
   ring_issue_n(R, min(kStages - (int)(R.gi - R.g), R.q_next - R.q_end + 1));
@@ -265,6 +268,9 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
                                              typename Step<CK>::W (&br)[NP], typename Step<CK>::W (&bi)[NP]) {
   using CT = typename Step<CK>::CT;
   using W = typename Step<CK>::W;
+#ifdef FPE_EXP_NO_STREAM
+  return;
+#endif
   int mx = lo, mn = hi;
   bool any = false;
 #pragma unroll
@@ -283,6 +289,9 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
     const CT* cb = ring_wait(R) - q * kChunk;
     const int k1 = min(hi, q * kChunk + kChunk - 1), k0 = max(lo, q * kChunk);
     int k = k1;
+#ifdef FPE_EXP_NO_MASK
+    k = min(k, F_hi);
+#endif
     for (const int m1 = max(k0, F_hi + 1); k >= m1; --k) {
       const CT a = cb[k];
 #pragma unroll
@@ -293,6 +302,9 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
       }
     }
     const int f0 = max(k0, F_lo);
+#ifdef FPE_EXP_NO_HOT
+    k = min(k, f0 - 1);
+#endif
     for (; k - 7 >= f0; k -= 8) {
       CT a[8];
 #pragma unroll
@@ -314,6 +326,9 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
 #pragma unroll
       for (int j = 0; j < NP; ++j) horner_step<CK, CPLX>(br[j], bi[j], zr[j], zi[j], a);
     }
+#ifdef FPE_EXP_NO_MASK
+    k = k0 - 1;
+#endif
     for (; k >= k0; --k) {
       const CT a = cb[k];
 #pragma unroll
@@ -370,6 +385,10 @@ __device__ __forceinline__ void acc_fold(Acc& A, double hr, double hi, int pbase
 template <int OK, bool CPLX>
 __device__ __forceinline__ void finalize(void* vals, long long* exps, long long idx, double x, double y,
                                          const Acc& A, const PolyDev& P) {
+#ifdef FPE_EXP_NO_FINALIZE
+  if (A.r == 1.2345) store_value<OK>(vals, exps, idx, A.r, A.i, 0);
+  return;
+#endif
   if (!isfinite(x) || !isfinite(y)) {
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
     store_value<OK>(vals, exps, idx, nan, CPLX ? nan : 0.0, 0);
@@ -383,7 +402,11 @@ __device__ __forceinline__ void finalize(void* vals, long long* exps, long long 
   }
   long long E = 0;
   const long long n = A.started ? (long long)A.base + P.k_min : 0;
+#ifdef FPE_EXP_NO_ZPOW
+  if (false) {
+#else
   if (n > 0) {
+#endif
     const xc_t p = power_polar<CPLX>(x, y, n);
     const double r = __fma_rn(qr, p.hr, -qi * p.hi);
     const double i = __fma_rn(qr, p.hi, qi * p.hr);
@@ -470,7 +493,12 @@ __device__ __forceinline__ void group_unpack(Pts<NP>& S, const GroupCtx<NP>& c, 
     S.valid[j] = pos < n;
     S.idx[j] = 0; S.x[j] = 0.0; S.y[j] = 0.0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
     if (S.valid[j]) {
-      S.idx[j] = c.h[j].x; S.x[j] = c.z[j].x; S.y[j] = c.z[j].y;
+#ifdef FPE_EXP_SORTED_STORE
+      S.idx[j] = pos;
+#else
+      S.idx[j] = c.h[j].x;
+#endif
+      S.x[j] = c.z[j].x; S.y[j] = c.z[j].y;
       if (c.h[j].w >= c.h[j].z) { S.wl[j] = c.h[j].z - kmin; S.wr[j] = c.h[j].w - kmin; }
     }
   }
