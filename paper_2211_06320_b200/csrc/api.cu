@@ -323,15 +323,23 @@ fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t
 
 fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
                       void* values_out, int64_t* exps_out, void* workspace, size_t ws_bytes, void* stream) {
-  (void)workspace; (void)ws_bytes;
   fpe_status st = check_eval_args(h, points, pt_dt, n_points, values_out);
   if (st != FPE_OK) return st;
   if (n_points == 0) return FPE_OK;
+  if (!h->hdr.sparse && (!workspace || ws_bytes < 256)) {
+    set_error("fpe_horner: workspace of %zu bytes < 256", ws_bytes);
+    return FPE_ERR_INVALID_ARG;
+  }
   DeviceGuard g(h->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PolyDev P = h->view();
   Stage stg(h, s);
-  launch_horner(pt_dt, points, n_points, P, values_out, reinterpret_cast<long long*>(exps_out), s);
+  if (h->hdr.sparse) {   // Horner over the nonzero terms with gap powers
+    launch_horner(pt_dt, points, n_points, P, values_out, reinterpret_cast<long long*>(exps_out), s);
+  } else {
+    run_horner_tiled(pt_dt, points, n_points, P, static_cast<uint32_t*>(workspace), values_out,
+                     reinterpret_cast<long long*>(exps_out), s);
+  }
   stg.mark("horner_full");
   h->last_launches = 1;
   FPE_CUDA(cudaGetLastError());

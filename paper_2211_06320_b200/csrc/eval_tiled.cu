@@ -639,6 +639,146 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(const double2* __
 }
 
 // ------------------------------------------------------------------------------------------------
+// Full Horner over all coefficients (the context baseline), with the evaluator's
+// streaming: warps take 64 consecutive input points (2 per lane) and stream every coefficient chunk
+// through the TMA ring.  Without the band there is no magnitude bound, so after every chunk each point
+// whose partial sum exceeds 2^(emax/2) is rescaled by a power of two (exponent E_j), and later
+// coefficients enter multiplied by 2^-E_j (0 once that is below the working range: they are then
+// below the partial sum's rounding).
+template <int CK, int NP, bool CPLX>
+__device__ __forceinline__ void stream_full(Ring<CK>& R, int lo, int hi, const typename Step<CK>::W (&zr)[NP],
+                                            const typename Step<CK>::W (&zi)[NP], typename Step<CK>::W (&br)[NP],
+                                            typename Step<CK>::W (&bi)[NP], int (&E)[NP]) {
+  using CT = typename Step<CK>::CT;
+  using W = typename Step<CK>::W;
+  constexpr bool F32 = std::is_same<W, float>::value;
+  constexpr int kHalf = F32 ? 60 : 500;      // rescale above 2^kHalf
+  constexpr int kDrop = F32 ? 150 : 1100;    // 2^-E underflows the working type
+  constexpr int kBlk = F32 ? 1 : 8;          // steps between checks: |z|^kBlk 2^kHalf stays finite for
+                                             // |z| < 2^65 (fp64); fp32 checks every step
+  auto rescale = [&]() {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const double m = fmax(fabs((double)br[j]), fabs((double)bi[j]));
+      if (m > ldexp(1.0, kHalf) && isfinite(m)) {
+        const int e = frexp_exp(m);
+        br[j] = (W)ldexp((double)br[j], -e);
+        bi[j] = (W)ldexp((double)bi[j], -e);
+        E[j] += e;
+      }
+    }
+  };
+  for (int q = hi / kChunk; q >= lo / kChunk; --q) {
+    const CT* cb = ring_wait(R) - q * kChunk;
+    const int k1 = min(hi, q * kChunk + kChunk - 1), k0 = max(lo, q * kChunk);
+    for (int kb = k1; kb >= k0; kb -= kBlk) {
+      const int ke = max(k0, kb - kBlk + 1);
+      bool any_scaled = false;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) any_scaled |= E[j] != 0;
+      if (!__any_sync(0xffffffffu, any_scaled)) {
+        if (kb - ke == 7) {
+          CT a[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a[u] = cb[kb - u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if constexpr (NP % 2 == 0 && CK == FPE_C64) {
+#pragma unroll
+              for (int j = 0; j < NP; j += 2)
+                horner_step2_c64(br[j], bi[j], br[j + 1], bi[j + 1], zr[j], zi[j], zr[j + 1], zi[j + 1], a[u]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < NP; ++j) horner_step<CK, CPLX>(br[j], bi[j], zr[j], zi[j], a[u]);
+            }
+          }
+        } else {
+          for (int k = kb; k >= ke; --k) {
+            const CT a = cb[k];
+#pragma unroll
+            for (int j = 0; j < NP; ++j) horner_step<CK, CPLX>(br[j], bi[j], zr[j], zi[j], a);
+          }
+        }
+      } else {
+        W s[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) s[j] = E[j] > kDrop ? (W)0 : (W)ldexp(1.0, -E[j]);
+        for (int k = kb; k >= ke; --k) {
+          const CT a = cb[k];
+#pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            CT as = a;
+            if constexpr (CK == FPE_C64 || CK == FPE_C32) { as.x *= s[j]; as.y *= s[j]; }
+            else as *= s[j];
+            horner_step<CK, CPLX>(br[j], bi[j], zr[j], zi[j], as);
+          }
+        }
+      }
+      rescale();
+    }
+    ring_release(R);
+  }
+}
+
+template <int PK, int CK, int OK, int NP>
+__global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __restrict__ pts, long long n, PolyDev P,
+                                                                 uint32_t* __restrict__ ctr, void* __restrict__ vals,
+                                                                 long long* __restrict__ exps) {
+  using CT = typename Step<CK>::CT;
+  using W = typename Step<CK>::W;
+  constexpr bool CPLX = PtTraits<OK>::cplx;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  CT* ring_buf = reinterpret_cast<CT*>(smem) + (size_t)wib * kStages * kChunk;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes<CK>()) + wib * kStages;
+  if (lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0};
+  const int hi = (int)(P.k_max - P.k_min);
+  const long long ngroups = (n + 32 * NP - 1) / (32 * NP);
+  for (;;) {
+    uint32_t g = 0;
+    if (lane == 0) g = atomicAdd(ctr, 1u);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if ((long long)g >= ngroups) break;
+    ring_begin(R, 0, hi);
+    double x[NP], y[NP];
+    long long idx[NP];
+    W zr[NP], zi[NP], br[NP], bi[NP];
+    int E[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      idx[j] = (long long)g * (32 * NP) + j * 32 + lane;
+      x[j] = 0.0; y[j] = 0.0;
+      if (idx[j] < n) load_point<PK>(pts, idx[j], x[j], y[j]);
+      zr[j] = (W)x[j]; zi[j] = (W)y[j]; br[j] = 0; bi[j] = 0; E[j] = 0;
+    }
+    stream_full<CK, NP, CPLX>(R, 0, hi, zr, zi, br, bi, E);
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      if (idx[j] >= n) continue;
+      Acc A{(double)br[j], (double)bi[j], 0, true};
+      if (!isfinite(x[j]) || !isfinite(y[j]) || (x[j] == 0.0 && y[j] == 0.0)) {
+        finalize<OK, CPLX>(vals, exps, idx[j], x[j], y[j], A, P);   // NaN / a_0 (the E = 0 paths)
+        continue;
+      }
+      double qr = A.r, qi = A.i;
+      long long Ez = 0;
+      if (P.k_min > 0) {
+        const xc_t p = power_polar<CPLX>(x[j], y[j], P.k_min);
+        const double r = __fma_rn(qr, p.hr, -qi * p.hi);
+        const double i = __fma_rn(qr, p.hi, qi * p.hr);
+        qr = r; qi = i; Ez = p.E;
+      }
+      store_value<OK>(vals, exps, idx[j], qr, qi, Ez + E[j] + P.shift);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // host side
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -700,6 +840,40 @@ static void launch_classify_bucket_t(const void* pts, long long n, const PolyDev
   size_t smem = P.nv <= kSmemHullDbl ? P.nv * (sizeof(int2) + sizeof(double2)) : 0;
   k_classify_bucket<PK><<<(int)n_ctas(n), 256, smem, s>>>(pts, n, pts_per_cta(n), P, lr, keys, gcount, cta_base,
                                                           diag, hard);
+}
+
+template <int PK, int CK>
+static void launch_horner_tiled_t(const void* pts, long long n, const PolyDev& P, uint32_t* ctr, void* vals,
+                                  long long* exps, cudaStream_t s) {
+  constexpr int NP = NPFor<PK, CK>::value, OK = NPFor<PK, CK>::OK;
+  static int grid = 0;
+  const size_t smem = eval_smem<CK>();
+  if (grid == 0) {
+    cudaFuncSetAttribute(k_horner_tiled<PK, CK, OK, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_horner_tiled<PK, CK, OK, NP>, kWarps * 32, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = max(1, per_sm) * sms;
+  }
+  cudaMemsetAsync(ctr, 0, sizeof(uint32_t), s);
+  k_horner_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(pts, n, P, ctr, vals, exps);
+}
+
+bool run_horner_tiled(int pk, const void* pts, long long n, const PolyDev& P, uint32_t* ctr, void* vals,
+                      long long* exps, cudaStream_t s) {
+  switch (pk * 4 + P.cdt) {
+    case FPE_R64 * 4 + FPE_R64: launch_horner_tiled_t<FPE_R64, FPE_R64>(pts, n, P, ctr, vals, exps, s); break;
+    case FPE_R64 * 4 + FPE_C64: launch_horner_tiled_t<FPE_R64, FPE_C64>(pts, n, P, ctr, vals, exps, s); break;
+    case FPE_C64 * 4 + FPE_R64: launch_horner_tiled_t<FPE_C64, FPE_R64>(pts, n, P, ctr, vals, exps, s); break;
+    case FPE_C64 * 4 + FPE_C64: launch_horner_tiled_t<FPE_C64, FPE_C64>(pts, n, P, ctr, vals, exps, s); break;
+    case FPE_R32 * 4 + FPE_R32: launch_horner_tiled_t<FPE_R32, FPE_R32>(pts, n, P, ctr, vals, exps, s); break;
+    case FPE_R32 * 4 + FPE_C32: launch_horner_tiled_t<FPE_R32, FPE_C32>(pts, n, P, ctr, vals, exps, s); break;
+    case FPE_C32 * 4 + FPE_R32: launch_horner_tiled_t<FPE_C32, FPE_R32>(pts, n, P, ctr, vals, exps, s); break;
+    case FPE_C32 * 4 + FPE_C32: launch_horner_tiled_t<FPE_C32, FPE_C32>(pts, n, P, ctr, vals, exps, s); break;
+    default: return false;
+  }
+  return true;
 }
 
 int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,

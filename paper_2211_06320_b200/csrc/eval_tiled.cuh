@@ -11,4 +11,7 @@ size_t tiled_ws_bytes(long long n);
 // classify + sort + plan + evaluate (dense handles).  Returns the number of kernel launches or -1.
 int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
               fpe_diag* diag, void* ws, unsigned long long* hard, Stage& st, cudaStream_t s);
+// full Horner (dense handles) with the streaming evaluator; ctr: one device uint32 of scratch
+bool run_horner_tiled(int pk, const void* pts, long long n, const PolyDev& P, uint32_t* ctr, void* vals,
+                      long long* exps, cudaStream_t s);
 }  // namespace fpe

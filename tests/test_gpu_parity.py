@@ -188,6 +188,18 @@ def test_horner_context(fpe):
     out = gpu_eval(poly3, p3, horner=True)
     err = rel_err_vs(P3.horner(p3), out["v"], out["e"], abs_sum_log2(a3, p3))
     assert np.all(err <= TOL64), err.max()
+    # real coefficients at real points (cfg2 family), and fp32 (cfg5 family), huge and tiny |z|
+    for cfg, fp32, tol in ((2, False, TOL64), (5, True, TOL32)):
+        ac = workloads.coefficients(cfg, d=(1 << 12) - 1)
+        pc = workloads.points(cfg, 200)
+        pc = np.concatenate([pc, pc[:20] * 1e6, pc[20:40] * 1e-6])
+        if fp32:
+            ac, pc = workloads.to_fp32(ac), workloads.to_fp32(pc)
+        polyc = fpe.precondition(ac)
+        Pc = oracle.OraclePoly(ac)
+        out = gpu_eval(polyc, pc, horner=True)
+        err = rel_err_vs(Pc.horner(pc), out["v"], out["e"], abs_sum_log2(ac, pc))
+        assert np.all(err <= tol), (cfg, err.max())
 
 
 def test_evaluate_host_matches_device(fpe):
