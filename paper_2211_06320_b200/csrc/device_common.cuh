@@ -35,13 +35,43 @@ __device__ __forceinline__ bool band_vertex(const int2* hull, int j, int2 vs, in
   int2 v = hull[j];
   return sign_lin(lam, (long long)v.x - vs.x, (long long)v.y - vs.y + drop) >= 0;
 }
+// lambda policies for the searches.  LamExact: the correctly rounded lambda, every predicate is the exact
+// sign of lambda I + J.  LamIv: an enclosure [lo, hi] of the exact log2|z| (and so of its rounding);
+// lambda I + J is monotone in lambda, so a predicate is decided for every lambda of the enclosure when
+// both ends agree -- otherwise `amb` is set and the caller redoes the search with the rounded lambda.
+struct LamExact {
+  double l;
+  __device__ __forceinline__ double mid() const { return l; }
+  __device__ __forceinline__ bool ge0(double I, double J) const { return __fma_rn(l, I, J) >= 0.0; }
+  __device__ __forceinline__ bool le0(double I, double J) const { return __fma_rn(l, I, J) <= 0.0; }
+};
+struct LamIv {
+  double lo, hi;
+  bool* amb;
+  __device__ __forceinline__ double mid() const { return 0.5 * (lo + hi); }
+  __device__ __forceinline__ bool ge0(double I, double J) const {
+    const bool a = __fma_rn(lo, I, J) >= 0.0, b = __fma_rn(hi, I, J) >= 0.0;
+    if (a != b) *amb = true;
+    return a;
+  }
+  __device__ __forceinline__ bool le0(double I, double J) const {
+    const bool a = __fma_rn(lo, I, J) <= 0.0, b = __fma_rn(hi, I, J) <= 0.0;
+    if (a != b) *amb = true;
+    return a;
+  }
+};
+
 // The same predicate in doubles: exact when every |I|, |J| < 2^53 (PolyDev::dbl_ok, checked per polynomial):
 // the products are exact integers and the fused multiply-add rounds lambda I + J once.
-__device__ __forceinline__ bool band_seg_d(int2 a, int2 b, int2 vs, int drop, double lam, long long k) {
+template <typename L>
+__device__ __forceinline__ bool band_seg_dp(int2 a, int2 b, int2 vs, int drop, const L& pl, long long k) {
   const double dk = (double)(b.x - a.x), dh = (double)(b.y - a.y);
   const double J = __fma_rn(dh, (double)(k - a.x), (double)(a.y - vs.y + drop) * dk);
   const double I = (double)(k - vs.x) * dk;
-  return __fma_rn(lam, I, J) >= 0.0;
+  return pl.ge0(I, J);
+}
+__device__ __forceinline__ bool band_seg_d(int2 a, int2 b, int2 vs, int drop, double lam, long long k) {
+  return band_seg_dp(a, b, vs, drop, LamExact{lam}, k);
 }
 __device__ __forceinline__ bool band_seg(int2 a, int2 b, int2 vs, int drop, double lam, long long k) {
   long long dk = (long long)b.x - a.x, dh = (long long)b.y - a.y;
@@ -104,6 +134,58 @@ __device__ __forceinline__ long long seg_last_true(int2 A, int2 B, int2 vs, int 
   }
   long long a = lo, b = hi;
   while (a < b) { long long m = (a + b + 1) >> 1; if ((DBL ? band_seg_d(A, B, vs, drop, lam, m) : band_seg(A, B, vs, drop, lam, m))) a = m; else b = m - 1; }
+  return a;
+}
+
+// seg_first_true / seg_last_true for a lambda policy (predicates in exact doubles: PolyDev::dbl_ok).
+template <typename L>
+__device__ __forceinline__ long long seg_first_true_p(int2 A, int2 B, int2 vs, int drop, const L& pl,
+                                                      long long lo, long long hi) {
+  const double lam = pl.mid();
+  const double dk = (double)(B.x - A.x), dh = (double)(B.y - A.y);
+  const double c1 = __fma_rn(lam, dk, dh);
+  const double g = __fma_rn(lam, (double)(A.x - vs.x), (double)(A.y - vs.y + drop));
+  long long k = hi;
+  if (c1 > 0.0) {
+    double e = (double)A.x + ceil(-(g * dk) / c1);
+    if (e >= (double)lo && e <= (double)hi) k = (long long)e;
+    else if (e < (double)lo) k = lo;
+  }
+  for (int it = 0; it < 4; ++it) {
+    if (band_seg_dp(A, B, vs, drop, pl, k)) {
+      if (k == lo || !band_seg_dp(A, B, vs, drop, pl, k - 1)) return k;
+      --k;
+    } else {
+      ++k;
+    }
+  }
+  long long a = lo, b = hi;
+  while (a < b) { long long m = (a + b) >> 1; if (band_seg_dp(A, B, vs, drop, pl, m)) b = m; else a = m + 1; }
+  return a;
+}
+template <typename L>
+__device__ __forceinline__ long long seg_last_true_p(int2 A, int2 B, int2 vs, int drop, const L& pl,
+                                                     long long lo, long long hi) {
+  const double lam = pl.mid();
+  const double dk = (double)(B.x - A.x), dh = (double)(B.y - A.y);
+  const double c1 = __fma_rn(lam, dk, dh);
+  const double g = __fma_rn(lam, (double)(A.x - vs.x), (double)(A.y - vs.y + drop));
+  long long k = lo;
+  if (c1 < 0.0) {
+    double e = (double)A.x + floor(-(g * dk) / c1);
+    if (e >= (double)lo && e <= (double)hi) k = (long long)e;
+    else if (e > (double)hi) k = hi;
+  }
+  for (int it = 0; it < 4; ++it) {
+    if (band_seg_dp(A, B, vs, drop, pl, k)) {
+      if (k == hi || !band_seg_dp(A, B, vs, drop, pl, k + 1)) return k;
+      ++k;
+    } else {
+      --k;
+    }
+  }
+  long long a = lo, b = hi;
+  while (a < b) { long long m = (a + b + 1) >> 1; if (band_seg_dp(A, B, vs, drop, pl, m)) a = m; else b = m - 1; }
   return a;
 }
 
@@ -184,6 +266,61 @@ __device__ __forceinline__ void classify_lambda_v(const int2* hull, const double
     const int2 A = hull[a], B = hull[a + 1];
     r = (int)seg_last_true<DBL>(A, B, vsi, drop, lam, (long long)A.x, (long long)B.x - 1);
   }
+}
+
+// The vertex searches of classify_lambda_v for a lambda policy (finite lambda; predicates in doubles).
+template <typename L>
+__device__ __forceinline__ void classify_lambda_vp(const int2* hull, const double2* hv, int nv, int drop, const L& pl,
+                                                   int& istar, int& l, int& r) {
+  const int m = nv - 1;
+  int a = 0, b = m;
+  while (a < b) {
+    const int i = (a + b) >> 1;
+    const double2 v0 = hv[i], v1 = hv[i + 1];
+    if (pl.le0(v1.x - v0.x, v1.y - v0.y)) b = i; else a = i + 1;
+  }
+  istar = a;
+  const double2 vs = hv[a];
+  const double Dd = (double)drop;
+  a = 0; b = istar;
+  while (a < b) {
+    const int j = (a + b) >> 1;
+    const double2 v = hv[j];
+    if (pl.ge0(v.x - vs.x, (v.y - vs.y) + Dd)) b = j; else a = j + 1;
+  }
+  const int2 vsi = hull[istar];
+  if (a == 0) {
+    l = hull[0].x;
+  } else {
+    const int2 A = hull[a - 1], B = hull[a];
+    l = (int)seg_first_true_p(A, B, vsi, drop, pl, (long long)A.x + 1, (long long)B.x);
+  }
+  a = istar; b = m;
+  while (a < b) {
+    const int j = (a + b + 1) >> 1;
+    const double2 v = hv[j];
+    if (pl.ge0(v.x - vs.x, (v.y - vs.y) + Dd)) a = j; else b = j - 1;
+  }
+  if (a == m) {
+    r = hull[m].x;
+  } else {
+    const int2 A = hull[a], B = hull[a + 1];
+    r = (int)seg_last_true_p(A, B, vsi, drop, pl, (long long)A.x, (long long)B.x - 1);
+  }
+}
+
+// An enclosure of log2|z| from plain fp64 (finite nonzero z): |z|^2 4^-e in [1/4, 2) to 2^-52 relative,
+// log2 to 1 ulp, so |error| < 2^-50.5 + 2^-52 |lambda|; the enclosure is widened to 2^-48 + 2^-50 |lambda|.
+__device__ __forceinline__ void lambda_enclosure(double x, double y, bool cplx, double& lo, double& hi, double& mid) {
+  double ax = fabs(x), ay = cplx ? fabs(y) : 0.0;
+  if (ay > ax) { const double t = ax; ax = ay; ay = t; }
+  const int e = frexp_exp(ax);
+  const double xs = ldexp(ax, -e), ys = ldexp(ay, -e);
+  const double v = __fma_rn(xs, xs, ys * ys);
+  mid = (double)e + 0.5 * log2(v);
+  const double w = __fma_rn(fabs(mid), 0x1p-50, 0x1p-48);
+  lo = mid - w;
+  hi = mid + w;
 }
 
 __device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ a, int n, int key) {

@@ -89,12 +89,26 @@ __global__ void __launch_bounds__(256) k_classify_bucket(const void* __restrict_
     if (ok) {
       double x, y;
       load_point<PK>(pts, i, x, y);
-      int hard;
-      double lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
+      int hard = 0;
+      double lam = 0.0;
       int istar, l, r;
-      if (staged && P.dbl_ok) classify_lambda_v<true>(hull, hv, P.nv, P.drop, lam, istar, l, r);
-      else if (staged) classify_lambda_v<false>(hull, hv, P.nv, P.drop, lam, istar, l, r);
-      else classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
+      bool done = false;
+      if (staged && P.dbl_ok && isfinite(x) && isfinite(y) && (x != 0.0 || (PtTraits<PK>::cplx && y != 0.0))) {
+        // fast path: searches on an enclosure of log2|z|; only undecided points compute the rounded lambda
+        // (the diagnostics still report the rounded lambda, so the tests check this path's indexing)
+        double lo, hi;
+        lambda_enclosure(x, y, PtTraits<PK>::cplx, lo, hi, lam);
+        bool amb = false;
+        classify_lambda_vp(hull, hv, P.nv, P.drop, LamIv{lo, hi, &amb}, istar, l, r);
+        done = !amb;
+        if (done && diag) lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
+      }
+      if (!done) {
+        lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
+        if (staged && P.dbl_ok) classify_lambda_v<true>(hull, hv, P.nv, P.drop, lam, istar, l, r);
+        else if (staged) classify_lambda_v<false>(hull, hv, P.nv, P.drop, lam, istar, l, r);
+        else classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
+      }
       lr[i] = make_int2(l, r);
       key = lambda_key(lam, l, r);
       keys[i] = key;

@@ -249,3 +249,16 @@ def test_plain_float_output(fpe):
     ref_re = np.ldexp(v1.real, np.clip(e1, -4000, 4000).astype(np.int32))
     ref_im = np.ldexp(v1.imag, np.clip(e1, -4000, 4000).astype(np.int32))
     assert np.array_equal(v2.real, ref_re) and np.array_equal(v2.imag, ref_im)
+
+
+def test_diag_and_plain_paths_agree(fpe):
+    """The classifier decides windows on an enclosure of log2|z| and falls back to the correctly rounded
+    lambda only when undecided; with diagnostics on it also reports the rounded lambda.  Both runs must
+    give bitwise-identical values (the windows, hence the arithmetic, are the same)."""
+    for cfg, d in ((3, (1 << 18) - 1), (2, (1 << 16) - 1), (1, None)):
+        a = workloads.coefficients(cfg, d=d)
+        pts = workloads.points(cfg, 1 << 16, shard=3)
+        poly = fpe.precondition(a)
+        o1 = gpu_eval(poly, pts, diag=True)
+        o2 = gpu_eval(poly, pts, diag=False)
+        assert np.array_equal(o1["v"], o2["v"]) and np.array_equal(o1["e"], o2["e"]), cfg
