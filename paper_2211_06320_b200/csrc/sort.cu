@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restri
   const int lane = threadIdx.x & 31;
   const long long beg = (long long)blockIdx.x * ppc;
   const long long end = min(n, beg + ppc);
-  constexpr int U = 4;   // independent loads in flight per thread
+  constexpr int U = 8;   // independent loads in flight per thread
   for (long long i0 = beg + threadIdx.x; i0 - lane < end; i0 += (long long)U * blockDim.x) {
     uint32_t key[U];
     int2 w[U];
