@@ -58,7 +58,8 @@ __device__ __forceinline__ uint32_t lambda_key(double lam, int l, int r) {
 }
 
 template <int PK>
-__global__ void __launch_bounds__(256) k_classify_bucket(const void* __restrict__ pts, long long n, int ppc, PolyDev P,
+__global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void* __restrict__ pts, long long n,
+                                                                     long long ppc, PolyDev P,
                                                          int2* __restrict__ lr, uint32_t* __restrict__ keys,
                                                          uint32_t* __restrict__ gcount,
                                                          uint32_t* __restrict__ cta_base,
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(256) k_classify_bucket(const void* __restrict_
       }
       lr[i] = make_int2(l, r);
       key = lambda_key(lam, l, r);
-      keys[i] = key;
+      keys[2 * i] = key;
       if (diag) {
         fpe_diag dg;
         dg.lambda = lam; dg.region = istar; dg.l = l; dg.r = r;
@@ -121,9 +122,15 @@ __global__ void __launch_bounds__(256) k_classify_bucket(const void* __restrict_
       if (hard) atomicAdd(hard_ctr, 1ull);
     }
     // one shared-memory atomic per distinct bucket in the warp
+    // one shared-memory atomic per distinct bucket in the warp; every point keeps its rank inside its
+    // (CTA, bucket) slice, so the scatter needs no atomics
     const uint32_t c = ok ? key >> (24 - kCoarseBits) : 0xffffffffu;
     const uint32_t peers = __match_any_sync(0xffffffffu, c);
-    if (ok && lane == __ffs(peers) - 1) atomicAdd(&hist[c], (uint32_t)__popc(peers));
+    const int leader = __ffs(peers) - 1;
+    uint32_t r0 = 0;
+    if (ok && lane == leader) r0 = atomicAdd(&hist[c], (uint32_t)__popc(peers));
+    r0 = __shfl_sync(0xffffffffu, r0, leader);
+    if (ok) keys[2 * i + 1] = r0 + __popc(peers & ((1u << lane) - 1));
   }
   __syncthreads();
   // claim this CTA's slice of every bucket
@@ -796,7 +803,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
 // host side
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-static size_t n_ctas(long long n) { const int p = pts_per_cta(n); return (size_t)((n + p - 1) / p); }
+static size_t n_ctas(long long n) { const long long p = pts_per_cta(n); return (size_t)((n + p - 1) / p); }
 // scratch for parallel pieces: 2 bytes per point (at least 1 MiB), in slots of 1 KiB (64 double2)
 static size_t scratch_slots(long long n) {
   size_t bytes = max((size_t)n * 2, (size_t)1 << 20);
@@ -804,7 +811,7 @@ static size_t scratch_slots(long long n) {
 }
 
 size_t tiled_ws_bytes(long long n) {
-  return al256(n * sizeof(int2)) + al256(n * sizeof(uint32_t)) + al256(n * sizeof(PtRec)) + al256(n * sizeof(double2)) +
+  return al256(n * sizeof(int2)) + al256(n * sizeof(uint2)) + al256(n * sizeof(PtRec)) + al256(n * sizeof(double2)) +
          al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 3 * al256((kBuckets + 1) * sizeof(uint32_t)) +
          al256(max_groups(n) * sizeof(GroupDesc)) + al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
@@ -852,7 +859,8 @@ static void launch_classify_bucket_t(const void* pts, long long n, const PolyDev
                                      uint32_t* gcount, uint32_t* cta_base, fpe_diag* diag, unsigned long long* hard,
                                      cudaStream_t s) {
   size_t smem = P.nv <= kSmemHullDbl ? P.nv * (sizeof(int2) + sizeof(double2)) : 0;
-  k_classify_bucket<PK><<<(int)n_ctas(n), 256, smem, s>>>(pts, n, pts_per_cta(n), P, lr, keys, gcount, cta_base,
+  k_classify_bucket<PK><<<(int)n_ctas(n), kScatterThreads, smem, s>>>(pts, n, pts_per_cta(n), P, lr, keys, gcount,
+                                                                     cta_base,
                                                           diag, hard);
 }
 
@@ -894,7 +902,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
               fpe_diag* diag, void* ws, unsigned long long* hard, Stage& st, cudaStream_t s) {
   char* p = static_cast<char*>(ws);
   int2* lr = reinterpret_cast<int2*>(p); p += al256(n * sizeof(int2));          // later: sorted windows
-  uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += al256(n * 4);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += al256(n * 8);            // {key, rank in (CTA, bucket)}
   PtRec* rec = reinterpret_cast<PtRec*>(p); p += al256(n * sizeof(PtRec));
   double2* zs = reinterpret_cast<double2*>(p); p += al256(n * sizeof(double2));   // points in sorted order
   uint32_t* cta_base = reinterpret_cast<uint32_t*>(p); p += al256(n_ctas(n) * kBuckets * 4);
@@ -922,7 +930,8 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     default: launch_classify_bucket_t<FPE_C32>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
   }
   st.mark("classify");
-  bucket_finish(keys, lr, n, pts_per_cta(n), gcount, cta_base, bstart, istart, rec, pk, pts, zs, P.k_min, plan, s);
+  bucket_finish(reinterpret_cast<const uint2*>(keys), lr, n, pts_per_cta(n), gcount, cta_base, bstart, istart, rec, pk,
+                pts, zs, P.k_min, plan, s);
   st.mark("bucket");
   int le = 0;
 #define FPE_EV(PKV, CKV) \

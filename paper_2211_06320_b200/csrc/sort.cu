@@ -16,6 +16,7 @@
 // Order inside a (CTA, bucket) run and inside equal keys is unspecified; every point's arithmetic
 // depends only on its own window, so results do not depend on it (bitwise).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 #include "sort.cuh"
 #include "fpe_internal.h"
@@ -78,49 +79,6 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(const uint32_t* __restrict
   }
 }
 
-// Records to bucket positions.  Lanes of a warp that hit the same bucket are aggregated
-// (__match_any_sync) so that each distinct bucket costs one shared-memory atomic per warp.
-__global__ void __launch_bounds__(256) k_bucket_scatter(const uint32_t* __restrict__ keys,
-                                                        const int2* __restrict__ lr, long long n, int ppc,
-                                                        const uint32_t* __restrict__ bstart,
-                                                        const uint32_t* __restrict__ cta_base,
-                                                        PtRec* __restrict__ rec) {
-  __shared__ uint32_t cnt[kBuckets];
-  __shared__ uint32_t base[kBuckets];
-  for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) {
-    cnt[b] = 0;
-    base[b] = bstart[b] + cta_base[(size_t)blockIdx.x * kBuckets + b];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const long long beg = (long long)blockIdx.x * ppc;
-  const long long end = min(n, beg + ppc);
-  constexpr int U = 8;   // independent loads in flight per thread
-  for (long long i0 = beg + threadIdx.x; i0 - lane < end; i0 += (long long)U * blockDim.x) {
-    uint32_t key[U];
-    int2 w[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = i0 + (long long)u * blockDim.x;
-      key[u] = 0xffffffffu;
-      if (i < end) { key[u] = __ldg(keys + i); w[u] = __ldg(lr + i); }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = i0 + (long long)u * blockDim.x;
-      const bool ok = i < end;
-      const uint32_t c = ok ? key[u] >> (24 - kCoarseBits) : 0xffffffffu;
-      const uint32_t peers = __match_any_sync(0xffffffffu, c);
-      const int leader = __ffs(peers) - 1;
-      const uint32_t rank = __popc(peers & ((1u << lane) - 1));
-      uint32_t r0 = 0;
-      if (ok && lane == leader) r0 = atomicAdd(&cnt[c], (uint32_t)__popc(peers));
-      r0 = __shfl_sync(0xffffffffu, r0, leader);
-      if (ok) rec[base[c] + r0 + rank] = PtRec{(int32_t)i, key[u], w[u].x, w[u].y};
-    }
-  }
-}
-
 __device__ __forceinline__ double2 load_point_any(int pk, const void* __restrict__ p, long long i) {
   switch (pk) {
     case FPE_R64: return make_double2(__ldg(static_cast<const double*>(p) + i), 0.0);
@@ -130,36 +88,67 @@ __device__ __forceinline__ double2 load_point_any(int pk, const void* __restrict
   }
 }
 
+// Records to bucket positions: bucket start + the classifying CTA's slice of the bucket + the point's rank
+// in that slice (both from the classifier) -- a pure streaming pass over all points, no atomics.
+__global__ void __launch_bounds__(256) k_bucket_scatter(const uint2* __restrict__ keys, const int2* __restrict__ lr,
+                                                        long long n, long long ppc,
+                                                        const uint32_t* __restrict__ bstart,
+                                                        const uint32_t* __restrict__ cta_base,
+                                                        PtRec* __restrict__ rec) {
+  constexpr int U = 4;   // independent loads in flight per thread
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    uint2 kr[U];
+    int2 w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < n) { kr[u] = __ldg(keys + i); w[u] = __ldg(lr + i); }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < n) {
+        const uint32_t c = kr[u].x >> (24 - kCoarseBits);
+        const uint32_t pos = __ldg(bstart + c) + __ldg(cta_base + (size_t)(i / ppc) * kBuckets + c) + kr[u].y;
+        rec[pos] = PtRec{(int32_t)i, kr[u].x, w[u].x, w[u].y};
+      }
+    }
+  }
+}
+
 // Counting sort of every chunk of the records by key bits [1, 1 + kLocalBits), in place: afterwards the
 // records (and the windows slr, for the planner) are ordered by key bits 1..23 (buckets are laid out in
-// key order); the points are gathered into the same order (zs, as doubles), so that every later pass
-// reads them coalesced.
-constexpr size_t kChunkSortSmem = (size_t)kChunkPts * sizeof(PtRec) + (1u << kLocalBits) * sizeof(uint32_t);
-__global__ void __launch_bounds__(256) k_chunk_sort(PtRec* __restrict__ rec, int2* __restrict__ slr,
-                                                    int pk, const void* __restrict__ pts, double2* __restrict__ zs,
+// key order), so that every later pass reads them coalesced.
+constexpr size_t kChunkSortSmem = (size_t)kChunkPts * (sizeof(PtRec) + sizeof(uint16_t)) +
+                                  (1u << kLocalBits) * sizeof(uint32_t);
+__global__ void __launch_bounds__(256) k_chunk_sort(PtRec* __restrict__ rec, int2* __restrict__ slr, int pk,
+                                                    const void* __restrict__ pts, double2* __restrict__ zs,
                                                     const uint32_t* __restrict__ gcount,
                                                     const uint32_t* __restrict__ bstart,
                                                     const uint32_t* __restrict__ istart) {
   extern __shared__ __align__(16) unsigned char sm[];
   PtRec* s_rec = reinterpret_cast<PtRec*>(sm);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(sm + (size_t)kChunkPts * sizeof(PtRec));
+  uint16_t* s_dst = reinterpret_cast<uint16_t*>(sm + (size_t)kChunkPts * sizeof(PtRec));
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sm + (size_t)kChunkPts * (sizeof(PtRec) + sizeof(uint16_t)));
   const int c = blockIdx.x;
   if (c >= (int)istart[kBuckets]) return;
   int bucket, npts;
   uint32_t p0;
   chunk_of(istart, gcount, bstart, c, bucket, p0, npts);
   for (int b = threadIdx.x; b < (1 << kLocalBits); b += blockDim.x) hist[b] = 0;
+  // records in (coalesced), staged in shared memory
+  for (int j = threadIdx.x; j < npts; j += 256)
+    reinterpret_cast<int4*>(s_rec)[j] = __ldg(reinterpret_cast<const int4*>(rec + p0 + j));
   __syncthreads();
   constexpr int kPer = kChunkPts / 256;
   uint32_t my_bin[kPer];
-  int4 my_h[kPer];
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
     const int j = threadIdx.x + q * 256;
     my_bin[q] = 0;
     if (j < npts) {
-      my_h[q] = __ldg(reinterpret_cast<const int4*>(rec + p0 + j));
-      my_bin[q] = ((uint32_t)my_h[q].y >> 1) & ((1u << kLocalBits) - 1);
+      my_bin[q] = (s_rec[j].key >> 1) & ((1u << kLocalBits) - 1);
       atomicAdd(&hist[my_bin[q]], 1u);
     }
   }
@@ -179,15 +168,14 @@ __global__ void __launch_bounds__(256) k_chunk_sort(PtRec* __restrict__ rec, int
 #pragma unroll
   for (int q = 0; q < kPer; ++q) {
     const int j = threadIdx.x + q * 256;
-    if (j < npts) {
-      const uint32_t d = atomicAdd(&hist[my_bin[q]], 1u);
-      reinterpret_cast<int4*>(s_rec + d)[0] = my_h[q];
-    }
+    if (j < npts) s_dst[j] = (uint16_t)atomicAdd(&hist[my_bin[q]], 1u);
   }
   __syncthreads();
+  // records out to their sorted positions inside the chunk (the chunk's lines complete in L2), with the
+  // points gathered into the same order (independent random loads issued together)
   double2 z[kPer];
 #pragma unroll
-  for (int q = 0; q < kPer; ++q) {   // gathers issued together (independent random loads)
+  for (int q = 0; q < kPer; ++q) {
     const int j = threadIdx.x + q * 256;
     if (j < npts) z[q] = load_point_any(pk, pts, s_rec[j].idx);
   }
@@ -195,9 +183,10 @@ __global__ void __launch_bounds__(256) k_chunk_sort(PtRec* __restrict__ rec, int
   for (int q = 0; q < kPer; ++q) {
     const int j = threadIdx.x + q * 256;
     if (j < npts) {
-      rec[p0 + j] = s_rec[j];
-      slr[p0 + j] = make_int2(s_rec[j].l, s_rec[j].r);
-      zs[p0 + j] = z[q];
+      const int d = s_dst[j];
+      rec[p0 + d] = s_rec[j];
+      slr[p0 + d] = make_int2(s_rec[j].l, s_rec[j].r);
+      zs[p0 + d] = z[q];
     }
   }
 }
@@ -246,12 +235,12 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const int2* __restric
   (void)single;
 }
 
-void bucket_finish(const uint32_t* keys, int2* lr, long long n, int ppc, const uint32_t* gcount,
+void bucket_finish(const uint2* keys, int2* lr, long long n, long long ppc, const uint32_t* gcount,
                    const uint32_t* cta_base, uint32_t* bstart, uint32_t* istart, PtRec* rec, int pk,
                    const void* pts, double2* zs, long long k_min, const Plan& plan, cudaStream_t s) {
   k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, istart);
-  const int ctas = (int)((n + ppc - 1) / ppc);
-  k_bucket_scatter<<<ctas, 256, 0, s>>>(keys, lr, n, ppc, bstart, cta_base, rec);
+  const long long blocks = std::min<long long>((n + 4 * 256 - 1) / (4 * 256), 148ll * 32);
+  k_bucket_scatter<<<(int)blocks, 256, 0, s>>>(keys, lr, n, ppc, bstart, cta_base, rec);
   // the sorted windows are written over lr: k_chunk_sort reads only the records
   static bool attr = false;
   if (!attr) {

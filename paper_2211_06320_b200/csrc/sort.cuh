@@ -6,12 +6,13 @@
 namespace fpe {
 constexpr int kCoarseBits = 12;                 // global buckets: top 12 of the 24 key bits
 constexpr int kBuckets = 1 << kCoarseBits;
-constexpr int kPtsPerCta = 32768;               // points per CTA of classify / scatter (at most)
-// points per classify / scatter CTA for a batch of n: enough CTAs to fill the GPU for small batches
-inline int pts_per_cta(long long n) {
-  long long p = (n + 148 * 8 - 1) / (148 * 8);
-  p = (p + 255) / 256 * 256;
-  return (int)(p < 2048 ? 2048 : (p > kPtsPerCta ? kPtsPerCta : p));
+constexpr int kScatterThreads = 1024;           // classify / scatter CTA size: one CTA per SM
+// points per classify / scatter CTA for a batch of n: one 1024-thread CTA per SM, so that the scatter's
+// open output lines (148 CTAs x 4096 buckets x 128 B = 77 MB) stay in L2 until they are complete
+inline long long pts_per_cta(long long n) {
+  long long p = (n + 147) / 148;
+  p = (p + 1023) / 1024 * 1024;
+  return p < 1024 ? 1024 : p;
 }
 constexpr int kChunkPts = 2048;                 // points per evaluator work item (one bucket's slice)
 constexpr int kLocalBits = 11;                  // in-chunk counting sort on key bits [1, 12)
@@ -62,7 +63,7 @@ __device__ __forceinline__ void chunk_of(const uint32_t* istart, const uint32_t*
 // bucket starts + item table (k_bucket_scan), records in bucket order (k_bucket_scatter), the records
 // sorted in place, their windows (written over lr) and points (zs) in sorted order (k_chunk_sort), and the
 // work plan (k_plan)
-void bucket_finish(const uint32_t* keys, int2* lr, long long n, int ppc, const uint32_t* gcount,
+void bucket_finish(const uint2* keys, int2* lr, long long n, long long ppc, const uint32_t* gcount,
                    const uint32_t* cta_base, uint32_t* bstart, uint32_t* istart, PtRec* rec, int pk,
                    const void* pts, double2* zs, long long k_min, const Plan& plan, cudaStream_t s);
 inline long long max_chunks(long long n) { return (n + kChunkPts - 1) / kChunkPts + kBuckets; }
