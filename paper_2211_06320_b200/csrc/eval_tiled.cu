@@ -7,8 +7,8 @@
 //                    histogram and slice claims (sort.cu).  l and r are both non-decreasing in lambda
 //                    (d/dlambda of cover(k) + lambda k - N is k - k_lambda), so points with close keys
 //                    have nested, nearly equal windows.
-//   bucket scan/scatter + k_chunk_sort + k_plan (sort.cu): permutation and windows sorted by key (bits
-//                    1..23), cut into groups of 32*NP consecutive points; per group the union window and the work
+//   bucket scan/scatter + k_plan (sort.cu): records and points in the order of the top 15 key bits,
+//                    cut into groups of 32*NP consecutive points; per group the union window and the work
 //                    items (one whole group, or one item per kPiece-aligned piece of a long window).
 //   k_eval_tiled     persistent warps: first the parallel pieces, then every other group in order.  A warp streams the coefficients of its item's range through a
 //                    private 3-stage shared-memory ring filled by 1-D TMA bulk copies (cp.async.bulk +
@@ -66,12 +66,12 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
                                                          fpe_diag* __restrict__ diag,
                                                          unsigned long long* __restrict__ hard_ctr) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  __shared__ uint32_t hist[kBuckets];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(s_dyn);   // kBuckets counters, then the staged cover
   const int2* hull = P.hull;
-  double2* hv = reinterpret_cast<double2*>(s_dyn);
+  double2* hv = reinterpret_cast<double2*>(s_dyn + kBuckets * sizeof(uint32_t));
   const bool staged = P.nv <= kSmemHullDbl;
   if (staged) {
-    int2* sh = reinterpret_cast<int2*>(s_dyn + (size_t)P.nv * sizeof(double2));
+    int2* sh = reinterpret_cast<int2*>(s_dyn + kBuckets * sizeof(uint32_t) + (size_t)P.nv * sizeof(double2));
     for (int i = threadIdx.x; i < P.nv; i += blockDim.x) {
       const int2 v = P.hull[i];
       sh[i] = v;
@@ -458,7 +458,7 @@ __device__ __forceinline__ void load_group(Pts<NP>& S, uint32_t g, long long n, 
     S.idx[j] = 0; S.x[j] = 0.0; S.y[j] = 0.0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
     if (S.valid[j]) {
       const int4 h = __ldg(reinterpret_cast<const int4*>(rec + pos));
-      const double2 z = __ldg(zs + pos);
+      const double2 z = __ldg(reinterpret_cast<const double2*>(rec + pos) + 1);
       S.idx[j] = h.x; S.x[j] = z.x; S.y[j] = z.y;
       if (h.w >= h.z) { S.wl[j] = h.z - kmin; S.wr[j] = h.w - kmin; }
     }
@@ -499,7 +499,7 @@ __device__ __forceinline__ void group_load(GroupCtx<NP>& c, uint32_t g, long lon
       const long long pos = (long long)g * (32 * NP) + j * 32 + lane;
       if (pos < n) {
         c.h[j] = __ldg(reinterpret_cast<const int4*>(rec + pos));
-        c.z[j] = __ldg(zs + pos);
+        c.z[j] = __ldg(reinterpret_cast<const double2*>(rec + pos) + 1);
       }
     }
   }
@@ -811,8 +811,8 @@ static size_t scratch_slots(long long n) {
 }
 
 size_t tiled_ws_bytes(long long n) {
-  return al256(n * sizeof(int2)) + al256(n * sizeof(uint2)) + al256(n * sizeof(PtRec)) + al256(n * sizeof(double2)) +
-         al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 3 * al256((kBuckets + 1) * sizeof(uint32_t)) +
+  return al256(n * sizeof(int2)) + al256(n * sizeof(uint2)) + al256(n * sizeof(PtRec)) +
+         al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) +
          al256(max_groups(n) * sizeof(GroupDesc)) + al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
 }
@@ -835,7 +835,7 @@ static int launch_eval_tiled_t(const double2* zs, long long n, const PolyDev& P,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid = max(1, per_sm) * sms;
   }
-  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(zs, n, P, rec, plan, vals, exps);
+  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(nullptr, n, P, rec, plan, vals, exps);
   return 1;
 }
 
@@ -858,7 +858,8 @@ template <int PK>
 static void launch_classify_bucket_t(const void* pts, long long n, const PolyDev& P, int2* lr, uint32_t* keys,
                                      uint32_t* gcount, uint32_t* cta_base, fpe_diag* diag, unsigned long long* hard,
                                      cudaStream_t s) {
-  size_t smem = P.nv <= kSmemHullDbl ? P.nv * (sizeof(int2) + sizeof(double2)) : 0;
+  const size_t smem = kBuckets * sizeof(uint32_t) + (P.nv <= kSmemHullDbl ? P.nv * (sizeof(int2) + sizeof(double2)) : 0);
+  cudaFuncSetAttribute(k_classify_bucket<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_classify_bucket<PK><<<(int)n_ctas(n), kScatterThreads, smem, s>>>(pts, n, pts_per_cta(n), P, lr, keys, gcount,
                                                                      cta_base,
                                                           diag, hard);
@@ -904,11 +905,9 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   int2* lr = reinterpret_cast<int2*>(p); p += al256(n * sizeof(int2));          // later: sorted windows
   uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += al256(n * 8);            // {key, rank in (CTA, bucket)}
   PtRec* rec = reinterpret_cast<PtRec*>(p); p += al256(n * sizeof(PtRec));
-  double2* zs = reinterpret_cast<double2*>(p); p += al256(n * sizeof(double2));   // points in sorted order
   uint32_t* cta_base = reinterpret_cast<uint32_t*>(p); p += al256(n_ctas(n) * kBuckets * 4);
   uint32_t* gcount = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   uint32_t* bstart = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
-  uint32_t* istart = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   Plan plan;
   plan.desc = reinterpret_cast<GroupDesc*>(p); p += al256(max_groups(n) * sizeof(GroupDesc));
   plan.gcnt = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
@@ -930,12 +929,12 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     default: launch_classify_bucket_t<FPE_C32>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
   }
   st.mark("classify");
-  bucket_finish(reinterpret_cast<const uint2*>(keys), lr, n, pts_per_cta(n), gcount, cta_base, bstart, istart, rec, pk,
-                pts, zs, P.k_min, plan, s);
+  bucket_finish(reinterpret_cast<const uint2*>(keys), lr, n, pts_per_cta(n), gcount, cta_base, bstart, rec, pk, pts,
+                P.k_min, plan, s);
   st.mark("bucket");
   int le = 0;
 #define FPE_EV(PKV, CKV) \
-  le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(zs, n, P, rec, plan, vals, exps, s)
+  le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(nullptr, n, P, rec, plan, vals, exps, s)
   switch (pk * 4 + P.cdt) {
     case FPE_R64 * 4 + FPE_R64: FPE_EV(FPE_R64, FPE_R64); break;
     case FPE_R64 * 4 + FPE_C64: FPE_EV(FPE_R64, FPE_C64); break;
@@ -949,7 +948,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   }
 #undef FPE_EV
   st.mark("eval_tiled");
-  return 5 + le;
+  return 4 + le;
 }
 
 }  // namespace fpe
