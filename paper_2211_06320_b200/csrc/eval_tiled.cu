@@ -394,7 +394,7 @@ __device__ __forceinline__ xc_t power_polar(double x, double y, long long n) {  
 }
 
 template <bool CPLX>
-__device__ __forceinline__ void acc_fold(Acc& A, double hr, double hi, int pbase, double x, double y) {
+__device__ __noinline__ void acc_fold(Acc& A, double hr, double hi, int pbase, double x, double y) {
   if (!A.started) { A.r = hr; A.i = hi; A.base = pbase; A.started = true; return; }
   const int gap = A.base - pbase;
   const xc_t m = (gap == kPiece) ? power_piece<CPLX>(x, y) : power_polar<CPLX>(x, y, gap);
@@ -404,8 +404,8 @@ __device__ __forceinline__ void acc_fold(Acc& A, double hr, double hi, int pbase
 }
 
 template <int OK, bool CPLX>
-__device__ __forceinline__ void finalize(void* vals, long long* exps, long long idx, double x, double y,
-                                         const Acc& A, const PolyDev& P) {
+__device__ __noinline__ void finalize(void* vals, long long* exps, long long idx, double x, double y, Acc A,
+                                      const PolyDev& P) {
 #ifdef FPE_EXP_NO_FINALIZE
   if (A.r == 1.2345) store_value<OK>(vals, exps, idx, A.r, A.i, 0);
   return;
@@ -845,13 +845,13 @@ static int launch_eval_tiled_t(const double2* zs, long long n, const PolyDev& P,
 template <int PK, int CK>
 struct NPFor {
   static constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
-  static constexpr int value = cplx ? 2 : 4;
+  static constexpr int value = 4;
   static constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
 };
 
 static int np_for(int pk, int cdt) {
   const bool cplx = (pk == FPE_C64 || pk == FPE_C32 || cdt == FPE_C64 || cdt == FPE_C32);
-  return cplx ? 2 : 4;
+  return 4;
 }
 
 template <int PK>
