@@ -644,7 +644,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(const double2* __
   const int kmin = (int)P.k_min;
   if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
   GroupCtx<NP> cur;
-  auto gid = [&](uint32_t it) { return it; };
+  // reverse bucket order: the long-window groups (the largest single items) first, the shortest last,
+  // so that the tail of the persistent loop is short
+  auto gid = [&](uint32_t it) { return it < plan.ngroups ? plan.ngroups - 1 - it : plan.ngroups; };
   group_load<PK, NP>(cur, gid(__shfl_sync(0xffffffffu, nxt, 0)), n, plan, rec, zs, kmin);
   if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
   while (cur.g < plan.ngroups) {
