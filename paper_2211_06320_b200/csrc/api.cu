@@ -356,7 +356,8 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   const bool cplx_out = (pt_dt == FPE_C64 || pt_dt == FPE_C32 || h->hdr.dtype == FPE_C64 || h->hdr.dtype == FPE_C32);
   const size_t in_sz = dtype_size(pt_dt);
   const size_t out_sz = is_f32(pt_dt) ? (cplx_out ? 8 : 4) : (cplx_out ? 16 : 8);
-  const long long chunk = std::min<long long>(n_points, 1ll << 22);
+  // large chunks: the evaluator groups points of similar |z|, which needs many points per batch
+  const long long chunk = std::min<long long>(n_points, 1ll << 24);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   constexpr int kSlots = 3;
   const size_t per = al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8) + ws_bytes_for(chunk);

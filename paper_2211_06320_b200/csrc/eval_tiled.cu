@@ -806,9 +806,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static size_t n_ctas(long long n) { const long long p = pts_per_cta(n); return (size_t)((n + p - 1) / p); }
-// scratch for parallel pieces: 2 bytes per point (at least 1 MiB), in slots of 1 KiB (64 double2)
+// scratch for parallel pieces: 4 bytes per point (at least 1 MiB), counted in 1 KiB units
 static size_t scratch_slots(long long n) {
-  size_t bytes = max((size_t)n * 2, (size_t)1 << 20);
+  size_t bytes = max((size_t)n * 4, (size_t)1 << 20);
   return bytes / 1024;
 }
 
