@@ -270,6 +270,21 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def profiled_traffic(kernel_prefix: str = "void k_eval_tiled"):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the committed ncu --set full
+    summary (profiles/r01_ncu_eval_tiled_cfg3.json, captured on the same workload); None if absent."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_eval_tiled_cfg3.json")
+    try:
+        with open(path) as f:
+            for k in json.load(f):
+                if k.get("kernel", "").startswith(kernel_prefix):
+                    return {"bytes": 1e9 * (k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]),
+                            "source": os.path.relpath(path, ROOT)}
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
+
+
 def run_fpe(args):
     import numpy as np
     import torch
@@ -380,7 +395,12 @@ def run_fpe(args):
                    "l2": "inputs (1 GiB/rank) larger than L2; no flush", "mean_kept_terms": meanK,
                    "hard_lambdas": hard},
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak,
+                     "traffic": (profiled_traffic() or {}).get("bytes"),
+                     "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of k_eval_tiled "
+                                     "(profiles/r01_ncu_eval_tiled_cfg3.json); algorithmic bytes 40 B/pt = "
+                                     f"{40 * n / 1e9:.2f} GB: the excess is the read-modify-write of the random "
+                                     "16-B/8-B output stores",
                      "peak_note": "fp64 FMA: 148 SM x 64 lanes x 1.965 GHz x 2 (guide unit counts/clock)",
                      "algorithmic_fma_per_launch": fma_total, "kernel_ms": dom_ms, "stages_ms": stages},
         "cpu_baseline": cpu,

@@ -74,7 +74,10 @@ typedef struct {
     int32_t r;
     int32_t kept;       /* K = #(G_p cap [l, r])                                           */
     int32_t hard;       /* 1 if lambda was within 2^-96 |lambda| of an fp64 rounding boundary */
-    int32_t pad;
+    int32_t cancel;     /* canceled bits c = s(M) - s(Q) (eq:def_prec_loss) with
+                           s(M) estimated by ceil(N_lambda), N_lambda = cover(k_lambda) + lambda k_lambda
+                           (log2 M lies in [N - 1, N]); the result has about p - c correct bits
+                           (Theorem thm:equivAlgo); INT32_MIN when Q = 0 or z is non-finite      */
 } fpe_diag;
 
 /*

@@ -243,9 +243,9 @@ def header_fields(buf: np.ndarray) -> dict:
 
 
 def diag_fields(dg):
-    """Split a (n, 32) uint8 diag tensor into named tensors (lambda, region, l, r, kept, hard)."""
+    """Split a (n, 32) uint8 diag tensor into named tensors (lambda, region, l, r, kept, hard, cancel)."""
     raw = dg.contiguous()
     lam = raw[:, 0:8].contiguous().view(_torch().float64).reshape(-1)
     ints = raw[:, 8:32].contiguous().view(_torch().int32).reshape(-1, 6)
     return {"lambda": lam, "region": ints[:, 0], "l": ints[:, 1], "r": ints[:, 2],
-            "kept": ints[:, 3], "hard": ints[:, 4]}
+            "kept": ints[:, 3], "hard": ints[:, 4], "cancel": ints[:, 5]}

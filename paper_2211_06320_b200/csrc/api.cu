@@ -299,6 +299,7 @@ fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t
     const size_t in_sz = dtype_size(pt_dt);
     const bool cplx_out = (pt_dt == FPE_C64 || pt_dt == FPE_C32 || h->hdr.dtype == FPE_C64 || h->hdr.dtype == FPE_C32);
     const size_t out_sz = is_f32(pt_dt) ? (cplx_out ? 8 : 4) : (cplx_out ? 16 : 8);
+    const int out_kind = is_f32(pt_dt) ? (cplx_out ? FPE_C32 : FPE_R32) : (cplx_out ? FPE_C64 : FPE_R64);
     const void* pp = static_cast<const char*>(points) + off * in_sz;
     void* vv = static_cast<char*>(values_out) + off * out_sz;
     long long* ee = exps_out ? reinterpret_cast<long long*>(exps_out) + off : nullptr;
@@ -307,6 +308,7 @@ fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t
       int l = run_tiled(pt_dt, pp, m, P, vv, ee, dd, workspace, h->dstats, stg, s);
       if (l < 0) { set_error("fpe_evaluate: tiled path rejected the launch"); return FPE_ERR_INVALID_ARG; }
       launches += l;
+      if (dd) { launch_confidence(out_kind, m, P, vv, ee, dd, s); launches += 1; }
     } else {
       int2* lr = static_cast<int2*>(workspace);
       launch_classify(pt_dt, pp, m, P, lr, dd, h->dstats, s);
@@ -314,6 +316,7 @@ fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t
       launch_eval_sparse(pt_dt, pp, m, P, lr, vv, ee, s);
       stg.mark("eval_sparse");
       launches += 2;
+      if (dd) { launch_confidence(out_kind, m, P, vv, ee, dd, s); launches += 1; }
     }
   }
   h->last_launches = launches;       // kernels of this library (memsets not counted)

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
       if (diag) {
         fpe_diag dg;
         dg.lambda = lam; dg.region = istar; dg.l = l; dg.r = r;
-        dg.kept = kept_count(P, l, r); dg.hard = hard; dg.pad = 0;
+        dg.kept = kept_count(P, l, r); dg.hard = hard; dg.cancel = INT32_MIN;
         diag[i] = dg;
       }
       if (hard) atomicAdd(hard_ctr, 1ull);

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) k_classify(const void* __restrict__ pts, 
     if (diag) {
       fpe_diag d;
       d.lambda = lam; d.region = istar; d.l = l; d.r = r;
-      d.kept = kept_count(P, l, r); d.hard = hard; d.pad = 0;
+      d.kept = kept_count(P, l, r); d.hard = hard; d.cancel = INT32_MIN;
       diag[i] = d;
     }
     if (hard) atomicAdd(hard_ctr, 1ull);
@@ -252,6 +252,38 @@ __global__ void __launch_bounds__(128) k_horner_full(const void* __restrict__ pt
 }
 
 // ------------------------------------------------------------------------------------------
+// Per-point confidence (eq:def_prec_loss; the errors file of P:2114-2118): after the
+// evaluation, c = ceil(N_lambda) - s(Q) with N_lambda = hh_i* + lambda hk_i* (the sheared cover's top,
+// log2 max_k |a_k z^k| in [N - 1, N]) and s(Q) the exact scale of the result (value = m 2^e with
+// max(|m_re|, |m_im|) in [1/2, 1): s = e + [m_re^2 + m_im^2 >= 1]).  Written into fpe_diag::cancel.
+template <int OK>
+__global__ void __launch_bounds__(256) k_confidence(long long n, PolyDev P, const void* __restrict__ vals,
+                                                    const long long* __restrict__ exps, fpe_diag* __restrict__ diag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    fpe_diag d = diag[i];
+    int c = INT32_MIN;
+    if (d.region >= 0 && isfinite(d.lambda)) {
+      double mr, mi;
+      if constexpr (OK == FPE_R64) { mr = static_cast<const double*>(vals)[i]; mi = 0.0; }
+      else if constexpr (OK == FPE_C64) { const double2 v = static_cast<const double2*>(vals)[i]; mr = v.x; mi = v.y; }
+      else if constexpr (OK == FPE_R32) { mr = static_cast<const float*>(vals)[i]; mi = 0.0; }
+      else { const float2 v = static_cast<const float2*>(vals)[i]; mr = v.x; mi = v.y; }
+      long long e = exps ? exps[i] : 0;
+      const double m = fmax(fabs(mr), fabs(mi));
+      if (m != 0.0 && isfinite(m)) {
+        const int k = frexp_exp(m);       // renormalise (plain-float outputs)
+        mr = ldexp(mr, -k); mi = ldexp(mi, -k); e += k;
+        const long long sQ = e + ((__fma_rn(mr, mr, mi * mi) >= 1.0) ? 1 : 0);
+        const int2 v = P.hull[d.region];
+        const double N = __fma_rn(d.lambda, (double)v.x, (double)v.y);
+        c = (int)max(-2000000000.0, min(2000000000.0, ceil(N) - (double)sQ));
+      }
+    }
+    diag[i].cancel = c;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // launchers
 static int grid_for(long long n, int block) {
   long long g = (n + block - 1) / block;
@@ -324,6 +356,16 @@ bool launch_eval_sparse(int pk, const void* pts, long long n, const PolyDev& P, 
                         long long* exps, cudaStream_t s) {
   FPE_DISPATCH_PC(launch_eval_sparse_t, pts, n, P, lr, vals, exps, s)
   return true;
+}
+
+void launch_confidence(int ok, long long n, const PolyDev& P, const void* vals, const long long* exps,
+                       fpe_diag* diag, cudaStream_t s) {
+  switch (ok) {
+    case FPE_R64: k_confidence<FPE_R64><<<grid_for(n, 256), 256, 0, s>>>(n, P, vals, exps, diag); break;
+    case FPE_C64: k_confidence<FPE_C64><<<grid_for(n, 256), 256, 0, s>>>(n, P, vals, exps, diag); break;
+    case FPE_R32: k_confidence<FPE_R32><<<grid_for(n, 256), 256, 0, s>>>(n, P, vals, exps, diag); break;
+    default: k_confidence<FPE_C32><<<grid_for(n, 256), 256, 0, s>>>(n, P, vals, exps, diag); break;
+  }
 }
 
 bool launch_horner(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,

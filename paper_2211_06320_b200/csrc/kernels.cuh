@@ -13,6 +13,9 @@ bool launch_eval_point(int pk, const void* pts, long long n, const PolyDev& P, c
                        long long* exps, cudaStream_t s);
 bool launch_eval_sparse(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
                         long long* exps, cudaStream_t s);
+// fpe_diag::cancel from the outputs (after an evaluation); ok = fpe_dtype of the values
+void launch_confidence(int ok, long long n, const PolyDev& P, const void* vals, const long long* exps,
+                       fpe_diag* diag, cudaStream_t s);
 bool launch_horner(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
                    cudaStream_t s);
 }  // namespace fpe

@@ -262,3 +262,27 @@ def test_diag_and_plain_paths_agree(fpe):
         o1 = gpu_eval(poly, pts, diag=True)
         o2 = gpu_eval(poly, pts, diag=False)
         assert np.array_equal(o1["v"], o2["v"]) and np.array_equal(o1["e"], o2["e"]), cfg
+
+
+def test_confidence_cancel_bits(fpe):
+    """fpe_diag::cancel (PAPER.md:1278-1285, eq:def_prec_loss): c = s(M) - s(P(z)), M = max_k |a_k z^k|.
+    The library estimates s(M) by ceil(N_lambda) (log2 M in [N - 1, N]) and takes s of its own result;
+    against the oracle's s(M) and s(P_ref) it may differ by 1 for each estimate."""
+    cases = [(workloads.coefficients(1), workloads.points(1, 4096, shard=4))]
+    # heavy cancellation: (z - 1)^40 near z = 1 loses many bits
+    from math import comb
+    a = np.array([comb(40, k) * (-1.0) ** (40 - k) for k in range(41)], dtype=np.complex128)
+    zc = 1 + 2.0 ** -np.arange(1, 30) * np.exp(1j * np.linspace(0, 6, 29))
+    cases.append((a, np.concatenate([zc, workloads.points(1, 500, shard=5)])))
+    for a, pts in cases:
+        poly = fpe.precondition(a)
+        P = oracle.OraclePoly(a)
+        out = gpu_eval(poly, pts)
+        c_gpu = out["diag"]["cancel"]
+        H = P.horner(pts)
+        sP = H.e + (np.abs(H.hi) >= 1.0)
+        sM = 1 + np.floor(P.log2_maxterm(pts)).astype(np.int64)
+        c_ref = sM - sP
+        ok = np.isfinite(P.log2_maxterm(pts)) & (c_ref < 40)
+        assert np.all(np.abs(c_gpu[ok] - c_ref[ok]) <= 2), (c_gpu[ok][:10], c_ref[ok][:10])
+        assert np.any(c_ref[ok] > 10) or a.shape[0] != 41   # the (z-1)^40 case does exercise cancellation
