@@ -169,6 +169,35 @@ fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n
                       void* stream);
 
 /*
+ * fpe_precondition_derivative -- preconditions P' ("the preconditioning of P and P'
+ * can be done simultaneously"; this implementation takes the paper's alternative, a separate
+ * preprocessing of P'): the coefficients b_j = (j+1) a_{j+1}, j = 0..d-1, are formed on the host in the
+ * working format (one rounding each) and preconditioned as by fpe_precondition (same arguments; coeffs
+ * are P's d+1 coefficients).  ZERO_POLY if P is constant.
+ */
+fpe_status fpe_precondition_derivative(const void* coeffs, int64_t n_coeffs, fpe_dtype dt, int32_t p_bits,
+                                       int32_t drop_override, int device, void* stream, fpe_poly* out);
+
+/* Bytes of device workspace fpe_newton_step needs for n_points points. */
+fpe_status fpe_newton_workspace_size(fpe_poly P, fpe_poly dP, int64_t n_points, size_t* bytes);
+
+/*
+ * fpe_newton_step -- one Newton step N_P(z) = z - P(z)/P'(z) (eq:newton) for every
+ * point: Q1 and Q2, the FPE values of P and P' (fpe_evaluate), stay in extended range (mantissa, int64
+ * exponent), so the quotient m1/m2 2^(e1-e2) is formed without overflow or loss -- the paper's
+ * "cancelation of valuation" m = min(l, l'): e.g. z^64 + 1 at z = 10 in FP32, where P and P'
+ * overflow, gives the increment 0.15625.
+ *   P, dP       handles of P and of P' (fpe_precondition_derivative), same device and precision.
+ *   points      device, n_points points of dtype pt_dt (as fpe_evaluate).
+ *   points_out  device, n_points values N_P(z) in the output type of fpe_evaluate (complex unless all real).
+ *   incr_out    device, n_points increments P(z)/P'(z) in the same type, or NULL.
+ *   workspace   device, at least fpe_newton_workspace_size bytes.
+ * Per point: P'(z) = 0 gives inf/NaN; non-finite z gives NaN.  Errors: INVALID_ARG, CUDA.
+ */
+fpe_status fpe_newton_step(fpe_poly P, fpe_poly dP, const void* points, fpe_dtype pt_dt, int64_t n_points,
+                           void* points_out, void* incr_out, void* workspace, size_t ws_bytes, void* stream);
+
+/*
  * Per-stage timing (measurement support for bench.py).  With fpe_set_profiling(h, 1) every
  * later fpe_evaluate / fpe_horner on h records CUDA events on its stream around each kernel;
  * fpe_last_stage_ms (synchronising the stream of that call) returns the stage durations in

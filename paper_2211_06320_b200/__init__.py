@@ -17,7 +17,8 @@ import numpy as np
 
 from ._lib import (DIAG_BYTES, FPE_C32, FPE_C64, FPE_R32, FPE_R64, FpeError, FpeInfo, check, lib)
 
-__all__ = ["precondition", "precondition_buffer", "Poly", "FpeError", "diag_fields", "header_fields"]
+__all__ = ["precondition", "precondition_derivative", "newton_step", "precondition_buffer", "Poly", "FpeError",
+           "diag_fields", "header_fields"]
 
 _TORCH_DT = None
 
@@ -201,6 +202,41 @@ def precondition(coeffs, p: int | None = None, drop: int | None = None, device: 
     check(lib().fpe_precondition(C.c_void_p(ptr), n, dt, p or 0, drop or 0, device,
                                  _stream_ptr(stream, device), C.byref(h)), "fpe_precondition")
     return Poly(h, device)
+
+
+def precondition_derivative(coeffs, p: int | None = None, drop: int | None = None, device: int | None = None,
+                            stream=None) -> Poly:
+    """P' preconditioned (fpe_precondition_derivative): coefficients (j+1) a_{j+1} of P's coefficients."""
+    torch = _torch()
+    dt = _dtype_code(coeffs)
+    if device is None:
+        device = coeffs.device.index if isinstance(coeffs, torch.Tensor) and coeffs.is_cuda else torch.cuda.current_device()
+    keep = coeffs.contiguous() if isinstance(coeffs, torch.Tensor) else np.ascontiguousarray(coeffs)
+    ptr = keep.data_ptr() if isinstance(keep, torch.Tensor) else keep.ctypes.data
+    n = keep.numel() if isinstance(keep, torch.Tensor) else len(keep)
+    h = C.c_void_p()
+    check(lib().fpe_precondition_derivative(C.c_void_p(ptr), n, dt, p or 0, drop or 0, device,
+                                            _stream_ptr(stream, device), C.byref(h)), "fpe_precondition_derivative")
+    return Poly(h, device)
+
+
+def newton_step(P: Poly, dP: Poly, points, incr: bool = False, stream=None):
+    """One Newton step N_P(z) = z - P(z)/P'(z) on a CUDA tensor of points (fpe_newton_step).
+    Returns the new points (and the increments P/P' when incr=True)."""
+    torch = _torch()
+    points = points.contiguous()
+    n = points.numel()
+    pdt = _dtype_code(points)
+    odt = _out_dtype(P.info["dtype"], pdt)
+    out = torch.empty(n, dtype=odt, device=points.device)
+    inc = torch.empty(n, dtype=odt, device=points.device) if incr else None
+    sz = C.c_size_t()
+    check(lib().fpe_newton_workspace_size(P._h, dP._h, n, C.byref(sz)), "fpe_newton_workspace_size")
+    ws = torch.empty(max(sz.value, 256), dtype=torch.uint8, device=points.device)
+    check(lib().fpe_newton_step(P._h, dP._h, C.c_void_p(points.data_ptr()), pdt, n, C.c_void_p(out.data_ptr()),
+                                C.c_void_p(inc.data_ptr() if inc is not None else 0), C.c_void_p(ws.data_ptr()),
+                                ws.numel(), _stream_ptr(stream, points.device)), "fpe_newton_step")
+    return (out, inc) if incr else out
 
 
 def precondition_buffer(coeffs: np.ndarray, p: int | None = None, drop: int | None = None) -> np.ndarray:

@@ -53,6 +53,9 @@ SIGNATURES = {
     "fpe_evaluate_host": (C.c_int, [_P, _P, C.c_int, _I64, _P, _P, _P]),
     "fpe_horner": (C.c_int, [_P, _P, C.c_int, _I64, _P, _P, _P, _SZ, _P]),
     "fpe_last_stats": (C.c_int, [_P, _P]),
+    "fpe_precondition_derivative": (C.c_int, [_P, _I64, C.c_int, _I32, _I32, C.c_int, _P, C.POINTER(_P)]),
+    "fpe_newton_workspace_size": (C.c_int, [_P, _P, _I64, C.POINTER(_SZ)]),
+    "fpe_newton_step": (C.c_int, [_P, _P, _P, C.c_int, _I64, _P, _P, _P, _SZ, _P]),
     "fpe_set_profiling": (C.c_int, [_P, C.c_int]),
     "fpe_last_stage_ms": (C.c_int, [_P, _P, C.c_int, C.POINTER(C.c_int)]),
     "fpe_stage_name": (C.c_char_p, [_P, C.c_int]),

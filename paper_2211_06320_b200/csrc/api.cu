@@ -414,6 +414,97 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   return FPE_OK;
 }
 
+fpe_status fpe_precondition_derivative(const void* coeffs, int64_t n_coeffs, fpe_dtype dt, int32_t p_bits,
+                                       int32_t drop_override, int device, void* stream, fpe_poly* out) {
+  if (!coeffs || !out || n_coeffs < 1 || !dtype_ok(dt)) {
+    set_error("fpe_precondition_derivative: invalid argument");
+    return FPE_ERR_INVALID_ARG;
+  }
+  if (n_coeffs < 2) { set_error("fpe_precondition_derivative: P is constant"); return FPE_ERR_ZERO_POLY; }
+  DeviceGuard g(device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t esz = dtype_size(dt);
+  std::vector<uint8_t> src((size_t)n_coeffs * esz);
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, coeffs) == cudaSuccess &&
+      (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged)) {
+    FPE_CUDA(cudaMemcpyAsync(src.data(), coeffs, src.size(), cudaMemcpyDeviceToHost, s));
+    FPE_CUDA(cudaStreamSynchronize(s));
+  } else {
+    cudaGetLastError();
+    std::memcpy(src.data(), coeffs, src.size());
+  }
+  const int64_t m = n_coeffs - 1;
+  std::vector<uint8_t> der((size_t)m * esz);
+  for (int64_t j = 0; j < m; ++j) {
+    const double f = (double)(j + 1);
+    switch (dt) {
+      case FPE_R64: reinterpret_cast<double*>(der.data())[j] = f * reinterpret_cast<const double*>(src.data())[j + 1]; break;
+      case FPE_C64:
+        for (int c = 0; c < 2; ++c)
+          reinterpret_cast<double*>(der.data())[2 * j + c] = f * reinterpret_cast<const double*>(src.data())[2 * (j + 1) + c];
+        break;
+      case FPE_R32: reinterpret_cast<float*>(der.data())[j] = (float)(f * reinterpret_cast<const float*>(src.data())[j + 1]); break;
+      default:
+        for (int c = 0; c < 2; ++c)
+          reinterpret_cast<float*>(der.data())[2 * j + c] = (float)(f * reinterpret_cast<const float*>(src.data())[2 * (j + 1) + c]);
+        break;
+    }
+  }
+  return fpe_precondition(der.data(), m, dt, p_bits, drop_override, device, stream, out);
+}
+
+fpe_status fpe_newton_workspace_size(fpe_poly P, fpe_poly dP, int64_t n_points, size_t* bytes) {
+  if (!P || !dP || !bytes || n_points < 0) { set_error("fpe_newton_workspace_size: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t osz = is_f32(P->hdr.dtype) ? 8 : 16;   // complex output is the largest
+  *bytes = 2 * (al((size_t)n_points * osz) + al((size_t)n_points * 8)) + ws_bytes_for(n_points);
+  return FPE_OK;
+}
+
+fpe_status fpe_newton_step(fpe_poly P, fpe_poly dP, const void* points, fpe_dtype pt_dt, int64_t n_points,
+                           void* points_out, void* incr_out, void* workspace, size_t ws_bytes, void* stream) {
+  fpe_status st = check_eval_args(P, points, pt_dt, n_points, points_out);
+  if (st != FPE_OK) return st;
+  if (!dP || dP->device != P->device || is_f32(dP->hdr.dtype) != is_f32(P->hdr.dtype)) {
+    set_error("fpe_newton_step: P and P' must be handles of the same device and precision");
+    return FPE_ERR_INVALID_ARG;
+  }
+  if (n_points == 0) return FPE_OK;
+  size_t need = 0;
+  fpe_newton_workspace_size(P, dP, n_points, &need);
+  if (!workspace || ws_bytes < need) { set_error("fpe_newton_step: workspace of %zu bytes < %zu", ws_bytes, need); return FPE_ERR_INVALID_ARG; }
+  DeviceGuard g(P->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  // both values in the output type of the complex-or-real evaluation of P
+  const bool cplx = (pt_dt == FPE_C64 || pt_dt == FPE_C32 || P->hdr.dtype == FPE_C64 || P->hdr.dtype == FPE_C32 ||
+                     dP->hdr.dtype == FPE_C64 || dP->hdr.dtype == FPE_C32);
+  const size_t osz = is_f32(pt_dt) ? (cplx ? 8 : 4) : (cplx ? 16 : 8);
+  char* p = static_cast<char*>(workspace);
+  void* v1 = p; p += al((size_t)n_points * osz);
+  int64_t* e1 = reinterpret_cast<int64_t*>(p); p += al((size_t)n_points * 8);
+  void* v2 = p; p += al((size_t)n_points * osz);
+  int64_t* e2 = reinterpret_cast<int64_t*>(p); p += al((size_t)n_points * 8);
+  const size_t ws = ws_bytes_for(n_points);
+  if (P->hdr.dtype != dP->hdr.dtype) {
+    set_error("fpe_newton_step: P and P' must have the same coefficient type");
+    return FPE_ERR_INVALID_ARG;
+  }
+  st = fpe_evaluate(P, points, pt_dt, n_points, v1, e1, nullptr, p, ws, stream);
+  if (st != FPE_OK) return st;
+  long long launches = P->last_launches;
+  st = fpe_evaluate(dP, points, pt_dt, n_points, v2, e2, nullptr, p, ws, stream);
+  if (st != FPE_OK) return st;
+  launches += dP->last_launches;
+  const int ok = is_f32(pt_dt) ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
+  launch_newton(pt_dt, ok, n_points, points, v1, reinterpret_cast<const long long*>(e1), v2,
+                reinterpret_cast<const long long*>(e2), points_out, incr_out, s);
+  P->last_launches = launches + 1;
+  FPE_CUDA(cudaGetLastError());
+  return FPE_OK;
+}
+
 fpe_status fpe_set_profiling(fpe_poly h, int enable) {
   if (!h) { set_error("fpe_set_profiling: invalid argument"); return FPE_ERR_INVALID_ARG; }
   DeviceGuard g(h->device);

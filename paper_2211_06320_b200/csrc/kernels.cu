@@ -284,6 +284,51 @@ __global__ void __launch_bounds__(256) k_confidence(long long n, PolyDev P, cons
 }
 
 // ------------------------------------------------------------------------------------------
+// Newton step (eq:newton): N_P(z) = z - Q1/Q2 with Q1 = m1 2^e1, Q2 = m2 2^e2 the
+// extended-range FPE values of P and P'; the quotient is (m1/m2) 2^(e1 - e2), so huge or tiny P(z), P'(z)
+// cancel their scales before any rounding to the working format (the valuation cancellation of P:1985).
+template <int PK, int OK>
+__global__ void __launch_bounds__(256) k_newton(long long n, const void* __restrict__ pts, const void* __restrict__ v1,
+                                                const long long* __restrict__ e1, const void* __restrict__ v2,
+                                                const long long* __restrict__ e2, void* __restrict__ out,
+                                                void* __restrict__ incr) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double x, y;
+    load_point<PK>(pts, i, x, y);
+    double ar, ai, br, bi;
+    if constexpr (OK == FPE_R64) { ar = static_cast<const double*>(v1)[i]; ai = 0; br = static_cast<const double*>(v2)[i]; bi = 0; }
+    else if constexpr (OK == FPE_C64) {
+      const double2 a = static_cast<const double2*>(v1)[i], b = static_cast<const double2*>(v2)[i];
+      ar = a.x; ai = a.y; br = b.x; bi = b.y;
+    } else if constexpr (OK == FPE_R32) { ar = static_cast<const float*>(v1)[i]; ai = 0; br = static_cast<const float*>(v2)[i]; bi = 0; }
+    else {
+      const float2 a = static_cast<const float2*>(v1)[i], b = static_cast<const float2*>(v2)[i];
+      ar = a.x; ai = a.y; br = b.x; bi = b.y;
+    }
+    // (a / b) 2^(e1 - e2), mantissas in [1/2, 1): the complex quotient is formed in fp64
+    const double den = __fma_rn(br, br, bi * bi);
+    double qr = __fma_rn(ar, br, ai * bi) / den, qi = __fma_rn(ai, br, -ar * bi) / den;
+    const long long de = e1[i] - e2[i];
+    const int sc = (int)max(-4000ll, min(4000ll, de));
+    qr = ldexp(qr, sc); qi = ldexp(qi, sc);
+    const double zr = x - qr, zi = y - qi;
+    if constexpr (OK == FPE_R64) {
+      static_cast<double*>(out)[i] = zr;
+      if (incr) static_cast<double*>(incr)[i] = qr;
+    } else if constexpr (OK == FPE_C64) {
+      static_cast<double2*>(out)[i] = make_double2(zr, zi);
+      if (incr) static_cast<double2*>(incr)[i] = make_double2(qr, qi);
+    } else if constexpr (OK == FPE_R32) {
+      static_cast<float*>(out)[i] = (float)zr;
+      if (incr) static_cast<float*>(incr)[i] = (float)qr;
+    } else {
+      static_cast<float2*>(out)[i] = make_float2((float)zr, (float)zi);
+      if (incr) static_cast<float2*>(incr)[i] = make_float2((float)qr, (float)qi);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // launchers
 static int grid_for(long long n, int block) {
   long long g = (n + block - 1) / block;
@@ -356,6 +401,27 @@ bool launch_eval_sparse(int pk, const void* pts, long long n, const PolyDev& P, 
                         long long* exps, cudaStream_t s) {
   FPE_DISPATCH_PC(launch_eval_sparse_t, pts, n, P, lr, vals, exps, s)
   return true;
+}
+
+template <int PK>
+static void launch_newton_t(int ok, long long n, const void* pts, const void* v1, const long long* e1, const void* v2,
+                            const long long* e2, void* out, void* incr, cudaStream_t s) {
+  switch (ok) {
+    case FPE_R64: k_newton<PK, FPE_R64><<<grid_for(n, 256), 256, 0, s>>>(n, pts, v1, e1, v2, e2, out, incr); break;
+    case FPE_C64: k_newton<PK, FPE_C64><<<grid_for(n, 256), 256, 0, s>>>(n, pts, v1, e1, v2, e2, out, incr); break;
+    case FPE_R32: k_newton<PK, FPE_R32><<<grid_for(n, 256), 256, 0, s>>>(n, pts, v1, e1, v2, e2, out, incr); break;
+    default: k_newton<PK, FPE_C32><<<grid_for(n, 256), 256, 0, s>>>(n, pts, v1, e1, v2, e2, out, incr); break;
+  }
+}
+
+void launch_newton(int pk, int ok, long long n, const void* pts, const void* v1, const long long* e1, const void* v2,
+                   const long long* e2, void* out, void* incr, cudaStream_t s) {
+  switch (pk) {
+    case FPE_R64: launch_newton_t<FPE_R64>(ok, n, pts, v1, e1, v2, e2, out, incr, s); break;
+    case FPE_C64: launch_newton_t<FPE_C64>(ok, n, pts, v1, e1, v2, e2, out, incr, s); break;
+    case FPE_R32: launch_newton_t<FPE_R32>(ok, n, pts, v1, e1, v2, e2, out, incr, s); break;
+    default: launch_newton_t<FPE_C32>(ok, n, pts, v1, e1, v2, e2, out, incr, s); break;
+  }
 }
 
 void launch_confidence(int ok, long long n, const PolyDev& P, const void* vals, const long long* exps,

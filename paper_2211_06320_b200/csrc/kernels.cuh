@@ -16,6 +16,9 @@ bool launch_eval_sparse(int pk, const void* pts, long long n, const PolyDev& P, 
 // fpe_diag::cancel from the outputs (after an evaluation); ok = fpe_dtype of the values
 void launch_confidence(int ok, long long n, const PolyDev& P, const void* vals, const long long* exps,
                        fpe_diag* diag, cudaStream_t s);
+// z - Q1/Q2 from extended-range values (fpe_newton_step)
+void launch_newton(int pk, int ok, long long n, const void* pts, const void* v1, const long long* e1, const void* v2,
+                   const long long* e2, void* out, void* incr, cudaStream_t s);
 bool launch_horner(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
                    cudaStream_t s);
 }  // namespace fpe

@@ -286,3 +286,40 @@ def test_confidence_cancel_bits(fpe):
         ok = np.isfinite(P.log2_maxterm(pts)) & (c_ref < 40)
         assert np.all(np.abs(c_gpu[ok] - c_ref[ok]) <= 2), (c_gpu[ok][:10], c_ref[ok][:10])
         assert np.any(c_ref[ok] > 10) or a.shape[0] != 41   # the (z-1)^40 case does exercise cancellation
+
+
+def test_newton_step_paper_example(fpe):
+    """P(z) = z^64 + 1, p = 24 (FP32): P(10) and P'(10) overflow FP32, yet the Newton
+    increment 10 - N_P(10) = 0.15625 (exact to 2e-65) comes out of the FP32 path."""
+    a = np.zeros(65, dtype=np.float32)
+    a[0] = 1.0
+    a[64] = 1.0
+    P = fpe.precondition(a)
+    dP = fpe.precondition_derivative(a)
+    z = torch.tensor([10.0], dtype=torch.float32, device="cuda")
+    zn, inc = fpe.newton_step(P, dP, z, incr=True)
+    assert inc.item() == 0.15625 and zn.item() == 10.0 - 0.15625
+
+
+def test_newton_step_vs_oracle(fpe):
+    """N_P(z) = z - P(z)/P'(z) (eq:newton) against binary128 full Horner of P and of P' (whose coefficients
+    (j+1) a_{j+1} are formed with the same single fp64 rounding as the library's)."""
+    a = workloads.coefficients(1, d=300)
+    pts = workloads.points(1, 3000, shard=6)
+    P = fpe.precondition(a)
+    dP = fpe.precondition_derivative(a)
+    zn, inc = fpe.newton_step(P, dP, torch.from_numpy(pts).cuda(), incr=True)
+    inc = inc.cpu().numpy()
+    da = (np.arange(1, len(a)) * a[1:].real) + 1j * (np.arange(1, len(a)) * a[1:].imag)
+    H1 = oracle.OraclePoly(a).horner(pts)
+    H2 = oracle.OraclePoly(da).horner(pts)
+    ref = (H1.hi + H1.lo) / (H2.hi + H2.lo) * np.exp2((H1.e - H2.e).astype(np.float64))
+    # condition: the library's values are within 2^-45 S of P and P'; compare where both are well away
+    # from cancellation (|P| >= 2^-20 S_P and |P'| >= 2^-20 S_P')
+    c1 = abs_sum_log2(a, pts) - (np.log2(np.abs(H1.hi)) + H1.e)
+    c2 = abs_sum_log2(da, pts) - (np.log2(np.abs(H2.hi)) + H2.e)
+    ok = (c1 < 20) & (c2 < 20) & np.isfinite(ref)
+    assert ok.mean() > 0.9
+    rel = np.abs(inc[ok] - ref[ok]) / np.abs(ref[ok])
+    assert np.all(rel < 2.0 ** -24), rel.max()
+    assert np.allclose(zn.cpu().numpy()[ok], pts[ok] - inc[ok], rtol=0, atol=0)
