@@ -274,3 +274,20 @@ def test_fpe_eval_worked_example_structure(worked):
         W = [k for k in range(c["l"][i], c["r"][i] + 1) if P.good[k]]
         ref = sum(mp.mpc(P.coeffs[k].real, P.coeffs[k].imag) * zz ** k for k in W)
         assert abs(_to_mpc(Q, i) - ref) <= mp.mpf(2) ** -100 * abs(ref)
+
+
+def test_half_circle_family_complexity():
+    """The half-circle family (eq:halfcirclepoly), a_n = 2^sqrt((n+1)(d+1-n)), nearly
+    saturates the complexity bound: on the Riemann sphere the mean band width / sqrt(d (p + s(d) + 3))
+    stays below Theorem thm:equivAlgo's 1.9046 and approaches C_3(0) = 1.32178 from below as d
+    grows (C_3(delta) increases to C_3(0) as delta -> 0)."""
+    ratios = []
+    for d in (250, 1000, 2000):
+        n = np.arange(d + 1)
+        a = np.exp2(np.sqrt((n + 1.0) * (d + 1.0 - n))).astype(np.complex128)
+        P = oracle.OraclePoly(a)
+        c = P.classify(workloads.sphere_points(1, 60000, shard=9))
+        ratios.append((c["r"] - c["l"] + 1).mean() / math.sqrt(P.d_eff * P.drop))
+    assert all(r < 1.9046 for r in ratios)
+    assert ratios[0] < ratios[1] < ratios[2] < 1.32178
+    assert ratios[2] > 1.25
