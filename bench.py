@@ -35,7 +35,7 @@ FP64_FMA_PEAK = 148 * 64 * 1.965e9      # SMs x fp64 FMA lanes/clk/SM x max SM c
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fpe", choices=["fpe", "reference"])
     ap.add_argument("--config", type=int, default=3)
@@ -71,7 +71,7 @@ class ClockSampler:
                     self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)

@@ -726,8 +726,7 @@ __device__ __forceinline__ void stream_full(Ring<CK>& R, int lo, int hi, const t
         W s[NP];
 #pragma unroll
         for (int j = 0; j < NP; ++j) s[j] = E[j] > kDrop ? (W)0 : (W)ldexp(1.0, -E[j]);
-        for (int k = kb; k >= ke; --k) {
-          const CT a = cb[k];
+        auto scaled_step = [&](const CT& a) {
 #pragma unroll
           for (int j = 0; j < NP; ++j) {
             CT as = a;
@@ -735,6 +734,15 @@ __device__ __forceinline__ void stream_full(Ring<CK>& R, int lo, int hi, const t
             else as *= s[j];
             horner_step<CK, CPLX>(br[j], bi[j], zr[j], zi[j], as);
           }
+        };
+        if (kb - ke == 7) {
+          CT a[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a[u] = cb[kb - u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) scaled_step(a[u]);
+        } else {
+          for (int k = kb; k >= ke; --k) scaled_step(cb[k]);
         }
       }
       rescale();
