@@ -246,7 +246,7 @@ def run_reference(args):
     import oracle
     import workloads
     cfg = args.config
-    sample = args.cpu_sample or 1024
+    sample = args.cpu_sample or 8192
     a = workloads.coefficients(cfg)
     P = oracle.OraclePoly(a)
     pts = workloads.points(cfg, sample, shard=977)
