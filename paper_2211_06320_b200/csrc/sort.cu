@@ -79,7 +79,12 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint2* __restrict_
       if (i < n) {
         const uint32_t c = kr[u].x >> (24 - kCoarseBits);
         const uint32_t pos = __ldg(bstart + c) + __ldg(cta_base + (size_t)(i / ppc) * kBuckets + c) + kr[u].y;
-        rec[pos] = PtRec{(int32_t)i, kr[u].x, w[u].x, w[u].y, z[u].x, z[u].y};
+        // one 256-bit store (STG.E.ENL2.256): the whole 32-byte sector in one request
+        const unsigned long long zx = __double_as_longlong(z[u].x), zy = __double_as_longlong(z[u].y);
+        asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(rec + pos), "r"((uint32_t)i),
+                     "r"(kr[u].x), "r"((uint32_t)w[u].x), "r"((uint32_t)w[u].y), "r"((uint32_t)zx),
+                     "r"((uint32_t)(zx >> 32)), "r"((uint32_t)zy), "r"((uint32_t)(zy >> 32))
+                     : "memory");
       }
     }
   }
