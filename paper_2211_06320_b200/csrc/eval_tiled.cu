@@ -38,20 +38,16 @@ constexpr int kStages = 3;     // TMA ring depth per warp
 // ------------------------------------------------------------------------------------------------
 // classification + sort key + first radix upsweep
 __device__ __forceinline__ uint32_t lambda_key(double lam, int l, int r) {
+  // |lambda| = (1.m) 2^E: mag = (E + 53) << 16 | top 16 bits of m (monotone in |lambda| >= 2^-52)
   uint32_t longw = (r - l + 1 > kLongWin) ? 1u : 0u;
   uint32_t u;
   if (!(lam == lam) || lam == -INFINITY) {
     u = 0;
   } else {
-    double a = fabs(lam);
+    const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(lam));
+    const int E = (int)(b >> 52) - 1023;
     uint32_t mag = 0;
-    if (a >= 0x1p-52) {
-      int e = frexp_exp(a);                       // a = f 2^e, f in [1/2, 1), e in [-51, 11]
-      uint32_t ec = (uint32_t)(e + 52);           // 6 bits
-      double f = ldexp(a, -e);
-      uint32_t m16 = (uint32_t)((f - 0.5) * 131072.0);   // 16 bits
-      mag = (ec << 16) | min(m16, 65535u);
-    }
+    if (E >= -52) mag = ((uint32_t)(E + 53) << 16) | (uint32_t)((b >> 36) & 0xffff);
     u = (lam >= 0.0) ? (1u << 22) + mag : (1u << 22) - 1u - mag;
   }
   return (longw << 23) | u;
