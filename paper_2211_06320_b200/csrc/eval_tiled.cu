@@ -441,11 +441,11 @@ struct Pts {
   bool valid[NP];
 };
 
-// Group g holds the sorted positions [g*32*NP, min(n, (g+1)*32*NP)) (k_plan); its records (index,
-// window) are read coalesced and without waiting for the descriptor, then the points themselves.
+// Group g holds the positions [g*32*NP, min(n, (g+1)*32*NP)) of the bucket order (k_plan); its records
+// (index, window, z) are read coalesced and without waiting for the descriptor.
 template <int PK, int NP>
 __device__ __forceinline__ void load_group(Pts<NP>& S, uint32_t g, long long n, const PtRec* __restrict__ rec,
-                                           const double2* __restrict__ zs, int kmin) {
+                                           int kmin) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
@@ -485,7 +485,7 @@ struct GroupCtx {   // raw loads of a group, consumed only when the group is eva
 
 template <int PK, int NP>
 __device__ __forceinline__ void group_load(GroupCtx<NP>& c, uint32_t g, long long n, const Plan& plan,
-                                           const PtRec* __restrict__ rec, const double2* __restrict__ zs, int kmin) {
+                                           const PtRec* __restrict__ rec, int kmin) {
   const int lane = threadIdx.x & 31;
   c.g = g;
   if (g < plan.ngroups) {
@@ -556,7 +556,7 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c,
 // the group's last piece folds all partials in order and finalises.
 template <int PK, int CK, int OK, int NP>
 __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long long n, const Plan& plan,
-                                            const PtRec* __restrict__ rec, const double2* __restrict__ zs,
+                                            const PtRec* __restrict__ rec,
                                             const PolyDev& P, void* vals,
                                             long long* exps) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
@@ -569,7 +569,7 @@ __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long
   const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
   ring_begin(R, rlo, rhi);
   Pts<NP> S;
-  load_group<PK, NP>(S, g, n, rec, zs, kmin);
+  load_group<PK, NP>(S, g, n, rec, kmin);
   W br[NP], bi[NP];
   eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, br, bi);
   const int p0 = d.lo / kPiece;
@@ -610,7 +610,7 @@ constexpr size_t ring_bytes() {
 // Persistent evaluator: every warp first takes parallel pieces of long windows, then whole groups,
 // both from global atomic counters (largest work first; the tail is at most one group).
 template <int PK, int CK, int OK, int NP>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(const double2* __restrict__ zs, long long n, PolyDev P,
+__global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(long long n, PolyDev P,
                                                                const PtRec* __restrict__ rec, Plan plan,
                                                                void* __restrict__ vals, long long* __restrict__ exps) {
   using CT = typename Step<CK>::CT;
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(const double2* __
     if (lane == 0) nxt = atomicAdd(plan.ctrs + 0, 1u);
     const uint2 item = plan.items[it];
     if (item.x == ~0u) continue;
-    multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, rec, zs, P, vals, exps);
+    multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, rec, P, vals, exps);
   }
   // groups: software-pipelined one group ahead (the next group's records load during this epilogue)
   const int kmin = (int)P.k_min;
@@ -643,12 +643,12 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(const double2* __
   // reverse bucket order: the long-window groups (the largest single items) first, the shortest last,
   // so that the tail of the persistent loop is short
   auto gid = [&](uint32_t it) { return it < plan.ngroups ? plan.ngroups - 1 - it : plan.ngroups; };
-  group_load<PK, NP>(cur, gid(__shfl_sync(0xffffffffu, nxt, 0)), n, plan, rec, zs, kmin);
+  group_load<PK, NP>(cur, gid(__shfl_sync(0xffffffffu, nxt, 0)), n, plan, rec, kmin);
   if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
   while (cur.g < plan.ngroups) {
     GroupCtx<NP> nx;
     auto fetch_next = [&]() {
-      group_load<PK, NP>(nx, gid(__shfl_sync(0xffffffffu, nxt, 0)), n, plan, rec, zs, kmin);
+      group_load<PK, NP>(nx, gid(__shfl_sync(0xffffffffu, nxt, 0)), n, plan, rec, kmin);
       if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
     };
     if (cur.d.npieces > 1) fetch_next();   // evaluated as parallel pieces (multi_piece)
@@ -829,7 +829,7 @@ static size_t eval_smem() {
 }
 
 template <int PK, int CK, int OK, int NP>
-static int launch_eval_tiled_t(const double2* zs, long long n, const PolyDev& P, const PtRec* rec, const Plan& plan, void* vals,
+static int launch_eval_tiled_t(long long n, const PolyDev& P, const PtRec* rec, const Plan& plan, void* vals,
                                long long* exps, cudaStream_t s) {
   static int grid = 0;
   const size_t smem = eval_smem<CK>();
@@ -841,7 +841,7 @@ static int launch_eval_tiled_t(const double2* zs, long long n, const PolyDev& P,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid = max(1, per_sm) * sms;
   }
-  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(nullptr, n, P, rec, plan, vals, exps);
+  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(n, P, rec, plan, vals, exps);
   return 1;
 }
 
@@ -940,7 +940,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   st.mark("bucket");
   int le = 0;
 #define FPE_EV(PKV, CKV) \
-  le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(nullptr, n, P, rec, plan, vals, exps, s)
+  le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(n, P, rec, plan, vals, exps, s)
   switch (pk * 4 + P.cdt) {
     case FPE_R64 * 4 + FPE_R64: FPE_EV(FPE_R64, FPE_R64); break;
     case FPE_R64 * 4 + FPE_C64: FPE_EV(FPE_R64, FPE_C64); break;

@@ -3,9 +3,9 @@
 //   k_classify     lines 5-8 of Algorithm FPE_p: lambda = log2|z| (correctly
 //                  rounded, fpe_math.cuh), k_lambda by binary search over the cover slopes staged in
 //                  shared memory, [l, r] by binary searches with exact predicates.
-//   k_eval_point   line 9: Q_lambda(z) = z^l * Horner over G_p cap [l, r]
-//                  (PAPER.md:1621-1622), one thread per point; the reference path of the tiled
-//                  evaluator and the path for sparse handles.
+//   k_eval_sparse  line 9 for sparse handles: the few kept terms a_k z^k of the compact
+//                  good-index list, each z^k by the polar route, summed in extended range.
+//   k_confidence   fpe_diag::cancel; k_newton: the Newton step of fpe_newton_step.
 //   k_horner_full  Horner's scheme over the whole coefficient range with
 //                  in-loop exponent rescaling -- the context baseline.
 #include <cuda_runtime.h>
@@ -44,75 +44,6 @@ __global__ void __launch_bounds__(256) k_classify(const void* __restrict__ pts, 
       diag[i] = d;
     }
     if (hard) atomicAdd(hard_ctr, 1ull);
-  }
-}
-
-// One thread per point: Q_lambda(z) = z^l sum_{k in G_p cap [l,r]} a_k z^(k-l).
-template <int PK, int CK, int OK>
-__global__ void __launch_bounds__(128) k_eval_point(const void* __restrict__ pts, long long n, PolyDev P,
-                                                    const int2* __restrict__ lr, void* __restrict__ vals,
-                                                    long long* __restrict__ exps) {
-  constexpr bool CPLX = PtTraits<OK>::cplx;
-  constexpr bool F32 = PtTraits<CK>::f32;
-  using W = typename std::conditional<F32, float, double>::type;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    double x, y;
-    load_point<PK>(pts, i, x, y);
-    int2 w = lr[i];
-    if (w.y < w.x) {   // non-finite point
-      double nan = __longlong_as_double(0x7ff8000000000000LL);
-      store_value<OK>(vals, exps, i, nan, CPLX ? nan : 0.0, 0);
-      continue;
-    }
-    if (x == 0.0 && y == 0.0) {   // z = 0: P(0) = a_0
-      double cr, ci;
-      a0_value<CK>(P, cr, ci);
-      store_value<OK>(vals, exps, i, cr, ci, cr == 0 && ci == 0 ? 0 : P.shift);
-      continue;
-    }
-    const W zr = (W)x, zi = (W)y;
-    W br = 0, bi = 0;
-    long long base;   // Q = b * z^base
-    if (!P.sparse) {
-      const long long off = P.k_min;
-      for (long long k = w.y; k >= w.x; --k) {
-        W cr, ci;
-        Coef<CK>::get(P.coef, k - off, cr, ci);
-        if constexpr (CPLX) {
-          W t = fma(br, zr, fma(-bi, zi, cr));
-          bi = fma(br, zi, fma(bi, zr, ci));
-          br = t;
-        } else {
-          br = fma(br, zr, cr);
-        }
-      }
-      base = w.x;
-    } else {
-      // Horner over the compact good list with gap powers z^(k_{j+1} - k_j)
-      int jlo = lower_bound_i32(P.sidx, (int)P.n_good, w.x);
-      int jhi = lower_bound_i32(P.sidx, (int)P.n_good, w.y + 1) - 1;
-      base = w.x;
-      if (jlo <= jhi) {
-        Coef<CK>::get(P.coef, jhi, br, bi);
-        for (int j = jhi - 1; j >= jlo; --j) {
-          long long gap = (long long)__ldg(P.sidx + j + 1) - __ldg(P.sidx + j);
-          double gr, gi;
-          long long gE;
-          times_zpow<CPLX>((double)br, (double)bi, x, y, gap, gr, gi, gE);
-          // b_{j+1} z^gap = b_j - c_j is bounded by K 2^D (cover argument)
-          int sc = (int)max(-3000ll, min(3000ll, gE));
-          W cr, ci;
-          Coef<CK>::get(P.coef, j, cr, ci);
-          br = (W)ldexp(gr, sc) + cr;
-          bi = (W)ldexp(gi, sc) + ci;
-        }
-        base = __ldg(P.sidx + jlo);
-      }
-    }
-    double qr, qi;
-    long long E;
-    times_zpow<CPLX>((double)br, (double)bi, x, y, base, qr, qi, E);
-    store_value<OK>(vals, exps, i, qr, qi, E + P.shift);
   }
 }
 
@@ -354,14 +285,6 @@ void launch_classify(int pk, const void* pts, long long n, const PolyDev& P, int
 }
 
 template <int PK, int CK>
-static void launch_eval_point_t(const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
-                                long long* exps, cudaStream_t s) {
-  constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
-  constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
-  k_eval_point<PK, CK, OK><<<grid_for(n, 128), 128, 0, s>>>(pts, n, P, lr, vals, exps);
-}
-
-template <int PK, int CK>
 static void launch_horner_t(const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
                             cudaStream_t s) {
   constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
@@ -381,12 +304,6 @@ static void launch_horner_t(const void* pts, long long n, const PolyDev& P, void
     case FPE_C32 * 4 + FPE_C32: FN<FPE_C32, FPE_C32>(__VA_ARGS__); break;               \
     default: return false;                                                              \
   }
-
-bool launch_eval_point(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
-                       long long* exps, cudaStream_t s) {
-  FPE_DISPATCH_PC(launch_eval_point_t, pts, n, P, lr, vals, exps, s)
-  return true;
-}
 
 template <int PK, int CK>
 static void launch_eval_sparse_t(const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,

@@ -9,8 +9,6 @@ constexpr int kSmemHullDbl = 1536;   // ... also as doubles (36 KiB) by the buck
 
 void launch_classify(int pk, const void* pts, long long n, const PolyDev& P, int2* lr, fpe_diag* diag,
                      unsigned long long* hard, cudaStream_t s);
-bool launch_eval_point(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
-                       long long* exps, cudaStream_t s);
 bool launch_eval_sparse(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
                         long long* exps, cudaStream_t s);
 // fpe_diag::cancel from the outputs (after an evaluation); ok = fpe_dtype of the values
