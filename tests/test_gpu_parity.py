@@ -337,3 +337,54 @@ def test_half_circle_family(fpe):
     out = gpu_eval(poly, pts)
     cls = check_indexing(P, pts, out["diag"])
     _values_ok(P, a, pts, out, np.arange(0, len(pts), 8), TOL64, cls)
+
+
+def _many_vertex_coeffs(m, cplx, seed):
+    """A concave cover with 2m + 1 vertices: edges (q, +1) for q = 1..m then (q, -1) for q = m..1
+    (strictly decreasing slopes), the other terms 8 bits below it; scales span m bits."""
+    ks, hs = [0], [-m]
+    for q in list(range(1, m + 1)) + list(range(m, 0, -1)):
+        ks.append(ks[-1] + q)
+        hs.append(hs[-1] + (1 if len(ks) <= m + 1 else -1))
+    kk = np.arange(ks[-1] + 1)
+    sc = np.floor(np.interp(kk, ks, hs)).astype(np.int64) - 8
+    sc[ks] = hs
+    a = np.ldexp(1.5, sc - 1)   # scale(a_k) = sc_k (1.5 keeps it through the phase rounding)
+    if cplx:
+        a = a * np.exp(1j * np.random.default_rng(seed).uniform(0, 2 * np.pi, len(a)))
+    return a
+
+
+@pytest.mark.parametrize("cplx", [True, False])
+def test_many_vertex_cover(fpe, cplx):
+    """A cover of 1601 vertices: more than the classifier stages in shared memory (1536), so the
+    bucketing classifier searches the cover in global memory (eval_tiled.cu k_classify_bucket)."""
+    a = _many_vertex_coeffs(800, cplx, 5)
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    assert len(P.hk) == 1601
+    rng = np.random.default_rng(6)
+    n = 4000
+    r = np.exp2(rng.uniform(-1.2, 1.2, n))
+    pts = r * np.exp(1j * rng.uniform(0, 2 * np.pi, n)) if cplx else r * rng.choice([-1.0, 1.0], n)
+    pts = np.concatenate([pts, [0.5, 2.0, 1.0, -1.0, 2.0 ** (-1 / 3)]]).astype(pts.dtype)
+    out = gpu_eval(poly, pts)
+    cls = check_indexing(P, pts, out["diag"])
+    _values_ok(P, a, pts, out, np.arange(0, len(pts), 16), TOL64, cls)
+
+
+def test_sparse_many_terms(fpe):
+    """Sparse handle with 20000 good terms (> the 8192 the sparse evaluator stages in shared
+    memory, kernels.cu k_eval_sparse), d = 2^20: global-index path, indexing exact, values 2^-45 S."""
+    rng = np.random.default_rng(12)
+    d = 1 << 20
+    a = np.zeros(d + 1, np.complex128)
+    idx = np.unique(np.concatenate([[0, d], rng.integers(1, d, 20000)]))
+    a[idx] = rng.uniform(-1, 1, len(idx)) + 1j * rng.uniform(-1, 1, len(idx))
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    assert int(P.good.sum()) > 8192 and int(P.good.sum()) * 32 < d + 1
+    pts = np.exp2(rng.uniform(-0.01, 0.01, 3000)) * np.exp(1j * rng.uniform(0, 2 * np.pi, 3000))
+    out = gpu_eval(poly, pts)
+    cls = check_indexing(P, pts, out["diag"])
+    _values_ok(P, a, pts, out, np.arange(0, len(pts), 10), TOL64, cls)
