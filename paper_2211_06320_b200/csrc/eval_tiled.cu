@@ -22,6 +22,7 @@
 //                    pieces were evaluated by one warp or in parallel (scratch + last-arriver fold).
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <algorithm>
 #include "fpe_internal.h"
 #include "fpe_math.cuh"
 #include "fpe_polar.cuh"
@@ -399,23 +400,35 @@ __device__ __noinline__ void acc_fold(Acc& A, double hr, double hi, int pbase, d
   A.base = pbase;
 }
 
-template <int OK, bool CPLX>
-__device__ __noinline__ void finalize(void* vals, long long* exps, long long idx, double x, double y, Acc A,
-                                      const PolyDev& P) {
+__device__ __forceinline__ void stage_value(PtOut* out, long long pos, double re, double im, long long E) {
+  const unsigned long long a = __double_as_longlong(re), b = __double_as_longlong(im), e = (unsigned long long)E;
+  asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(out + pos), "r"((uint32_t)a),
+               "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)), "r"((uint32_t)e),
+               "r"((uint32_t)(e >> 32)), "r"(0u), "r"(0u)
+               : "memory");
+}
+
+// Q = acc z^l as (re + i im) 2^E; the caller stages it (evaluator: over the point's record, in bucket
+// order -- every warp that reads the record has done so before the last piece is folded) or stores it
+// (full Horner).
+struct Fin {
+  double re, im;
+  long long E;
+};
+
+template <bool CPLX>
+__device__ __noinline__ Fin finalize(double x, double y, Acc A, const PolyDev& P) {
 #ifdef FPE_EXP_NO_FINALIZE
-  if (A.r == 1.2345) store_value<OK>(vals, exps, idx, A.r, A.i, 0);
-  return;
+  return Fin{A.r, A.i, 0};
 #endif
   if (!isfinite(x) || !isfinite(y)) {
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
-    store_value<OK>(vals, exps, idx, nan, CPLX ? nan : 0.0, 0);
-    return;
+    return Fin{nan, CPLX ? nan : 0.0, 0};
   }
   double qr = A.started ? A.r : 0.0, qi = A.started ? A.i : 0.0;
   if (x == 0.0 && y == 0.0) {   // z = 0: P(0) = a_0 (window {k_min})
     if (P.k_min != 0) { qr = 0.0; qi = 0.0; }
-    store_value<OK>(vals, exps, idx, qr, qi, (qr == 0.0 && qi == 0.0) ? 0 : P.shift);
-    return;
+    return Fin{qr, qi, (qr == 0.0 && qi == 0.0) ? 0 : (long long)P.shift};
   }
   long long E = 0;
   const long long n = A.started ? (long long)A.base + P.k_min : 0;
@@ -429,13 +442,13 @@ __device__ __noinline__ void finalize(void* vals, long long* exps, long long idx
     const double i = __fma_rn(qr, p.hi, qi * p.hr);
     qr = r; qi = i; E = p.E;
   }
-  store_value<OK>(vals, exps, idx, qr, qi, E + P.shift);
+  return Fin{qr, qi, E + P.shift};
 }
 
 // The NP points of each lane of a group: sorted position j*32 + lane.
 template <int NP>
 struct Pts {
-  long long idx[NP];
+  long long idx[NP];   // sorted position
   double x[NP], y[NP];
   int wl[NP], wr[NP];   // relative window; empty (wl > wr) for padding and non-finite points
   bool valid[NP];
@@ -453,9 +466,9 @@ __device__ __forceinline__ void load_group(Pts<NP>& S, uint32_t g, long long n, 
     S.valid[j] = pos < n;
     S.idx[j] = 0; S.x[j] = 0.0; S.y[j] = 0.0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
     if (S.valid[j]) {
-      const int4 h = __ldg(reinterpret_cast<const int4*>(rec + pos));
-      const double2 z = __ldg(reinterpret_cast<const double2*>(rec + pos) + 1);
-      S.idx[j] = h.x; S.x[j] = z.x; S.y[j] = z.y;
+      const int4 h = __ldcg(reinterpret_cast<const int4*>(rec + pos));
+      const double2 z = __ldcg(reinterpret_cast<const double2*>(rec + pos) + 1);
+      S.idx[j] = pos; S.x[j] = z.x; S.y[j] = z.y;
       if (h.w >= h.z) { S.wl[j] = h.z - kmin; S.wr[j] = h.w - kmin; }
     }
   }
@@ -485,7 +498,7 @@ struct GroupCtx {   // raw loads of a group, consumed only when the group is eva
 
 template <int PK, int NP>
 __device__ __forceinline__ void group_load(GroupCtx<NP>& c, uint32_t g, long long n, const Plan& plan,
-                                           const PtRec* __restrict__ rec, int kmin) {
+                                           const PtRec* rec, int kmin) {
   const int lane = threadIdx.x & 31;
   c.g = g;
   if (g < plan.ngroups) {
@@ -494,8 +507,8 @@ __device__ __forceinline__ void group_load(GroupCtx<NP>& c, uint32_t g, long lon
     for (int j = 0; j < NP; ++j) {
       const long long pos = (long long)g * (32 * NP) + j * 32 + lane;
       if (pos < n) {
-        c.h[j] = __ldg(reinterpret_cast<const int4*>(rec + pos));
-        c.z[j] = __ldg(reinterpret_cast<const double2*>(rec + pos) + 1);
+        c.h[j] = __ldcg(reinterpret_cast<const int4*>(rec + pos));
+        c.z[j] = __ldcg(reinterpret_cast<const double2*>(rec + pos) + 1);
       }
     }
   }
@@ -510,11 +523,7 @@ __device__ __forceinline__ void group_unpack(Pts<NP>& S, const GroupCtx<NP>& c, 
     S.valid[j] = pos < n;
     S.idx[j] = 0; S.x[j] = 0.0; S.y[j] = 0.0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
     if (S.valid[j]) {
-#ifdef FPE_EXP_SORTED_STORE
       S.idx[j] = pos;
-#else
-      S.idx[j] = c.h[j].x;
-#endif
       S.x[j] = c.z[j].x; S.y[j] = c.z[j].y;
       if (c.h[j].w >= c.h[j].z) { S.wl[j] = c.h[j].z - kmin; S.wr[j] = c.h[j].w - kmin; }
     }
@@ -523,7 +532,7 @@ __device__ __forceinline__ void group_unpack(Pts<NP>& S, const GroupCtx<NP>& c, 
 
 template <int PK, int CK, int OK, int NP, typename Prefetch>
 __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c, long long n, const PolyDev& P,
-                                             void* vals, long long* exps, Prefetch prefetch) {
+                                             PtOut* out, Prefetch prefetch) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
   const GroupDesc d = c.d;
@@ -549,16 +558,17 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c,
   prefetch();
 #pragma unroll
   for (int j = 0; j < NP; ++j)
-    if (S.valid[j]) finalize<OK, CPLX>(vals, exps, S.idx[j], S.x[j], S.y[j], A[j], P);
+    if (S.valid[j]) {
+      const Fin f = finalize<CPLX>(S.x[j], S.y[j], A[j], P);
+      stage_value(out, S.idx[j], f.re, f.im, f.E);
+    }
 }
 
 // One warp evaluates piece p of a multi-piece group into its scratch slot; the warp that completes
 // the group's last piece folds all partials in order and finalises.
 template <int PK, int CK, int OK, int NP>
 __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long long n, const Plan& plan,
-                                            const PtRec* __restrict__ rec,
-                                            const PolyDev& P, void* vals,
-                                            long long* exps) {
+                                            const PtRec* rec, const PolyDev& P, PtOut* out) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
   using W2 = typename std::conditional<std::is_same<W, float>::value, float2, double2>::type;
@@ -598,7 +608,8 @@ __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long
         }
       }
     }
-    finalize<OK, CPLX>(vals, exps, S.idx[j], S.x[j], S.y[j], A, P);
+    const Fin f = finalize<CPLX>(S.x[j], S.y[j], A, P);
+    stage_value(out, S.idx[j], f.re, f.im, f.E);
   }
 }
 
@@ -611,8 +622,7 @@ constexpr size_t ring_bytes() {
 // both from global atomic counters (largest work first; the tail is at most one group).
 template <int PK, int CK, int OK, int NP>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(long long n, PolyDev P,
-                                                               const PtRec* __restrict__ rec, Plan plan,
-                                                               void* __restrict__ vals, long long* __restrict__ exps) {
+                                                               PtRec* rec, Plan plan) {
   using CT = typename Step<CK>::CT;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -624,6 +634,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(long long n, Poly
   }
   __syncwarp();
   Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0};
+  PtOut* const out = reinterpret_cast<PtOut*>(rec);   // results overwrite the records (bucket order)
   const uint32_t n_multi = min(plan.ctrs[2], plan.cap);
   // the next item index is fetched one item ahead, so the atomic's latency hides behind the work
   uint32_t nxt = 0;
@@ -634,7 +645,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(long long n, Poly
     if (lane == 0) nxt = atomicAdd(plan.ctrs + 0, 1u);
     const uint2 item = plan.items[it];
     if (item.x == ~0u) continue;
-    multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, rec, P, vals, exps);
+    multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, rec, P, out);
   }
   // groups: software-pipelined one group ahead (the next group's records load during this epilogue)
   const int kmin = (int)P.k_min;
@@ -652,7 +663,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(long long n, Poly
       if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
     };
     if (cur.d.npieces > 1) fetch_next();   // evaluated as parallel pieces (multi_piece)
-    else single_group<PK, CK, OK, NP>(R, cur, n, P, vals, exps, fetch_next);
+    else single_group<PK, CK, OK, NP>(R, cur, n, P, out, fetch_next);
     cur = nx;
   }
 }
@@ -773,7 +784,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
     if ((long long)g >= ngroups) break;
     ring_begin(R, 0, hi);
     double x[NP], y[NP];
-    long long idx[NP];
+    long long idx[NP];   // sorted position
     W zr[NP], zi[NP], br[NP], bi[NP];
     int E[NP];
 #pragma unroll
@@ -789,7 +800,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
       if (idx[j] >= n) continue;
       Acc A{(double)br[j], (double)bi[j], 0, true};
       if (!isfinite(x[j]) || !isfinite(y[j]) || (x[j] == 0.0 && y[j] == 0.0)) {
-        finalize<OK, CPLX>(vals, exps, idx[j], x[j], y[j], A, P);   // NaN / a_0 (the E = 0 paths)
+        const Fin f = finalize<CPLX>(x[j], y[j], A, P);   // NaN / a_0 (the E = 0 paths)
+        store_value<OK>(vals, exps, idx[j], f.re, f.im, f.E);
         continue;
       }
       double qr = A.r, qi = A.i;
@@ -806,6 +818,39 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
 }
 
 // ------------------------------------------------------------------------------------------------
+// Results from bucket order to the caller's order: a coalesced pass over the caller's indices gathering one
+// 32-byte staged result each (a random sector read instead of the evaluator's random partial-sector
+// writes, which the DRAM turns into read-modify-writes).
+template <int OK>
+__global__ void __launch_bounds__(256) k_unsort(const PtOut* __restrict__ staged, const uint32_t* __restrict__ spos,
+                                                long long n, void* __restrict__ vals, long long* __restrict__ exps) {
+  constexpr int U = 4;   // independent gathers in flight per thread
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    double re[U], im[U];
+    long long E[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < n) {
+        uint32_t w[8];
+        asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                     : "l"(staged + __ldg(spos + i)));
+        re[u] = __hiloint2double((int)w[1], (int)w[0]);
+        im[u] = __hiloint2double((int)w[3], (int)w[2]);
+        E[u] = (long long)(((unsigned long long)w[5] << 32) | w[4]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < n) store_value<OK>(vals, exps, i, re[u], im[u], E[u]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // host side
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -817,7 +862,7 @@ static size_t scratch_slots(long long n) {
 }
 
 size_t tiled_ws_bytes(long long n) {
-  return al256(n * sizeof(int2)) + al256(n * sizeof(uint2)) + al256(n * sizeof(PtRec)) +
+  return al256(n * sizeof(int2)) + al256(n * sizeof(uint2)) + al256(n * sizeof(PtRec)) + al256(n * 4) +
          al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) +
          al256(max_groups(n) * sizeof(GroupDesc)) + al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
@@ -829,8 +874,7 @@ static size_t eval_smem() {
 }
 
 template <int PK, int CK, int OK, int NP>
-static int launch_eval_tiled_t(long long n, const PolyDev& P, const PtRec* rec, const Plan& plan, void* vals,
-                               long long* exps, cudaStream_t s) {
+static int launch_eval_tiled_t(long long n, const PolyDev& P, PtRec* rec, const Plan& plan, cudaStream_t s) {
   static int grid = 0;
   const size_t smem = eval_smem<CK>();
   if (grid == 0) {
@@ -841,7 +885,7 @@ static int launch_eval_tiled_t(long long n, const PolyDev& P, const PtRec* rec, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid = max(1, per_sm) * sms;
   }
-  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(n, P, rec, plan, vals, exps);
+  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(n, P, rec, plan);
   return 1;
 }
 
@@ -908,9 +952,10 @@ bool run_horner_tiled(int pk, const void* pts, long long n, const PolyDev& P, ui
 int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
               fpe_diag* diag, void* ws, unsigned long long* hard, Stage& st, cudaStream_t s) {
   char* p = static_cast<char*>(ws);
-  int2* lr = reinterpret_cast<int2*>(p); p += al256(n * sizeof(int2));          // later: sorted windows
+  int2* lr = reinterpret_cast<int2*>(p); p += al256(n * sizeof(int2));          // {l, r} of input point i
   uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += al256(n * 8);            // {key, rank in (CTA, bucket)}
-  PtRec* rec = reinterpret_cast<PtRec*>(p); p += al256(n * sizeof(PtRec));
+  PtRec* rec = reinterpret_cast<PtRec*>(p); p += al256(n * sizeof(PtRec));   // later: the results (PtOut)
+  uint32_t* spos = reinterpret_cast<uint32_t*>(p); p += al256(n * 4);          // bucket position of point i
   uint32_t* cta_base = reinterpret_cast<uint32_t*>(p); p += al256(n_ctas(n) * kBuckets * 4);
   uint32_t* gcount = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   uint32_t* bstart = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
@@ -935,12 +980,12 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     default: launch_classify_bucket_t<FPE_C32>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
   }
   st.mark("classify");
-  bucket_finish(reinterpret_cast<const uint2*>(keys), lr, n, pts_per_cta(n), gcount, cta_base, bstart, rec, pk, pts,
-                P.k_min, plan, s);
+  bucket_finish(reinterpret_cast<const uint2*>(keys), lr, n, pts_per_cta(n), gcount, cta_base, bstart, rec, spos, pk,
+                pts, P.k_min, plan, s);
   st.mark("bucket");
   int le = 0;
 #define FPE_EV(PKV, CKV) \
-  le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(n, P, rec, plan, vals, exps, s)
+  le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(n, P, rec, plan, s)
   switch (pk * 4 + P.cdt) {
     case FPE_R64 * 4 + FPE_R64: FPE_EV(FPE_R64, FPE_R64); break;
     case FPE_R64 * 4 + FPE_C64: FPE_EV(FPE_R64, FPE_C64); break;
@@ -954,7 +999,17 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   }
 #undef FPE_EV
   st.mark("eval_tiled");
-  return 4 + le;
+  const long long blocks = std::min<long long>((n + 4 * 256 - 1) / (4 * 256), 148ll * 16);
+  const PtOut* staged = reinterpret_cast<const PtOut*>(rec);
+  switch (pk * 4 + P.cdt) {   // the output kind follows NPFor<PK, CK>::OK
+    case FPE_R64 * 4 + FPE_R64: k_unsort<FPE_R64><<<(int)blocks, 256, 0, s>>>(staged, spos, n, vals, exps); break;
+    case FPE_R32 * 4 + FPE_R32: k_unsort<FPE_R32><<<(int)blocks, 256, 0, s>>>(staged, spos, n, vals, exps); break;
+    case FPE_R32 * 4 + FPE_C32: case FPE_C32 * 4 + FPE_R32: case FPE_C32 * 4 + FPE_C32:
+      k_unsort<FPE_C32><<<(int)blocks, 256, 0, s>>>(staged, spos, n, vals, exps); break;
+    default: k_unsort<FPE_C64><<<(int)blocks, 256, 0, s>>>(staged, spos, n, vals, exps); break;
+  }
+  st.mark("unsort");
+  return 5 + le;
 }
 
 }  // namespace fpe

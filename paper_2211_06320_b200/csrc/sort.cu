@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint2* __restrict_
                                                         int pk, const void* __restrict__ pts, long long n,
                                                         long long ppc, const uint32_t* __restrict__ bstart,
                                                         const uint32_t* __restrict__ cta_base,
-                                                        PtRec* __restrict__ rec) {
+                                                        PtRec* __restrict__ rec, uint32_t* __restrict__ spos) {
   constexpr int U = 4;   // independent loads in flight per thread
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint2* __restrict_
       if (i < n) {
         const uint32_t c = kr[u].x >> (24 - kCoarseBits);
         const uint32_t pos = __ldg(bstart + c) + __ldg(cta_base + (size_t)(i / ppc) * kBuckets + c) + kr[u].y;
+        spos[i] = pos;
         // one 256-bit store (STG.E.ENL2.256): the whole 32-byte sector in one request
         const unsigned long long zx = __double_as_longlong(z[u].x), zy = __double_as_longlong(z[u].y);
         asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(rec + pos), "r"((uint32_t)i),
@@ -132,11 +133,11 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const PtRec* __restri
 }
 
 void bucket_finish(const uint2* keys, const int2* lr, long long n, long long ppc, const uint32_t* gcount,
-                   const uint32_t* cta_base, uint32_t* bstart, PtRec* rec, int pk, const void* pts,
-                   long long k_min, const Plan& plan, cudaStream_t s) {
+                   const uint32_t* cta_base, uint32_t* bstart, PtRec* rec, uint32_t* spos, int pk,
+                   const void* pts, long long k_min, const Plan& plan, cudaStream_t s) {
   k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart);
   const long long blocks = std::min<long long>((n + 4 * 256 - 1) / (4 * 256), 148ll * 32);
-  k_bucket_scatter<<<(int)blocks, 256, 0, s>>>(keys, lr, pk, pts, n, ppc, bstart, cta_base, rec);
+  k_bucket_scatter<<<(int)blocks, 256, 0, s>>>(keys, lr, pk, pts, n, ppc, bstart, cta_base, rec, spos);
   const long long groups = (n + plan.gsize - 1) / plan.gsize;
   k_plan<<<(int)((groups + 7) / 8), 256, 0, s>>>(n, rec, k_min, plan);
 }

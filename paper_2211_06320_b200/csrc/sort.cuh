@@ -26,6 +26,13 @@ struct __align__(32) PtRec {
   int32_t l, r;
   double x, y;
 };
+// The evaluator overwrites a group's records with its results, in bucket order (coalesced; every read of
+// a record precedes its overwrite); k_unsort moves them to the caller's order.
+struct __align__(32) PtOut {
+  double re, im;
+  long long E;   // value = (re + i im) 2^E, before store_value's normalisation
+  long long pad;
+};
 
 // A group: 32*NP consecutive points of the sorted permutation, evaluated by one warp (NP points per
 // lane) over the union [lo, hi] of their windows (relative to k_min; hi < lo: no finite point).
@@ -50,9 +57,9 @@ struct Plan {
 };
 
 // bucket starts (k_bucket_scan), records and points in bucket order (k_bucket_scatter), and the work plan
-// (k_plan)
+// (k_plan); spos[i] = bucket position of input point i
 void bucket_finish(const uint2* keys, const int2* lr, long long n, long long ppc, const uint32_t* gcount,
-                   const uint32_t* cta_base, uint32_t* bstart, PtRec* rec, int pk, const void* pts,
-                   long long k_min, const Plan& plan, cudaStream_t s);
+                   const uint32_t* cta_base, uint32_t* bstart, PtRec* rec, uint32_t* spos, int pk,
+                   const void* pts, long long k_min, const Plan& plan, cudaStream_t s);
 inline long long max_groups(long long n) { return (n + 63) / 64; }   // groups of >= 64 points
 }  // namespace fpe
