@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -277,9 +278,11 @@ static fpe_status check_eval_args(fpe_poly h, const void* points, fpe_dtype pt_d
   return FPE_OK;
 }
 
-fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
-                        void* values_out, int64_t* exps_out, fpe_diag* diag_out,
-                        void* workspace, size_t ws_bytes, void* stream) {
+// reset_stats: clear the hard-lambda counter first (fpe_evaluate); fpe_evaluate_host clears it once and
+// lets its chunks, whose kernels run on several streams, accumulate into it.
+static fpe_status evaluate_impl(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
+                                void* values_out, int64_t* exps_out, fpe_diag* diag_out,
+                                void* workspace, size_t ws_bytes, void* stream, bool reset_stats) {
   fpe_status st = check_eval_args(h, points, pt_dt, n_points, values_out);
   if (st != FPE_OK) return st;
   if (n_points == 0) return FPE_OK;
@@ -291,7 +294,7 @@ fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PolyDev P = h->view();
   int2* lr = static_cast<int2*>(workspace);
-  FPE_CUDA(cudaMemsetAsync(h->dstats, 0, sizeof(unsigned long long), s));
+  if (reset_stats) FPE_CUDA(cudaMemsetAsync(h->dstats, 0, sizeof(unsigned long long), s));
   Stage stg(h, s);
   long long launches = 0;
   for (long long off = 0; off < n_points; off += kMaxBatch) {
@@ -322,6 +325,12 @@ fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t
   h->last_launches = launches;       // kernels of this library (memsets not counted)
   FPE_CUDA(cudaGetLastError());
   return FPE_OK;
+}
+
+fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
+                        void* values_out, int64_t* exps_out, fpe_diag* diag_out,
+                        void* workspace, size_t ws_bytes, void* stream) {
+  return evaluate_impl(h, points, pt_dt, n_points, values_out, exps_out, diag_out, workspace, ws_bytes, stream, true);
 }
 
 fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
@@ -359,21 +368,36 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   const bool cplx_out = (pt_dt == FPE_C64 || pt_dt == FPE_C32 || h->hdr.dtype == FPE_C64 || h->hdr.dtype == FPE_C32);
   const size_t in_sz = dtype_size(pt_dt);
   const size_t out_sz = is_f32(pt_dt) ? (cplx_out ? 8 : 4) : (cplx_out ? 16 : 8);
-  // large chunks: the evaluator groups points of similar |z|, which needs many points per batch
-  const long long chunk = std::min<long long>(n_points, 1ll << 24);
+  // Pipeline over kSlots staging slots: H2D of chunk c (one copy stream) -> classify/sort/evaluate on the
+  // slot's own kernel stream -> D2H (one copy stream).  Consecutive chunks' kernels overlap, so one
+  // chunk's evaluator tail (its last long-window groups) runs beside the next chunk's work; the chunks
+  // stay large enough for the evaluator's window sharing (points of similar |z| per group), and the
+  // first one is smaller so that the D2H stream -- the steady-state bound -- starts early.
+  static const int kSlots = [] {
+    const char* e = std::getenv("FPE_HOST_SLOTS");   // tuning experiments only
+    return e ? std::max(2, std::min(fpe_poly_s::kHostSlots, std::atoi(e))) : 6;
+  }();
+  static const int lg_chunk = [] {
+    const char* e = std::getenv("FPE_HOST_CHUNK_LOG2");   // tuning experiments only
+    return e ? std::max(16, std::min(26, std::atoi(e))) : 22;
+  }();
+  static const int lg_first = [] {
+    const char* e = std::getenv("FPE_HOST_FIRST_LOG2");   // tuning experiments only
+    return e ? std::max(16, std::min(26, std::atoi(e))) : 21;
+  }();
+  const long long chunk = std::min<long long>(n_points, 1ll << lg_chunk);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  constexpr int kSlots = 3;
   const size_t per = al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8) + ws_bytes_for(chunk);
   if (h->st_bytes < kSlots * per) {
     if (h->st_dev) { cudaFree(h->st_dev); h->st_dev = nullptr; h->st_bytes = 0; }
     if (cudaMalloc(&h->st_dev, kSlots * per) != cudaSuccess) { cudaGetLastError(); set_error("staging cudaMalloc failed"); return FPE_ERR_OOM; }
     h->st_bytes = kSlots * per;
   }
-  for (int b = 0; b < 3; ++b)
-    if (!h->st_streams[b]) {
+  for (auto& sp : h->st_streams)
+    if (!sp) {
       cudaStream_t ns;
       FPE_CUDA(cudaStreamCreateWithFlags(&ns, cudaStreamNonBlocking));
-      h->st_streams[b] = ns;
+      sp = ns;
     }
   for (auto& e : h->st_events)
     if (!e) {
@@ -381,15 +405,17 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
       FPE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       e = ev;
     }
-  // three-stage pipeline over staging slots: H2D of chunk c+1 || kernels of chunk c || D2H of chunk c-1
   cudaStream_t s_in = static_cast<cudaStream_t>(h->st_streams[0]);
-  cudaStream_t s_ev = static_cast<cudaStream_t>(h->st_streams[1]);
-  cudaStream_t s_out = static_cast<cudaStream_t>(h->st_streams[2]);
+  cudaStream_t s_out = static_cast<cudaStream_t>(h->st_streams[1]);
+  FPE_CUDA(cudaMemsetAsync(h->dstats, 0, sizeof(unsigned long long), s_in));   // before every chunk (events)
   auto ev = [&](int slot, int kind) { return static_cast<cudaEvent_t>(h->st_events[slot * 3 + kind]); };
   long long launches = 0;
-  for (long long off = 0, c = 0; off < n_points; off += chunk, ++c) {
-    const long long m = std::min(chunk, n_points - off);
+  long long next = std::min<long long>(chunk, 1ll << lg_first);
+  for (long long off = 0, c = 0, m = 0; off < n_points; off += m, ++c) {
+    m = std::min(next, n_points - off);
+    next = chunk;
     const int b = (int)(c % kSlots);
+    cudaStream_t s_ev = static_cast<cudaStream_t>(h->st_streams[2 + b]);
     char* base = static_cast<char*>(h->st_dev) + b * per;
     void* dp = base;
     void* dv = base + al(chunk * in_sz);
@@ -399,8 +425,8 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
     FPE_CUDA(cudaMemcpyAsync(dp, static_cast<const char*>(points_host) + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
     FPE_CUDA(cudaEventRecord(ev(b, 0), s_in));
     FPE_CUDA(cudaStreamWaitEvent(s_ev, ev(b, 0), 0));
-    fpe_status est = fpe_evaluate(h, dp, pt_dt, m, dv, exps_host ? reinterpret_cast<int64_t*>(de) : nullptr, nullptr,
-                                  wsp, ws_bytes_for(chunk), s_ev);
+    fpe_status est = evaluate_impl(h, dp, pt_dt, m, dv, exps_host ? reinterpret_cast<int64_t*>(de) : nullptr, nullptr,
+                                   wsp, ws_bytes_for(chunk), s_ev, false);
     if (est != FPE_OK) return est;
     launches += h->last_launches;
     FPE_CUDA(cudaEventRecord(ev(b, 1), s_ev));

@@ -59,8 +59,9 @@ struct fpe_poly_s {
   void* prof_stream = nullptr;
   // staging for fpe_evaluate_host (grown on demand, owned)
   void* st_dev = nullptr; size_t st_bytes = 0;
-  void* st_streams[3] = {nullptr, nullptr, nullptr};   // H2D copies, kernels, D2H copies
-  void* st_events[9] = {};                            // per staging slot: h2d done, eval done, d2h done
+  static constexpr int kHostSlots = 8;   // staging slots available to fpe_evaluate_host
+  void* st_streams[2 + kHostSlots] = {};   // H2D copies, D2H copies, one kernel stream per staging slot
+  void* st_events[3 * kHostSlots] = {};    // per staging slot: h2d done, eval done, d2h done
   fpe::PolyDev view() const;
 };
 
