@@ -277,7 +277,7 @@ __device__ __forceinline__ void ring_release(Ring<CK>& R) {
 // point j updates b_j = b_j z_j + a_k only for k in its own window [wl_j, wr_j] (b_j must be 0 on
 // entry).  Inside [F_lo, F_hi], common to all points whose window meets [lo, hi], the steps are
 // unmasked (8 coefficients loaded ahead, then NP independent Horner chains per coefficient); outside
-// it a masked step zeroes the coefficient above a window (b stays exactly 0) and freezes b below it.
+// it a masked step freezes b outside the window (above it b stays exactly 0, as the unmasked step would keep it).
 // Points whose window misses [lo, hi] compute garbage that the caller discards.
 template <int CK, int NP, bool CPLX>
 __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const int (&wl)[NP], const int (&wr)[NP],
@@ -302,7 +302,6 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
   int F_lo = __reduce_max_sync(0xffffffffu, mx);
   int F_hi = __reduce_min_sync(0xffffffffu, mn);
   if (!__any_sync(0xffffffffu, any) || F_lo > F_hi) { F_lo = lo; F_hi = lo - 1; }
-  const CT zero = CT{};
   for (int q = hi / kChunk; q >= lo / kChunk; --q) {
     const CT* cb = ring_wait(R) - q * kChunk;
     const int k1 = min(hi, q * kChunk + kChunk - 1), k0 = max(lo, q * kChunk);
@@ -315,8 +314,8 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
 #pragma unroll
       for (int j = 0; j < NP; ++j) {
         W nr = br[j], ni = bi[j];
-        horner_step<CK, CPLX>(nr, ni, zr[j], zi[j], k <= wr[j] ? a : zero);
-        if (k >= wl[j]) { br[j] = nr; bi[j] = ni; }
+        horner_step<CK, CPLX>(nr, ni, zr[j], zi[j], a);
+        if (k >= wl[j] && k <= wr[j]) { br[j] = nr; bi[j] = ni; }
       }
     }
     const int f0 = max(k0, F_lo);
@@ -352,8 +351,8 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
 #pragma unroll
       for (int j = 0; j < NP; ++j) {
         W nr = br[j], ni = bi[j];
-        horner_step<CK, CPLX>(nr, ni, zr[j], zi[j], k <= wr[j] ? a : zero);
-        if (k >= wl[j]) { br[j] = nr; bi[j] = ni; }
+        horner_step<CK, CPLX>(nr, ni, zr[j], zi[j], a);
+        if (k >= wl[j] && k <= wr[j]) { br[j] = nr; bi[j] = ni; }
       }
     }
     ring_release(R);
