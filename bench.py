@@ -198,6 +198,29 @@ def extra_context(device: int, steps: int = 3):
         del poly, pts
     except Exception as e:  # noqa: BLE001
         out["full_horner_cfg3"] = {"error": repr(e)[:200]}
+    # preconditioning (§8(f) row 3): host path (coefficients copied to the host, precondition.cpp, upload)
+    # vs the device preconditioner (precondition_gpu.cu), coefficients resident on the GPU; wall clock
+    for cfg in (3, 5, 4):
+        try:
+            a = torch.from_numpy(workloads.coefficients(cfg)).to(dev)
+
+            def wall(f, reps=3):
+                ts = []
+                for _ in range(reps):
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    f()
+                    torch.cuda.synchronize()
+                    ts.append(time.perf_counter() - t0)
+                return 1e3 * sorted(ts)[len(ts) // 2]
+            fpe.precondition_gpu(a).close()
+            ms_host = wall(lambda: fpe.precondition(a).close())
+            ms_gpu = wall(lambda: fpe.precondition_gpu(a).close())
+            out[f"precondition_cfg{cfg}"] = {"coefficients": a.numel(), "host_ms": ms_host, "gpu_ms": ms_gpu,
+                                             "speedup": ms_host / ms_gpu}
+            del a
+        except Exception as e:  # noqa: BLE001
+            out[f"precondition_cfg{cfg}"] = {"error": repr(e)[:200]}
     specs = [(1, None, False), (2, None, False), (4, None, False), (5, None, False), (5, None, True)]
     for cfg, n, fp32 in specs:
         name = f"cfg{cfg}" + ("_fp32" if fp32 else "")

@@ -98,6 +98,22 @@ fpe_status fpe_precondition(const void* coeffs, int64_t n_coeffs, fpe_dtype dt,
                             void* stream, fpe_poly* out);
 
 /*
+ * fpe_precondition_gpu -- the same preconditioning computed on the device (
+ * PAPER.md:1239-1243 with the scales PAPER.md:509-532, the cover PAPER.md:1413-1509 and G_p
+ * PAPER.md:1512-1521): per-coefficient scales, per-chunk monotone chains merged level by level into the
+ * canonical cover, G_p flags by exact integer tests, a scan for the prefix counts / compact list.
+ * The flat buffer is byte-identical to fpe_precondition's.
+ *   coeffs        device pointer on `device` to a_0..a_d (n_coeffs = d+1 entries of dtype dt); read
+ *                 during the call only.
+ *   other arguments as fpe_precondition; the call synchronises `stream`.  Temporary device memory:
+ *   ~13 bytes per coefficient.
+ * Errors: as fpe_precondition; INVALID_ARG also when coeffs is not device memory of `device`.
+ */
+fpe_status fpe_precondition_gpu(const void* coeffs, int64_t n_coeffs, fpe_dtype dt,
+                                int32_t p_bits, int32_t drop_override, int device,
+                                void* stream, fpe_poly* out);
+
+/*
  * fpe_precondition_host -- the same preconditioning, entirely on the host (no CUDA call):
  * writes the flat buffer that fpe_poly_device_buffer would hold into the host array buf.
  * With buf == NULL or cap too small, only *bytes (the required size) is set and

@@ -204,6 +204,21 @@ def precondition(coeffs, p: int | None = None, drop: int | None = None, device: 
     return Poly(h, device)
 
 
+def precondition_gpu(coeffs, p: int | None = None, drop: int | None = None, stream=None) -> Poly:
+    """Algorithm FPE_p lines 2-4 computed on the device (fpe_precondition_gpu) from a CUDA tensor;
+    the handle's buffer is byte-identical to precondition()'s."""
+    torch = _torch()
+    if not (isinstance(coeffs, torch.Tensor) and coeffs.is_cuda):
+        raise ValueError("precondition_gpu needs a CUDA tensor")
+    dt = _dtype_code(coeffs)
+    keep = coeffs.contiguous()
+    device = keep.device.index
+    h = C.c_void_p()
+    check(lib().fpe_precondition_gpu(C.c_void_p(keep.data_ptr()), keep.numel(), dt, p or 0, drop or 0, device,
+                                     _stream_ptr(stream, device), C.byref(h)), "fpe_precondition_gpu")
+    return Poly(h, device)
+
+
 def precondition_derivative(coeffs, p: int | None = None, drop: int | None = None, device: int | None = None,
                             stream=None) -> Poly:
     """P' preconditioned (fpe_precondition_derivative): coefficients (j+1) a_{j+1} of P's coefficients."""

@@ -175,6 +175,37 @@ fpe_status fpe_precondition(const void* coeffs, int64_t n_coeffs, fpe_dtype dt, 
   return FPE_OK;
 }
 
+fpe_status fpe_precondition_gpu(const void* coeffs, int64_t n_coeffs, fpe_dtype dt, int32_t p_bits,
+                                int32_t drop_override, int device, void* stream, fpe_poly* out) {
+  if (!coeffs || !out || n_coeffs < 1 || !dtype_ok(dt) || p_bits < 0 || drop_override < 0) {
+    set_error("fpe_precondition_gpu: invalid argument");
+    return FPE_ERR_INVALID_ARG;
+  }
+  if (n_coeffs > (1ll << 31) - 2) { set_error("fpe_precondition_gpu: n_coeffs > 2^31-2"); return FPE_ERR_UNSUPPORTED; }
+  *out = nullptr;
+  int ndev = 0;
+  FPE_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) { set_error("fpe_precondition_gpu: bad device %d", device); return FPE_ERR_INVALID_ARG; }
+  DeviceGuard g(device);
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, coeffs) != cudaSuccess ||
+      !(attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) || attr.device != device) {
+    cudaGetLastError();
+    set_error("fpe_precondition_gpu: coeffs must be device memory of device %d", device);
+    return FPE_ERR_INVALID_ARG;
+  }
+  fpe_poly h = new (std::nothrow) fpe_poly_s();
+  if (!h) { set_error("out of host memory"); return FPE_ERR_OOM; }
+  h->device = device;
+  fpe_status st = precondition_device(coeffs, n_coeffs, dt, p_bits, drop_override, static_cast<cudaStream_t>(stream),
+                                      &h->dbuf, h->hdr, h->hk, h->hh);
+  if (st != FPE_OK) { delete h; return st; }
+  st = finish_handle(h);
+  if (st != FPE_OK) { fpe_destroy(h); return st; }
+  *out = h;
+  return FPE_OK;
+}
+
 fpe_status fpe_precondition_host(const void* coeffs, int64_t n_coeffs, fpe_dtype dt, int32_t p_bits,
                                  int32_t drop_override, void* buf, size_t cap, size_t* bytes) {
   if (!coeffs || !bytes || n_coeffs < 1 || !dtype_ok(dt) || p_bits < 0 || drop_override < 0) {

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <vector>
 #include <vector_types.h>
+#include <cuda_runtime.h>
 #include "../../include/fpe.h"
 
 namespace fpe {
@@ -78,4 +79,9 @@ struct Stage {
 fpe_status precondition_host(const void* coeffs_host, int64_t n, fpe_dtype dt, int32_t p_bits,
                              int32_t drop_override, std::vector<uint8_t>& flat, Header& hdr,
                              std::vector<int32_t>& hk, std::vector<int32_t>& hh);
+// The same on the device (precondition_gpu.cu): coeffs is a device pointer; *dbuf receives the flat
+// buffer (cudaMalloc'd, byte-identical to precondition_host's), hdr / hk / hh its host-side metadata.
+fpe_status precondition_device(const void* coeffs, int64_t n, fpe_dtype dt, int32_t p_bits, int32_t drop_override,
+                               cudaStream_t s, void** dbuf, Header& hdr, std::vector<int32_t>& hk,
+                               std::vector<int32_t>& hh);
 }  // namespace fpe

@@ -388,3 +388,71 @@ def test_sparse_many_terms(fpe):
     out = gpu_eval(poly, pts)
     cls = check_indexing(P, pts, out["diag"])
     _values_ok(P, a, pts, out, np.arange(0, len(pts), 10), TOL64, cls)
+
+
+# ------------------------------------------------- device preconditioner ----
+def _gpu_buffer(fpe, a):
+    t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    poly = fpe.precondition_gpu(t)
+    out = np.zeros(poly.nbytes, np.uint8)
+    poly.export(out.ctypes.data, len(out))
+    torch.cuda.synchronize()
+    return poly, out
+
+
+def _precondition_cases(rng):
+    d = 1 << 20
+    sp = np.zeros(d + 1, np.complex128)
+    idx = np.unique(np.concatenate([[0, d], rng.integers(1, d, 20000)]))
+    sp[idx] = rng.uniform(-1, 1, len(idx)) + 1j * rng.uniform(-1, 1, len(idx))
+    cases = [workloads.coefficients(1), workloads.coefficients(2), workloads.coefficients(3),
+             workloads.coefficients(5), workloads.to_fp32(workloads.coefficients(5)),
+             workloads.to_fp32(workloads.coefficients(2)), _many_vertex_coeffs(800, True, 5),
+             _many_vertex_coeffs(800, False, 5), sp,
+             np.array([0.0, 0.0, 3.0]), np.array([1.0, 1.0]), np.array([0, 0, 1 + 1j, 0, 0, 0, 2j, 0]),
+             np.full(100, 0.5 + 0.5j), np.array([5e-324, 1.0, 1e300]), np.array([2.0 ** -1074 + 0j]),
+             np.ldexp(1.0, np.floor(300 * np.sin(np.pi * np.arange(4001) / 4000)).astype(int))]
+    for _ in range(30):
+        n = int(rng.integers(1, 5000))
+        a = rng.normal(size=n) * np.exp2(rng.integers(-60, 60, size=n))
+        a[rng.random(n) < 0.4] = 0
+        if not a.any():
+            a[-1] = 1
+        cases.append(a)
+        cases.append(a * np.exp(1j * rng.uniform(0, 6.3, n)))
+        cases.append(workloads.to_fp32(a * np.exp(1j * rng.uniform(0, 6.3, n))))
+    return cases
+
+
+def test_precondition_gpu_matches_host(fpe):
+    """fpe_precondition_gpu (scales, chunked + merged monotone chains, G_p, scan) builds a flat buffer
+    byte-identical to the host preconditioner's, which the oracle pins (test_abi_host.py)."""
+    rng = np.random.default_rng(31)
+    for ci, a in enumerate(_precondition_cases(rng)):
+        try:
+            host = fpe.precondition_buffer(a)
+        except fpe.FpeError as e:
+            with pytest.raises(fpe.FpeError) as e2:
+                _gpu_buffer(fpe, a)
+            assert e2.value.status == e.status
+            continue
+        try:
+            poly, dev = _gpu_buffer(fpe, a)
+        except fpe.FpeError as e:
+            raise AssertionError(f"case {ci}: {a.dtype} n={len(a)} {a[:4]}: {e}")
+        assert len(host) == len(dev) and np.array_equal(host, dev), (a.dtype, len(a))
+        hk, hh = poly.hull()
+        P = oracle.OraclePoly(a)
+        assert np.array_equal(hk, P.hk) and np.array_equal(hh, P.hh)
+
+
+def test_precondition_gpu_errors(fpe):
+    for a, status in ((np.zeros(100), 2), (np.array([1.0, np.nan, 2.0]), 3),
+                      (np.array([1.0, np.inf + 0j]), 3), (np.array([1e-300, 1e300]), 4)):
+        t = torch.from_numpy(a).cuda()
+        with pytest.raises(fpe.FpeError) as e:
+            fpe.precondition_gpu(t)
+        assert e.value.status == status
+        with pytest.raises(fpe.FpeError) as e2:
+            fpe.precondition(a)
+        assert e2.value.status == status
