@@ -421,9 +421,10 @@ def run_fpe(args):
                      "frac": achieved / peak,
                      "traffic": (profiled_traffic() or {}).get("bytes"),
                      "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of k_eval_tiled "
-                                     "(profiles/r01_ncu_eval_tiled_cfg3.json); algorithmic bytes 40 B/pt = "
-                                     f"{40 * n / 1e9:.2f} GB: the excess is the read-modify-write of the random "
-                                     "16-B/8-B output stores",
+                                     "(profiles/r01_ncu_eval_tiled_cfg3.json): it reads the 32-B bucket-order records "
+                                     f"and writes its 32-B results over them ({64 * n / 1e9:.2f} GB); the path's "
+                                     f"algorithmic bytes are 40 B/pt = {40 * n / 1e9:.2f} GB (points in, values and "
+                                     "exponents out, the latter written by k_unsort)",
                      "peak_note": "fp64 FMA: 148 SM x 64 lanes x 1.965 GHz x 2 (guide unit counts/clock)",
                      "algorithmic_fma_per_launch": fma_total, "kernel_ms": dom_ms, "stages_ms": stages},
         "cpu_baseline": cpu,
