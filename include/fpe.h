@@ -114,6 +114,25 @@ fpe_status fpe_precondition_gpu(const void* coeffs, int64_t n_coeffs, fpe_dtype 
                                 void* stream, fpe_poly* out);
 
 /*
+ * Partial preprocessing (remark rem:partialpreproc): lines 2-3 of FPE_p (the
+ * scales and the concave cover) do not depend on p, so they can be computed once and G_p (line 4)
+ * finished in O(d) for each precision p later.
+ * fpe_cover_build   -- scales and canonical cover on the device from device coefficients (copied:
+ *                      the caller's array is read during the call only); synchronises `stream`.
+ *                      Errors: INVALID_ARG (bad arguments or coeffs not device memory of `device`),
+ *                      ZERO_POLY, NONFINITE_COEFF, OOM, CUDA.
+ * fpe_cover_finish  -- a handle for precision p_bits (0: 53 / 24 by dtype) and D = drop_override
+ *                      (0: p + s(d_eff) + 3), byte-identical to fpe_precondition's; the cover object
+ *                      stays valid.  Errors: INVALID_ARG, UNSUPPORTED, OOM, CUDA.
+ * fpe_cover_destroy -- frees the cover (NULL is a no-op).
+ */
+typedef struct fpe_cover_s* fpe_cover;
+fpe_status fpe_cover_build(const void* coeffs, int64_t n_coeffs, fpe_dtype dt, int device, void* stream,
+                           fpe_cover* out);
+fpe_status fpe_cover_finish(fpe_cover c, int32_t p_bits, int32_t drop_override, void* stream, fpe_poly* out);
+void fpe_cover_destroy(fpe_cover c);
+
+/*
  * fpe_precondition_host -- the same preconditioning, entirely on the host (no CUDA call):
  * writes the flat buffer that fpe_poly_device_buffer would hold into the host array buf.
  * With buf == NULL or cap too small, only *bytes (the required size) is set and

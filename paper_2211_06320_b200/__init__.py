@@ -219,6 +219,38 @@ def precondition_gpu(coeffs, p: int | None = None, drop: int | None = None, stre
     return Poly(h, device)
 
 
+class Cover:
+    """Partial preprocessing (PAPER.md:1529-1537): scales and concave cover of P on the device, once;
+    finish(p) completes G_p and the flat buffer for a precision p in O(d)."""
+
+    def __init__(self, coeffs, stream=None):
+        torch = _torch()
+        if not (isinstance(coeffs, torch.Tensor) and coeffs.is_cuda):
+            raise ValueError("Cover needs a CUDA tensor")
+        keep = coeffs.contiguous()
+        self.device = keep.device.index
+        self._h = C.c_void_p()
+        check(lib().fpe_cover_build(C.c_void_p(keep.data_ptr()), keep.numel(), _dtype_code(keep), self.device,
+                                    _stream_ptr(stream, self.device), C.byref(self._h)), "fpe_cover_build")
+
+    def finish(self, p: int | None = None, drop: int | None = None, stream=None) -> "Poly":
+        h = C.c_void_p()
+        check(lib().fpe_cover_finish(self._h, p or 0, drop or 0, _stream_ptr(stream, self.device), C.byref(h)),
+              "fpe_cover_finish")
+        return Poly(h, self.device)
+
+    def close(self):
+        if self._h:
+            lib().fpe_cover_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 def precondition_derivative(coeffs, p: int | None = None, drop: int | None = None, device: int | None = None,
                             stream=None) -> Poly:
     """P' preconditioned (fpe_precondition_derivative): coefficients (j+1) a_{j+1} of P's coefficients."""

@@ -206,6 +206,59 @@ fpe_status fpe_precondition_gpu(const void* coeffs, int64_t n_coeffs, fpe_dtype 
   return FPE_OK;
 }
 
+fpe_status fpe_cover_build(const void* coeffs, int64_t n_coeffs, fpe_dtype dt, int device, void* stream,
+                           fpe_cover* out) {
+  if (!coeffs || !out || n_coeffs < 1 || !dtype_ok(dt)) { set_error("fpe_cover_build: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  if (n_coeffs > (1ll << 31) - 2) { set_error("fpe_cover_build: n_coeffs > 2^31-2"); return FPE_ERR_UNSUPPORTED; }
+  *out = nullptr;
+  int ndev = 0;
+  FPE_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) { set_error("fpe_cover_build: bad device %d", device); return FPE_ERR_INVALID_ARG; }
+  DeviceGuard g(device);
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, coeffs) != cudaSuccess ||
+      !(attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) || attr.device != device) {
+    cudaGetLastError();
+    set_error("fpe_cover_build: coeffs must be device memory of device %d", device);
+    return FPE_ERR_INVALID_ARG;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  fpe_cover c = new (std::nothrow) fpe_cover_s();
+  if (!c) { set_error("out of host memory"); return FPE_ERR_OOM; }
+  c->cv.device = device;
+  const size_t nbytes = (size_t)n_coeffs * dtype_size(dt);
+  if (cudaMalloc(&c->cv.owned, nbytes) != cudaSuccess) { cudaGetLastError(); delete c; set_error("cudaMalloc(%zu) failed", nbytes); return FPE_ERR_OOM; }
+  cudaError_t e = cudaMemcpyAsync(c->cv.owned, coeffs, nbytes, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) { set_error("copy failed: %s", cudaGetErrorString(e)); c->cv.release(); delete c; return FPE_ERR_CUDA; }
+  fpe_status st = cover_build(c->cv.owned, n_coeffs, dt, s, c->cv);
+  if (st != FPE_OK) { c->cv.release(); delete c; return st; }
+  *out = c;
+  return FPE_OK;
+}
+
+fpe_status fpe_cover_finish(fpe_cover c, int32_t p_bits, int32_t drop_override, void* stream, fpe_poly* out) {
+  if (!c || !out || p_bits < 0 || drop_override < 0) { set_error("fpe_cover_finish: invalid argument"); return FPE_ERR_INVALID_ARG; }
+  *out = nullptr;
+  DeviceGuard g(c->cv.device);
+  fpe_poly h = new (std::nothrow) fpe_poly_s();
+  if (!h) { set_error("out of host memory"); return FPE_ERR_OOM; }
+  h->device = c->cv.device;
+  fpe_status st = cover_finish(c->cv, p_bits, drop_override, static_cast<cudaStream_t>(stream), &h->dbuf, h->hdr,
+                               h->hk, h->hh);
+  if (st != FPE_OK) { delete h; return st; }
+  st = finish_handle(h);
+  if (st != FPE_OK) { fpe_destroy(h); return st; }
+  *out = h;
+  return FPE_OK;
+}
+
+void fpe_cover_destroy(fpe_cover c) {
+  if (!c) return;
+  DeviceGuard g(c->cv.device);
+  c->cv.release();
+  delete c;
+}
+
 fpe_status fpe_precondition_host(const void* coeffs, int64_t n_coeffs, fpe_dtype dt, int32_t p_bits,
                                  int32_t drop_override, void* buf, size_t cap, size_t* bytes) {
   if (!coeffs || !bytes || n_coeffs < 1 || !dtype_ok(dt) || p_bits < 0 || drop_override < 0) {

@@ -79,9 +79,29 @@ struct Stage {
 fpe_status precondition_host(const void* coeffs_host, int64_t n, fpe_dtype dt, int32_t p_bits,
                              int32_t drop_override, std::vector<uint8_t>& flat, Header& hdr,
                              std::vector<int32_t>& hk, std::vector<int32_t>& hh);
+// Stage 1 of the device preconditioner (independent of p): scales and the canonical cover, kept on the
+// device (precondition_gpu.cu); stage 2 finishes G_p and the flat buffer for a given p.
+struct CoverDev {
+  const void* coeffs = nullptr;   // device coefficients (borrowed or == owned)
+  void* owned = nullptr;          // device copy owned by an fpe_cover
+  void* scales = nullptr;         // int32[n]
+  void* hull = nullptr;           // int2[nv]
+  int64_t n = 0, k_min = 0, k_max = 0, nv = 0;
+  fpe_dtype dt = FPE_R64;
+  int device = 0;
+  std::vector<int32_t> hk, hh;
+  void release();
+};
+fpe_status cover_build(const void* coeffs, int64_t n, fpe_dtype dt, cudaStream_t s, CoverDev& cv);
+fpe_status cover_finish(const CoverDev& cv, int32_t p_bits, int32_t drop_override, cudaStream_t s, void** dbuf,
+                        Header& hdr, std::vector<int32_t>& hk, std::vector<int32_t>& hh);
 // The same on the device (precondition_gpu.cu): coeffs is a device pointer; *dbuf receives the flat
 // buffer (cudaMalloc'd, byte-identical to precondition_host's), hdr / hk / hh its host-side metadata.
 fpe_status precondition_device(const void* coeffs, int64_t n, fpe_dtype dt, int32_t p_bits, int32_t drop_override,
                                cudaStream_t s, void** dbuf, Header& hdr, std::vector<int32_t>& hk,
                                std::vector<int32_t>& hh);
 }  // namespace fpe
+
+struct fpe_cover_s {
+  fpe::CoverDev cv;
+};

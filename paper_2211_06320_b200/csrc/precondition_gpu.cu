@@ -296,27 +296,20 @@ struct DevBuf {
     if (e_ != cudaSuccess) { set_error("%s: %s", #x, cudaGetErrorString(e_)); return FPE_ERR_CUDA; } \
   } while (0)
 
-fpe_status precondition_device(const void* coeffs, int64_t n, fpe_dtype dt, int32_t p_bits, int32_t drop_override,
-                               cudaStream_t s, void** dbuf, Header& hdr, std::vector<int32_t>& hk,
-                               std::vector<int32_t>& hh) {
-  const bool cplx = (dt == FPE_C64 || dt == FPE_C32);
-  const bool f32 = (dt == FPE_R32 || dt == FPE_C32);
-  (void)cplx;
+// Stage 1 (independent of p, PAPER.md:1529-1537 remark rem:partialpreproc): scales and the canonical cover.
+fpe_status cover_build(const void* coeffs, int64_t n, fpe_dtype dt, cudaStream_t s, CoverDev& cv) {
+  cv.coeffs = coeffs; cv.n = n; cv.dt = dt;
   const long long nchunks_max = (n + kHullChunk - 1) / kHullChunk;
-  // scratch: scales (4 B), G_p flags (1 B), chunk covers (8 B) per coefficient; counts; block sums; stats
   const size_t sz_s = align256((size_t)n * 4), sz_v = align256((size_t)nchunks_max * kHullChunk * sizeof(int2));
-  const size_t sz_g = align256((size_t)n), sz_c = align256((size_t)(nchunks_max + 1) * 4 * 2);
-  const long long nblocks_scan = (n + kScanBlock - 1) / kScanBlock;
-  const size_t sz_b = align256((size_t)(nblocks_scan + 1) * 4);
+  const size_t sz_c = align256((size_t)(nchunks_max + 1) * 4 * 2);
+  if (cudaMalloc(&cv.scales, sz_s) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc(%zu) failed", sz_s); return FPE_ERR_OOM; }
   DevBuf scratch;
-  const size_t total = sz_s + sz_v + sz_g + sz_c + sz_b + align256(sizeof(PreStats));
+  const size_t total = sz_v + sz_c + align256(sizeof(PreStats));
   if (cudaMalloc(&scratch.p, total) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc(%zu) failed", total); return FPE_ERR_OOM; }
   char* q = static_cast<char*>(scratch.p);
-  int32_t* d_s = reinterpret_cast<int32_t*>(q); q += sz_s;
+  int32_t* d_s = static_cast<int32_t*>(cv.scales);
   int2* d_v = reinterpret_cast<int2*>(q); q += sz_v;
-  uint8_t* d_good = reinterpret_cast<uint8_t*>(q); q += sz_g;
   int* d_cnt = reinterpret_cast<int*>(q); q += sz_c;
-  int* d_bsum = reinterpret_cast<int*>(q); q += sz_b;
   PreStats* d_st = reinterpret_cast<PreStats*>(q);
 
   PreStats init{};
@@ -330,11 +323,12 @@ fpe_status precondition_device(const void* coeffs, int64_t n, fpe_dtype dt, int3
   PRE_CUDA(cudaStreamSynchronize(s));
   if (st.nonfinite) { set_error("a coefficient is not finite"); return FPE_ERR_NONFINITE_COEFF; }
   if (st.k_min == 0x7fffffffffffffffll) { set_error("all %lld coefficients are zero", (long long)n); return FPE_ERR_ZERO_POLY; }
-  const long long k_min = st.k_min, k_max = st.k_max, d_eff = k_max - k_min;
+  cv.k_min = st.k_min; cv.k_max = st.k_max;
+  const long long d_eff = cv.k_max - cv.k_min;
 
   // cover: chunk chains, then merges of kMergeFan partial covers until one is left
   int nparts = (int)((d_eff + kHullChunk) / kHullChunk);
-  k_pre_hull_chunk<<<(nparts + 127) / 128, 128, 0, s>>>(d_s, k_min, k_max, d_v, d_cnt, nparts);
+  k_pre_hull_chunk<<<(nparts + 127) / 128, 128, 0, s>>>(d_s, cv.k_min, cv.k_max, d_v, d_cnt, nparts);
   long long stride = kHullChunk;
   int* cnt_a = d_cnt;
   int* cnt_b = d_cnt + (nchunks_max + 1);
@@ -348,28 +342,55 @@ fpe_status precondition_device(const void* coeffs, int64_t n, fpe_dtype dt, int3
   int nv_i = 0;
   PRE_CUDA(cudaMemcpyAsync(&nv_i, cnt_a, sizeof(int), cudaMemcpyDeviceToHost, s));
   PRE_CUDA(cudaStreamSynchronize(s));
-  const long long nv = nv_i;
+  cv.nv = nv_i;
+  if (cudaMalloc(&cv.hull, cv.nv * sizeof(int2)) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc failed"); return FPE_ERR_OOM; }
+  PRE_CUDA(cudaMemcpyAsync(cv.hull, d_v, cv.nv * sizeof(int2), cudaMemcpyDeviceToDevice, s));
+  std::vector<int2> hv(cv.nv);
+  PRE_CUDA(cudaMemcpyAsync(hv.data(), d_v, cv.nv * sizeof(int2), cudaMemcpyDeviceToHost, s));
+  PRE_CUDA(cudaStreamSynchronize(s));
+  cv.hk.resize(cv.nv); cv.hh.resize(cv.nv);
+  for (long long i = 0; i < cv.nv; ++i) { cv.hk[i] = hv[i].x; cv.hh[i] = hv[i].y; }
+  return FPE_OK;
+}
+
+// Stage 2 (for a given p, O(d)): G_p, the shift, the layout and the flat buffer.
+fpe_status cover_finish(const CoverDev& cv, int32_t p_bits, int32_t drop_override, cudaStream_t s, void** dbuf,
+                        Header& hdr, std::vector<int32_t>& hk, std::vector<int32_t>& hh) {
+  const fpe_dtype dt = cv.dt;
+  const int64_t n = cv.n;
+  const bool cplx = (dt == FPE_C64 || dt == FPE_C32);
+  const bool f32 = (dt == FPE_R32 || dt == FPE_C32);
+  const long long k_min = cv.k_min, k_max = cv.k_max, d_eff = k_max - k_min, nv = cv.nv;
+  const long long nblocks_scan = (d_eff + kScanBlock) / kScanBlock;
+  const size_t sz_g = align256((size_t)(d_eff + 1)), sz_b = align256((size_t)(nblocks_scan + 1) * 4);
+  DevBuf scratch;
+  const size_t total = sz_g + sz_b + align256(sizeof(PreStats));
+  if (cudaMalloc(&scratch.p, total) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc(%zu) failed", total); return FPE_ERR_OOM; }
+  char* q = static_cast<char*>(scratch.p);
+  uint8_t* d_good = reinterpret_cast<uint8_t*>(q); q += sz_g;
+  int* d_bsum = reinterpret_cast<int*>(q); q += sz_b;
+  PreStats* d_st = reinterpret_cast<PreStats*>(q);
+  PreStats init{};
+  init.smin = INT32_MAX; init.hmax = INT32_MIN;
+  PRE_CUDA(cudaMemcpyAsync(d_st, &init, sizeof(init), cudaMemcpyHostToDevice, s));
 
   // D and G_p
   const int32_t p = p_bits > 0 ? p_bits : (f32 ? 24 : 53);
   const int32_t drop = drop_override > 0 ? drop_override : p + (d_eff >= 1 ? bit_length(d_eff) : 0) + 3;
   const size_t shm = nv <= 4096 ? (size_t)nv * sizeof(int2) : 0;
-  k_pre_good<<<(int)std::min<long long>((d_eff + 256) / 256, 148 * 8), 256, shm, s>>>(d_s, k_min, k_max, d_v,
-                                                                                     (int)nv, drop, d_good, d_st);
+  k_pre_good<<<(int)std::min<long long>((d_eff + 256) / 256, 148 * 8), 256, shm, s>>>(
+      static_cast<const int32_t*>(cv.scales), k_min, k_max, static_cast<const int2*>(cv.hull), (int)nv, drop, d_good, d_st);
+  PreStats st;
   PRE_CUDA(cudaMemcpyAsync(&st, d_st, sizeof(st), cudaMemcpyDeviceToHost, s));
-  hk.resize(nv); hh.resize(nv);
-  std::vector<int2> hv(nv);
-  PRE_CUDA(cudaMemcpyAsync(hv.data(), d_v, nv * sizeof(int2), cudaMemcpyDeviceToHost, s));
   PRE_CUDA(cudaStreamSynchronize(s));
-  for (long long i = 0; i < nv; ++i) { hk[i] = hv[i].x; hh[i] = hv[i].y; }
+  hk = cv.hk; hh = cv.hh;
   const long long n_good = st.n_good;
   const bool all_good = (n_good == d_eff + 1);
   const bool sparse = (n_good * 32 < d_eff + 1);
   const int32_t shift = st.hmax;
   const int32_t limit = f32 ? 100 : 1000;
   if ((long long)shift - st.smin > limit || drop + 30 > (f32 ? 120 : 1000)) {
-    set_error("coefficient scales of G_p span %d bits (limit %d for this dtype; max %d, min %d, nv %lld)",
-              shift - st.smin, limit, shift, st.smin, nv);
+    set_error("coefficient scales of G_p span %d bits (limit %d for this dtype)", shift - st.smin, limit);
     return FPE_ERR_UNSUPPORTED;
   }
 
@@ -397,14 +418,14 @@ fpe_status precondition_device(const void* coeffs, int64_t n, fpe_dtype dt, int3
   char* b = static_cast<char*>(buf);
   PRE_CUDA(cudaMemsetAsync(b, 0, off, s));
   PRE_CUDA(cudaMemcpyAsync(b, &hdr, sizeof(hdr), cudaMemcpyHostToDevice, s));
-  PRE_CUDA(cudaMemcpyAsync(b + hdr.off_hull, d_v, nv * sizeof(int2), cudaMemcpyDeviceToDevice, s));
+  PRE_CUDA(cudaMemcpyAsync(b + hdr.off_hull, cv.hull, nv * sizeof(int2), cudaMemcpyDeviceToDevice, s));
   const long long n_rel = d_eff + 1;
   const int nb = (int)((n_rel + kScanBlock - 1) / kScanBlock);
   k_scan_block_sums<<<nb, kScanBlock, 0, s>>>(d_good, n_rel, d_bsum);
   k_scan_sums<<<1, 1024, 0, s>>>(d_bsum, nb);
   int32_t* prefix = hdr.off_prefix ? reinterpret_cast<int32_t*>(b + hdr.off_prefix) : nullptr;
   int32_t* sidx = hdr.off_sidx ? reinterpret_cast<int32_t*>(b + hdr.off_sidx) : nullptr;
-  k_pre_fill<<<nb, kScanBlock, 0, s>>>(dt, coeffs, k_min, n_rel, d_good, d_bsum, shift, sparse ? 1 : 0,
+  k_pre_fill<<<nb, kScanBlock, 0, s>>>(dt, cv.coeffs, k_min, n_rel, d_good, d_bsum, shift, sparse ? 1 : 0,
                                        reinterpret_cast<uint8_t*>(b + hdr.off_coef), prefix, sidx);
   if (prefix) {   // prefix[d_eff + 1] = |G_p|
     const int32_t tot = (int32_t)n_good;
@@ -415,6 +436,23 @@ fpe_status precondition_device(const void* coeffs, int64_t n, fpe_dtype dt, int3
   guard.p = nullptr;
   *dbuf = buf;
   return FPE_OK;
+}
+
+void CoverDev::release() {
+  if (scales) cudaFree(scales);
+  if (hull) cudaFree(hull);
+  if (owned) cudaFree(owned);
+  scales = hull = owned = nullptr;
+}
+
+fpe_status precondition_device(const void* coeffs, int64_t n, fpe_dtype dt, int32_t p_bits, int32_t drop_override,
+                               cudaStream_t s, void** dbuf, Header& hdr, std::vector<int32_t>& hk,
+                               std::vector<int32_t>& hh) {
+  CoverDev cv;
+  fpe_status st = cover_build(coeffs, n, dt, s, cv);
+  if (st == FPE_OK) st = cover_finish(cv, p_bits, drop_override, s, dbuf, hdr, hk, hh);
+  cv.release();
+  return st;
 }
 
 }  // namespace fpe

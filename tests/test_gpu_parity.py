@@ -456,3 +456,29 @@ def test_precondition_gpu_errors(fpe):
         with pytest.raises(fpe.FpeError) as e2:
             fpe.precondition(a)
         assert e2.value.status == status
+
+
+def test_partial_preprocessing(fpe):
+    """Remark rem:partialpreproc: one cover (lines 2-3), finished for several p
+    (line 4) in O(d); every finished buffer equals the host preconditioner's at that p, byte for byte."""
+    rng = np.random.default_rng(41)
+    cases = [workloads.coefficients(3), workloads.to_fp32(workloads.coefficients(5)), _many_vertex_coeffs(300, True, 2)]
+    a = rng.normal(size=3000) * np.exp2(rng.integers(-40, 40, 3000))
+    a[rng.random(3000) < 0.5] = 0
+    cases.append(a)
+    for a in cases:
+        cover = fpe.Cover(torch.from_numpy(np.ascontiguousarray(a)).cuda())
+        for p in (0, 53, 30, 12, 4):
+            try:
+                host = fpe.precondition_buffer(a, p=p or None)
+            except fpe.FpeError as e:
+                with pytest.raises(fpe.FpeError) as e2:
+                    cover.finish(p=p or None)
+                assert e2.value.status == e.status
+                continue
+            poly = cover.finish(p=p or None)
+            dev = np.zeros(poly.nbytes, np.uint8)
+            poly.export(dev.ctypes.data, len(dev))
+            torch.cuda.synchronize()
+            assert np.array_equal(host, dev), (a.dtype, len(a), p)
+        cover.close()
