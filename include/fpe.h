@@ -144,6 +144,25 @@ fpe_status fpe_precondition_host(const void* coeffs_host, int64_t n_coeffs, fpe_
 
 fpe_status fpe_poly_get_info(fpe_poly h, fpe_poly_info* out);
 
+/*
+ * fpe_analyse -- the "-analyse" task: the intervals of lambda = log2|z| on which
+ * the evaluation strategy (the reduced polynomial Q_lambda: its region i* and window [l, r],
+ * PAPER.md:1249-1253) is constant, inside [lam_lo, lam_hi].  Host computation on the handle's cover
+ * and G_p: breakpoints are the cover slopes -sigma_i (where i* changes) and, per region, the values
+ * lambda = -J/I at which an index k enters or leaves the band (the exact predicates of the evaluator,
+ * PAPER.md:1543-1559); each interval's (i*, l, r) is classified exactly at its midpoint and equal
+ * neighbours are merged.  Breakpoints are reported rounded to double.  Intended for low degrees
+ * (UNSUPPORTED when d_eff * |cover| > 2^26).
+ *   out    host array of capacity cap (may be NULL with cap = 0 to query the count);
+ *   *n     receives the number of intervals (INVALID_ARG if cap < *n and out != NULL).
+ */
+typedef struct {
+    double lam_lo, lam_hi;   /* the interval [lam_lo, lam_hi] of log2|z|                              */
+    int32_t region, l, r;    /* i* (k_lambda vertex index) and the window [l, r] (absolute indices)   */
+    int32_t kept;            /* |G_p intersected with [l, r]|                                         */
+} fpe_interval;
+fpe_status fpe_analyse(fpe_poly h, double lam_lo, double lam_hi, fpe_interval* out, int64_t cap, int64_t* n);
+
 /* Canonical cover vertices (hk[i], hh[i] = s(a_hk[i])) into host arrays of capacity cap;
  * *n receives the vertex count (INVALID_ARG if cap is too small). */
 fpe_status fpe_poly_get_hull(fpe_poly h, int32_t* hk, int32_t* hh, int64_t cap, int64_t* n);

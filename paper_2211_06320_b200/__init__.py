@@ -81,6 +81,18 @@ class Poly:
         check(lib().fpe_poly_get_hull(self._h, hk.ctypes.data, hh.ctypes.data, n, C.byref(cnt)), "fpe_poly_get_hull")
         return hk, hh
 
+    def analyse(self, lam_lo: float, lam_hi: float) -> np.ndarray:
+        """The -analyse task (fpe_analyse): the lambda = log2|z| intervals on which (i*, l, r) is constant,
+        as a structured array (lam_lo, lam_hi, region, l, r, kept)."""
+        dt = np.dtype([("lam_lo", np.float64), ("lam_hi", np.float64), ("region", np.int32), ("l", np.int32),
+                       ("r", np.int32), ("kept", np.int32)])
+        cnt = C.c_int64(0)
+        check(lib().fpe_analyse(self._h, float(lam_lo), float(lam_hi), None, 0, C.byref(cnt)), "fpe_analyse")
+        out = np.zeros(cnt.value, dt)
+        check(lib().fpe_analyse(self._h, float(lam_lo), float(lam_hi), out.ctypes.data, len(out), C.byref(cnt)),
+              "fpe_analyse")
+        return out
+
     def device_buffer(self):
         p = C.c_void_p(); b = C.c_size_t()
         check(lib().fpe_poly_device_buffer(self._h, C.byref(p), C.byref(b)), "fpe_poly_device_buffer")

@@ -46,6 +46,7 @@ SIGNATURES = {
     "fpe_cover_build": (C.c_int, [_P, _I64, C.c_int, C.c_int, _P, C.POINTER(_P)]),
     "fpe_cover_finish": (C.c_int, [_P, _I32, _I32, _P, C.POINTER(_P)]),
     "fpe_cover_destroy": (None, [_P]),
+    "fpe_analyse": (C.c_int, [_P, C.c_double, C.c_double, _P, _I64, C.POINTER(_I64)]),
     "fpe_precondition_host": (C.c_int, [_P, _I64, C.c_int, _I32, _I32, _P, _SZ, C.POINTER(_SZ)]),
     "fpe_poly_get_info": (C.c_int, [_P, C.POINTER(FpeInfo)]),
     "fpe_poly_get_hull": (C.c_int, [_P, _P, _P, _I64, C.POINTER(_I64)]),

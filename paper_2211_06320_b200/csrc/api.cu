@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of include/fpe.h.
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -8,6 +9,7 @@
 #include <new>
 #include <vector>
 #include "fpe_internal.h"
+#include "fpe_math.cuh"
 #include "kernels.cuh"
 #include "eval_tiled.cuh"
 
@@ -203,6 +205,95 @@ fpe_status fpe_precondition_gpu(const void* coeffs, int64_t n_coeffs, fpe_dtype 
   st = finish_handle(h);
   if (st != FPE_OK) { fpe_destroy(h); return st; }
   *out = h;
+  return FPE_OK;
+}
+
+// -analyse (host): exact classification of a lambda on the handle's cover (the evaluator's predicates,
+// by linear scans: intended for low degrees).
+namespace {
+struct HostClass { int32_t istar, l, r; };
+HostClass classify_host(const std::vector<int32_t>& hk, const std::vector<int32_t>& hh, int drop, double lam) {
+  const int nv = (int)hk.size(), m = nv - 1;
+  int is = m;
+  for (int i = 0; i < m; ++i)
+    if (fpe::sign_lin(lam, (long long)hk[i + 1] - hk[i], (long long)hh[i + 1] - hh[i]) <= 0) { is = i; break; }
+  auto in_band = [&](long long k) {   // cover(k) + lam (k - hk_i*) - hh_i* + D >= 0, exactly
+    int sgm = 0;
+    while (sgm + 1 < m && hk[sgm + 1] <= k) ++sgm;
+    if (m == 0) return true;
+    const long long dk = (long long)hk[sgm + 1] - hk[sgm], dh = (long long)hh[sgm + 1] - hh[sgm];
+    const long long J = ((long long)hh[sgm] - hh[is] + drop) * dk + dh * (k - hk[sgm]);
+    const long long I = (k - hk[is]) * dk;
+    return fpe::sign_lin(lam, I, J) >= 0;
+  };
+  long long l = hk[is], r = hk[is];
+  while (l - 1 >= hk[0] && in_band(l - 1)) --l;   // the band is an interval containing hk_i*
+  while (r + 1 <= hk[m] && in_band(r + 1)) ++r;
+  return HostClass{is, (int32_t)l, (int32_t)r};
+}
+}  // namespace
+
+fpe_status fpe_analyse(fpe_poly h, double lam_lo, double lam_hi, fpe_interval* out, int64_t cap, int64_t* n) {
+  if (!h || !n || !(lam_lo < lam_hi) || !std::isfinite(lam_lo) || !std::isfinite(lam_hi) || cap < 0) {
+    set_error("fpe_analyse: invalid argument");
+    return FPE_ERR_INVALID_ARG;
+  }
+  const auto& hk = h->hk;
+  const auto& hh = h->hh;
+  const int nv = (int)hk.size(), m = nv - 1, drop = h->hdr.drop;
+  const long long d_eff = h->hdr.k_max - h->hdr.k_min;
+  if ((double)(d_eff + 1) * nv > (double)(1 << 26)) { set_error("fpe_analyse: d_eff * |cover| too large"); return FPE_ERR_UNSUPPORTED; }
+  // G_p membership for the kept counts (prefix counts, compact list, or all good)
+  DeviceGuard g(h->device);
+  std::vector<int32_t> aux;
+  if (!h->hdr.all_good) {
+    const bool sp = h->hdr.sparse;
+    const size_t cnt = sp ? (size_t)h->hdr.n_good : (size_t)(d_eff + 2);
+    aux.resize(cnt);
+    FPE_CUDA(cudaMemcpy(aux.data(), static_cast<char*>(h->dbuf) + (sp ? h->hdr.off_sidx : h->hdr.off_prefix),
+                        cnt * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  }
+  auto kept = [&](long long l, long long r) -> int32_t {
+    if (h->hdr.all_good) return (int32_t)(r - l + 1);
+    if (!h->hdr.sparse) return aux[r + 1 - h->hdr.k_min] - aux[l - h->hdr.k_min];
+    return (int32_t)(std::upper_bound(aux.begin(), aux.end(), (int32_t)r) - std::lower_bound(aux.begin(), aux.end(), (int32_t)l));
+  };
+  // candidate breakpoints: slopes, and per region i the band entry/exit values of every index
+  std::vector<double> bp;
+  for (int i = 0; i < m; ++i) bp.push_back(-(double)(hh[i + 1] - hh[i]) / (double)(hk[i + 1] - hk[i]));
+  for (int i = 0; i <= m; ++i) {
+    for (int sgm = 0; sgm < std::max(m, 1); ++sgm) {
+      const long long k0 = hk[sgm], k1 = m ? hk[sgm + 1] : hk[0];
+      for (long long k = k0; k <= k1; ++k) {
+        if (k == hk[i]) continue;
+        const long long dk = m ? (long long)hk[sgm + 1] - hk[sgm] : 1, dh = m ? (long long)hh[sgm + 1] - hh[sgm] : 0;
+        const long long J = ((long long)hh[sgm] - hh[i] + drop) * dk + dh * (k - hk[sgm]);
+        const long long I = (k - hk[i]) * dk;
+        const double b = -(double)J / (double)I;
+        if (b > lam_lo && b < lam_hi) bp.push_back(b);
+      }
+    }
+  }
+  bp.push_back(lam_lo);
+  bp.push_back(lam_hi);
+  std::sort(bp.begin(), bp.end());
+  bp.erase(std::unique(bp.begin(), bp.end()), bp.end());
+  std::vector<fpe_interval> iv;
+  for (size_t j = 0; j + 1 < bp.size(); ++j) {
+    const double a = std::max(bp[j], lam_lo), b = std::min(bp[j + 1], lam_hi);
+    if (!(a < b)) continue;
+    const HostClass c = classify_host(hk, hh, drop, 0.5 * (a + b));
+    if (!iv.empty() && iv.back().region == c.istar && iv.back().l == c.l && iv.back().r == c.r) {
+      iv.back().lam_hi = b;
+    } else {
+      iv.push_back(fpe_interval{a, b, c.istar, c.l, c.r, kept(c.l, c.r)});
+    }
+  }
+  *n = (int64_t)iv.size();
+  if (out) {
+    if (cap < (int64_t)iv.size()) { set_error("fpe_analyse: need %zu intervals", iv.size()); return FPE_ERR_INVALID_ARG; }
+    std::copy(iv.begin(), iv.end(), out);
+  }
   return FPE_OK;
 }
 

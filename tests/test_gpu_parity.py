@@ -482,3 +482,36 @@ def test_partial_preprocessing(fpe):
             torch.cuda.synchronize()
             assert np.array_equal(host, dev), (a.dtype, len(a), p)
         cover.close()
+
+
+def test_analyse_intervals(fpe, worked):
+    """-analyse: the lambda intervals of constant (i*, l, r) tile [lo, hi], neighbours
+    differ, and every interval's triple (and kept count) is the oracle's at points inside it; on the
+    paper's worked example the intervals through lambda = 0 and -3 carry the printed bands."""
+    s = np.array(worked["scales"])
+    wa = np.ldexp(1.0, s - 1).astype(np.complex128)
+    rng = np.random.default_rng(51)
+    b = rng.normal(size=600) * np.exp2(rng.integers(-30, 30, 600))
+    b[rng.random(600) < 0.6] = 0
+    cases = [(wa, 6), (wa, None), (workloads.coefficients(1, d=200), None), (b, None),
+             (_many_vertex_coeffs(40, True, 3), None)]
+    for a, drop in cases:
+        poly = fpe.precondition(a, p=6 if drop else None, drop=drop)
+        P = oracle.OraclePoly(a, p=6 if drop else None, drop=drop)
+        iv = poly.analyse(-12.0, 12.0)
+        assert iv[0]["lam_lo"] == -12.0 and iv[-1]["lam_hi"] == 12.0
+        assert np.all(iv["lam_hi"][:-1] == iv["lam_lo"][1:])
+        trip = np.stack([iv["region"], iv["l"], iv["r"]], 1)
+        assert np.all(np.any(trip[1:] != trip[:-1], axis=1))
+        for f in (0.5, 0.01, 0.99):
+            lam = iv["lam_lo"] + f * (iv["lam_hi"] - iv["lam_lo"])
+            ist, l, r = P.search(lam)
+            assert np.array_equal(ist, iv["region"]) and np.array_equal(l, iv["l"]) and np.array_equal(r, iv["r"])
+            K = P.good_prefix[r + 1] - P.good_prefix[l]
+            assert np.array_equal(K, iv["kept"])
+        if drop == 6:
+            band = worked["derived_not_printed"]["band_drop6"]
+            for lam, key in ((0.0, "lambda0"), (-3.0, "lambda_m3")):
+                j = np.flatnonzero((iv["lam_lo"] < lam) & (lam < iv["lam_hi"]))
+                if len(j):
+                    assert [iv["l"][j[0]], iv["r"][j[0]]] == band[key]
