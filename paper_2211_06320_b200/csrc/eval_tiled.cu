@@ -620,7 +620,10 @@ constexpr size_t ring_bytes() {
 // Persistent evaluator: every warp first takes parallel pieces of long windows, then whole groups,
 // both from global atomic counters (largest work first; the tail is at most one group).
 template <int PK, int CK, int OK, int NP>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_eval_tiled(long long n, PolyDev P,
+#ifndef FPE_EVAL_MIN_CTAS
+#define FPE_EVAL_MIN_CTAS 3   // CTAs per SM the register budget is sized for (12 warps)
+#endif
+__global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(long long n, PolyDev P,
                                                                PtRec* rec, Plan plan) {
   using CT = typename Step<CK>::CT;
   extern __shared__ __align__(128) unsigned char smem[];
