@@ -80,6 +80,15 @@ __device__ __forceinline__ bool band_seg(int2 a, int2 b, int2 vs, int drop, doub
   return sign_lin(lam, I, J) >= 0;
 }
 
+// 1/c for the boundary estimates below: the fp32 reciprocal refined by one Newton step in fp64 (relative
+// error ~2^-46; an IEEE division costs a subroutine of ~40 instructions).  The estimate only seeds the
+// exact predicate tests, which correct any error (and fall back to bisection), so the result is exact
+// whatever the estimate.
+__device__ __forceinline__ double rcp_est(double c) {
+  const double r = (double)__frcp_rn((float)c);
+  return fma(r, fma(-c, r, 1.0), r);
+}
+
 // Least k in [lo, hi] with band_seg(A, B, ...) true, given that it holds at hi and the predicate
 // is monotone on the segment (left branch: increasing).  The sheared cover is affine on the
 // segment, F(k) = c0 + c1 k, so the crossing is estimated in fp64 and then verified exactly.
@@ -92,7 +101,7 @@ __device__ __forceinline__ long long seg_first_true(int2 A, int2 B, int2 vs, int
   const double g = __fma_rn(lam, (double)(A.x - vs.x), (double)(A.y - vs.y + drop));
   long long k = hi;
   if (c1 > 0.0) {
-    double e = (double)A.x + ceil(-(g * dk) / c1);
+    double e = (double)A.x + ceil(-(g * dk) * rcp_est(c1));
     if (e >= (double)lo && e <= (double)hi) k = (long long)e;
     else if (e < (double)lo) k = lo;
   }
@@ -119,7 +128,7 @@ __device__ __forceinline__ long long seg_last_true(int2 A, int2 B, int2 vs, int 
   const double g = __fma_rn(lam, (double)(A.x - vs.x), (double)(A.y - vs.y + drop));
   long long k = lo;
   if (c1 < 0.0) {
-    double e = (double)A.x + floor(-(g * dk) / c1);
+    double e = (double)A.x + floor(-(g * dk) * rcp_est(c1));
     if (e >= (double)lo && e <= (double)hi) k = (long long)e;
     else if (e > (double)hi) k = hi;
   }
@@ -147,7 +156,7 @@ __device__ __forceinline__ long long seg_first_true_p(int2 A, int2 B, int2 vs, i
   const double g = __fma_rn(lam, (double)(A.x - vs.x), (double)(A.y - vs.y + drop));
   long long k = hi;
   if (c1 > 0.0) {
-    double e = (double)A.x + ceil(-(g * dk) / c1);
+    double e = (double)A.x + ceil(-(g * dk) * rcp_est(c1));
     if (e >= (double)lo && e <= (double)hi) k = (long long)e;
     else if (e < (double)lo) k = lo;
   }
@@ -172,7 +181,7 @@ __device__ __forceinline__ long long seg_last_true_p(int2 A, int2 B, int2 vs, in
   const double g = __fma_rn(lam, (double)(A.x - vs.x), (double)(A.y - vs.y + drop));
   long long k = lo;
   if (c1 < 0.0) {
-    double e = (double)A.x + floor(-(g * dk) / c1);
+    double e = (double)A.x + floor(-(g * dk) * rcp_est(c1));
     if (e >= (double)lo && e <= (double)hi) k = (long long)e;
     else if (e > (double)hi) k = hi;
   }
