@@ -278,11 +278,26 @@ __device__ __forceinline__ void classify_lambda_v(const int2* hull, const double
 }
 
 // The vertex searches of classify_lambda_v for a lambda policy (finite lambda; predicates in doubles).
+// Most points lie beyond the extreme cover slopes and have narrow bands, so k_lambda tests the two end
+// slopes before bisecting, and the band's end vertices are found by galloping outward from i*
+// (1, 2, 4, ... vertices, then bisection inside the last step): a narrow band costs one test per side.
 template <typename L>
 __device__ __forceinline__ void classify_lambda_vp(const int2* hull, const double2* hv, int nv, int drop, const L& pl,
                                                    int& istar, int& l, int& r) {
   const int m = nv - 1;
-  int a = 0, b = m;
+  int a = 0, b = m;   // least i in [0, m) with lambda dk_i + dh_i <= 0, else m
+  if (m > 0) {
+    const double2 v0 = hv[0], v1 = hv[1];
+    if (pl.le0(v1.x - v0.x, v1.y - v0.y)) {
+      b = 0;
+    } else {
+      a = 1;
+      if (m > 1) {
+        const double2 w0 = hv[m - 1], w1 = hv[m];
+        if (pl.le0(w1.x - w0.x, w1.y - w0.y)) b = m - 1; else a = m;
+      }
+    }
+  }
   while (a < b) {
     const int i = (a + b) >> 1;
     const double2 v0 = hv[i], v1 = hv[i + 1];
@@ -291,12 +306,15 @@ __device__ __forceinline__ void classify_lambda_vp(const int2* hull, const doubl
   istar = a;
   const double2 vs = hv[a];
   const double Dd = (double)drop;
-  a = 0; b = istar;
-  while (a < b) {
-    const int j = (a + b) >> 1;
-    const double2 v = hv[j];
-    if (pl.ge0(v.x - vs.x, (v.y - vs.y) + Dd)) b = j; else a = j + 1;
+  auto band = [&](int j) { const double2 v = hv[j]; return pl.ge0(v.x - vs.x, (v.y - vs.y) + Dd); };
+  int t = istar, f = -1;   // least vertex in the band: band(t) true, band(f) false (f = -1: none)
+  for (int st = 1;; st <<= 1) {
+    const int j = istar - st;
+    if (j < 0) break;
+    if (band(j)) t = j; else { f = j; break; }
   }
+  while (t - f > 1) { const int mid = (f + t) >> 1; if (band(mid)) t = mid; else f = mid; }
+  a = t;
   const int2 vsi = hull[istar];
   if (a == 0) {
     l = hull[0].x;
@@ -304,12 +322,14 @@ __device__ __forceinline__ void classify_lambda_vp(const int2* hull, const doubl
     const int2 A = hull[a - 1], B = hull[a];
     l = (int)seg_first_true_p(A, B, vsi, drop, pl, (long long)A.x + 1, (long long)B.x);
   }
-  a = istar; b = m;
-  while (a < b) {
-    const int j = (a + b + 1) >> 1;
-    const double2 v = hv[j];
-    if (pl.ge0(v.x - vs.x, (v.y - vs.y) + Dd)) a = j; else b = j - 1;
+  t = istar; f = m + 1;    // greatest vertex in the band
+  for (int st = 1;; st <<= 1) {
+    const int j = istar + st;
+    if (j > m) break;
+    if (band(j)) t = j; else { f = j; break; }
   }
+  while (f - t > 1) { const int mid = (t + f) >> 1; if (band(mid)) t = mid; else f = mid; }
+  a = t;
   if (a == m) {
     r = hull[m].x;
   } else {
