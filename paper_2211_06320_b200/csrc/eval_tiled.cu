@@ -148,6 +148,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -473,13 +476,44 @@ __device__ __forceinline__ void load_group(Pts<NP>& S, uint32_t g, long long n, 
   }
 }
 
+// The Horner sums of piece p = [rlo, rhi] for the NP points of every lane (b = 0 on entry).  Points that
+// cover the whole piece on the tensor cores (mma_covers; complex fp64 coefficients) take k_eval_mma's
+// partial from its scratch instead; the others stream the part of the piece their windows need.
 template <int CK, int NP, bool CPLX>
-__device__ __forceinline__ void eval_piece(Ring<CK>& R, const Pts<NP>& S, int rlo, int rhi,
-                                           typename Step<CK>::W (&br)[NP], typename Step<CK>::W (&bi)[NP]) {
+__device__ __forceinline__ void eval_piece(Ring<CK>& R, const Pts<NP>& S, int rlo, int rhi, int p, const GroupDesc& d,
+                                           const Plan& plan, typename Step<CK>::W (&br)[NP],
+                                           typename Step<CK>::W (&bi)[NP]) {
   using W = typename Step<CK>::W;
   W zr[NP], zi[NP];
 #pragma unroll
   for (int j = 0; j < NP; ++j) { zr[j] = (W)S.x[j]; zi[j] = (W)S.y[j]; br[j] = 0; bi[j] = 0; }
+  if constexpr (CK == FPE_C64) {
+    if (d.mma_np > 0 && p >= d.mma_p0 && p < d.mma_p0 + d.mma_np) {
+      int wl[NP], wr[NP];
+      bool cov[NP];
+      int v_lo = rhi + 1, v_hi = rlo - 1;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        cov[j] = mma_covers(S.wl[j], S.wr[j], S.x[j], S.y[j], p);
+        wl[j] = cov[j] ? 0x3fffffff : S.wl[j];
+        wr[j] = cov[j] ? -1 : S.wr[j];
+        if (wl[j] <= wr[j] && wl[j] <= rhi && wr[j] >= rlo) { v_lo = min(v_lo, wl[j]); v_hi = max(v_hi, wr[j]); }
+      }
+      v_lo = max(rlo, __reduce_min_sync(0xffffffffu, v_lo));
+      v_hi = min(rhi, __reduce_max_sync(0xffffffffu, v_hi));
+      if (v_lo <= v_hi) {
+        ring_begin(R, v_lo, v_hi);
+        stream_range<CK, NP, CPLX>(R, v_lo, v_hi, wl, wr, zr, zi, br, bi);
+      }
+      const double2* scr = plan.mma_scratch + (size_t)(d.mma_slot + (p - d.mma_p0)) * plan.gsize;
+      const int lane = threadIdx.x & 31;
+#pragma unroll
+      for (int j = 0; j < NP; ++j)
+        if (cov[j]) { const double2 v = __ldcg(scr + j * 32 + lane); br[j] = v.x; bi[j] = v.y; }
+      return;
+    }
+  }
+  ring_begin(R, rlo, rhi);
   stream_range<CK, NP, CPLX>(R, rlo, rhi, S.wl, S.wr, zr, zi, br, bi);
 }
 
@@ -531,7 +565,7 @@ __device__ __forceinline__ void group_unpack(Pts<NP>& S, const GroupCtx<NP>& c, 
 
 template <int PK, int CK, int OK, int NP, typename Prefetch>
 __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c, long long n, const PolyDev& P,
-                                             PtOut* out, Prefetch prefetch) {
+                                             const Plan& plan, PtOut* out, Prefetch prefetch) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
   const GroupDesc d = c.d;
@@ -545,9 +579,8 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c,
   if (nonempty) {
     for (int p = p_hi; p >= p_lo; --p) {
       const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
-      ring_begin(R, rlo, rhi);
       W br[NP], bi[NP];
-      eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, br, bi);
+      eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, p, d, plan, br, bi);
 #pragma unroll
       for (int j = 0; j < NP; ++j)
         if (S.wl[j] <= S.wr[j] && S.wl[j] <= p * kPiece + kPiece - 1 && S.wr[j] >= p * kPiece)
@@ -576,11 +609,10 @@ __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long
   const GroupDesc d = plan.desc[g];
   const int kmin = (int)P.k_min;
   const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
-  ring_begin(R, rlo, rhi);
   Pts<NP> S;
   load_group<PK, NP>(S, g, n, rec, kmin);
   W br[NP], bi[NP];
-  eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, br, bi);
+  eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, p, d, plan, br, bi);
   const int p0 = d.lo / kPiece;
   W2* scr = static_cast<W2*>(plan.scratch);
 #pragma unroll
@@ -665,8 +697,201 @@ __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(l
       if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
     };
     if (cur.d.npieces > 1) fetch_next();   // evaluated as parallel pieces (multi_piece)
-    else single_group<PK, CK, OK, NP>(R, cur, n, P, out, fetch_next);
+    else single_group<PK, CK, OK, NP>(R, cur, n, P, plan, out, fetch_next);
     cur = nx;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Whole kPiece-aligned pieces on the FP64 tensor cores (complex fp64 coefficients).
+//
+// A DFMA that reads three fresh register pairs issues at 2/3 of the fp64 rate on B200 and ptxas's
+// schedule of the complex Horner step leaves most DFMAs without a reused operand: the vector Horner tops
+// out near 72% of the pipe.  mma.sync DMMA runs the same datapath from its fragments at 99.7%
+// (profiles/r01_dmma_vs_dfma.json).  Over whole 256-coefficient chunks the Horner sum is a dense
+// contraction once split by phase k mod 16:
+//   sum_{k in piece} a_k z^{k-k0} = sum_{m<16} z^m R_m,  R_m = sum_t a_{k0+16t+m} u^t,  u = z^16,
+// and each chunk q is C <- C (.) w + A V with A[m][i] = a_{256q+16i+m} (16 x 16, straight from the staged
+// chunk), V[i][p] = u_p^i, w_p = u_p^16 = z_p^256 and C[m][p] = R_m at point p: 4 real m16n8k4 DMMAs per
+// 4 powers and 8 points for the complex product.  One CTA (8 warps x 16 points = a group) per item
+// (group, piece), the piece's 64 chunks staged once per CTA by TMA into a 4-stage ring shared by the
+// warps.  A point's column is active iff mma_covers (its window covers the whole piece), so every value
+// is relative to the piece start, which lies in the point's window; u, u^4, w are
+// rounded once from double-double squarings (w carries 1 ulp per chunk, the chunk powers ~11 ulp).
+#ifndef FPE_NO_MMA_ITEMS
+#define FPE_NO_MMA_ITEMS 0   // experiments: 1 keeps every piece on the vector Horner
+#endif
+constexpr int kMmaWarps = 8;
+constexpr int kMmaStages = 4;
+constexpr int kPieceChunks = kPiece / kChunk;
+
+__device__ __forceinline__ void cmul(double& r, double& i, double ar, double ai, double br, double bi) {
+  const double t = fma(ar, br, -ai * bi);
+  i = fma(ar, bi, ai * br);
+  r = t;
+}
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b));
+}
+__device__ __forceinline__ void dd_sqr_c(xc_t& v) {
+  xc_sqr(v);
+  const dd_t r = two_sum(v.hr, v.er), i = two_sum(v.hi, v.ei);
+  v.hr = r.hi; v.er = r.lo; v.hi = i.hi; v.ei = i.lo;
+}
+
+__global__ void __launch_bounds__(kMmaWarps * 32, 1) k_eval_mma(long long n, const double2* __restrict__ coef,
+                                                                int kmin, const PtRec* __restrict__ rec, Plan plan) {
+  __shared__ __align__(128) double2 ring[kMmaStages][kChunk];
+  __shared__ uint64_t full[kMmaStages], empty[kMmaStages];
+  __shared__ uint2 item_sh;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, c = lane & 3;
+  if (tid == 0) {
+    for (int s = 0; s < kMmaStages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, kMmaWarps); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t n_items = min(plan.mma_ctrs[0], plan.mma_cap);
+  uint32_t t_seq = 0;      // chunks consumed by this CTA (every warp consumes every chunk)
+  uint32_t t_issued = 0;   // chunks issued (thread 0)
+  auto issue = [&](int piece_chunk) {   // thread 0: next chunk into the ring
+    const int s = (int)(t_issued % kMmaStages);
+    if (t_issued >= (uint32_t)kMmaStages) mbar_wait(empty + s, ((t_issued / kMmaStages) - 1) & 1u);
+    fence_proxy_async();
+    mbar_expect_tx(full + s, kChunk * sizeof(double2));
+    tma_load_1d(ring[s], coef + (size_t)piece_chunk * kChunk, kChunk * sizeof(double2), full + s);
+    ++t_issued;
+  };
+  for (;;) {
+    if (tid == 0) {
+      const uint32_t it = atomicAdd(plan.mma_ctrs + 1, 1u);
+      item_sh = it < n_items ? plan.mma_items[it] : make_uint2(0xfffffffeu, 0u);
+    }
+    __syncthreads();
+    const uint2 item = item_sh;
+    __syncthreads();
+    if (item.x == 0xfffffffeu) break;
+    if (item.x == ~0u) continue;
+    const uint32_t grp = item.x;
+    const int p = (int)item.y;
+    const int q0 = p * kPieceChunks + kPieceChunks - 1;   // chunks descend from q0
+    if (tid == 0)
+      for (int i = 0; i < kMmaStages; ++i) issue(q0 - i);
+    __syncwarp();
+    // this warp's 16 points: lanes [0, 16) own point 16 w + lane (lanes 16..31 mirror them)
+    const int q = 16 * w + (lane & 15);
+    const long long pos = (long long)grp * plan.gsize + q;
+    double x = 0.0, y = 0.0;
+    int wl = 1, wr = 0;
+    if (pos < n) {
+      const int4 h = __ldg(reinterpret_cast<const int4*>(rec + pos));
+      const double2 z = __ldg(reinterpret_cast<const double2*>(rec + pos) + 1);
+      x = z.x; y = z.y;
+      if (h.w >= h.z) { wl = h.z - kmin; wr = h.w - kmin; }
+    }
+    const int act = mma_covers(wl, wr, x, y, p) ? 1 : 0;
+    // u = z^16, u^4, w = z^256 of the lane's point (double-double squarings, one rounding each)
+    double ur, ui, u4r, u4i, wwr, wwi;
+    {
+      xc_t v{act ? x : 1.0, act ? y : 0.0, 0.0, 0.0, 0};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dd_sqr_c(v);
+      ur = v.hr + v.er; ui = v.hi + v.ei;
+      dd_sqr_c(v); dd_sqr_c(v);
+      u4r = v.hr + v.er; u4i = v.hi + v.ei;
+      dd_sqr_c(v); dd_sqr_c(v);
+      wwr = v.hr + v.er; wwi = v.hi + v.ei;
+    }
+    double vr[2][4], vi[2][4], cwr[2][2], cwi[2][2], cr[2][4], ci[2][4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int src = 8 * t + g;                   // the point of B column g
+      const double qr = __shfl_sync(0xffffffffu, ur, src), qi = __shfl_sync(0xffffffffu, ui, src);
+      const double q4r = __shfl_sync(0xffffffffu, u4r, src), q4i = __shfl_sync(0xffffffffu, u4i, src);
+      const int on = __shfl_sync(0xffffffffu, act, src);
+      double pr = 1.0, pi = 0.0;                   // u^c
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        if (i < c) cmul(pr, pi, pr, pi, qr, qi);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {             // B row c of k-step ks: u^(4 ks + c); inactive column: 0
+        if (ks) cmul(pr, pi, pr, pi, q4r, q4i);
+        vr[t][ks] = on ? pr : 0.0;
+        vi[t][ks] = on ? pi : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {                // w of the C columns 2c, 2c + 1
+        const int s2 = 8 * t + 2 * c + e;
+        cwr[t][e] = __shfl_sync(0xffffffffu, wwr, s2);
+        cwi[t][e] = __shfl_sync(0xffffffffu, wwi, s2);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) { cr[t][e] = 0.0; ci[t][e] = 0.0; }
+    }
+    for (int k = 0; k < kPieceChunks; ++k) {
+      const int s = (int)(t_seq % kMmaStages);
+      mbar_wait(full + s, (t_seq / kMmaStages) & 1u);
+      const double2* cb = ring[s];
+      if (k) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) cmul(cr[t][e], ci[t][e], cr[t][e], ci[t][e], cwr[t][e & 1], cwi[t][e & 1]);
+      }
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const double2 a0 = cb[64 * ks + 16 * c + g], a1 = cb[64 * ks + 16 * c + g + 8];   // A[g|g+8][4ks + c]
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          dmma(cr[t], a0.x, a1.x, vr[t][ks]);      // Re: ar vr - ai vi
+          dmma(cr[t], -a0.y, -a1.y, vi[t][ks]);
+          dmma(ci[t], a0.x, a1.x, vi[t][ks]);      // Im: ar vi + ai vr
+          dmma(ci[t], a0.y, a1.y, vr[t][ks]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+      ++t_seq;
+      if (tid == 0 && k + kMmaStages < kPieceChunks) issue(q0 - k - kMmaStages);
+      __syncwarp();
+    }
+    // sum_m z^m R_m: rows g and g + 8 in the thread, then a tree over g (lane bits 2..4)
+    double hr[2][2], hi[2][2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int src = 8 * t + 2 * c + e;
+        const double zr = __shfl_sync(0xffffffffu, x, src), zi = __shfl_sync(0xffffffffu, y, src);
+        double z2r, z2i, z4r, z4i, z8r, z8i;
+        cmul(z2r, z2i, zr, zi, zr, zi);
+        cmul(z4r, z4i, z2r, z2i, z2r, z2i);
+        cmul(z8r, z8i, z4r, z4i, z4r, z4i);
+        double pr = cr[t][e], pi = ci[t][e];
+        pr = fma(cr[t][e + 2], z8r, fma(-ci[t][e + 2], z8i, pr));
+        pi = fma(cr[t][e + 2], z8i, fma(ci[t][e + 2], z8r, pi));
+        double nr = __shfl_xor_sync(0xffffffffu, pr, 4), ni = __shfl_xor_sync(0xffffffffu, pi, 4);
+        pr = fma(nr, zr, fma(-ni, zi, pr)); pi = fma(nr, zi, fma(ni, zr, pi));
+        nr = __shfl_xor_sync(0xffffffffu, pr, 8); ni = __shfl_xor_sync(0xffffffffu, pi, 8);
+        pr = fma(nr, z2r, fma(-ni, z2i, pr)); pi = fma(nr, z2i, fma(ni, z2r, pi));
+        nr = __shfl_xor_sync(0xffffffffu, pr, 16); ni = __shfl_xor_sync(0xffffffffu, pi, 16);
+        pr = fma(nr, z4r, fma(-ni, z4i, pr)); pi = fma(nr, z4i, fma(ni, z4r, pi));
+        hr[t][e] = pr; hi[t][e] = pi;              // valid in lanes 0..3 (g = 0)
+      }
+    double orr = 0.0, oi = 0.0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double a = __shfl_sync(0xffffffffu, hr[t][e], (lane & 7) >> 1);
+        const double b = __shfl_sync(0xffffffffu, hi[t][e], (lane & 7) >> 1);
+        if (((lane >> 3) & 1) == t && (lane & 1) == e) { orr = a; oi = b; }
+      }
+    if (lane < 16 && act) {
+      const GroupDesc d = plan.desc[grp];
+      plan.mma_scratch[(size_t)(d.mma_slot + (p - d.mma_p0)) * plan.gsize + q] = make_double2(orr, oi);
+    }
   }
 }
 
@@ -863,8 +1088,12 @@ static size_t scratch_slots(long long n) {
   return bytes / 1024;
 }
 
+// DMMA items: scratch of 2 KiB per (group, piece), 4 bytes per point (at least 64 items)
+static size_t mma_cap(long long n) { return max((size_t)64, (size_t)n * 4 / (128 * sizeof(double2))); }
+
 size_t tiled_ws_bytes(long long n) {
   return al256(n * sizeof(int2)) + al256(n * sizeof(uint2)) + al256(n * sizeof(PtRec)) + al256(n * 4) +
+         al256(mma_cap(n) * sizeof(uint2)) + al256(mma_cap(n) * 128 * sizeof(double2)) +
          al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) +
          al256(max_groups(n) * sizeof(GroupDesc)) + al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
@@ -966,15 +1195,20 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   plan.gcnt = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
   plan.items = reinterpret_cast<uint2*>(p); p += al256(scratch_slots(n) * sizeof(uint2));
   plan.scratch = p; p += al256(scratch_slots(n) * 1024);
+  plan.mma_items = reinterpret_cast<uint2*>(p); p += al256(mma_cap(n) * sizeof(uint2));
+  plan.mma_scratch = reinterpret_cast<double2*>(p); p += al256(mma_cap(n) * 128 * sizeof(double2));
+  plan.mma_cap = (uint32_t)mma_cap(n);
   plan.ctrs = reinterpret_cast<uint32_t*>(p);
+  plan.mma_ctrs = plan.ctrs + 4;
   const int np = np_for(pk, P.cdt);
   plan.gsize = 32 * np;
+  plan.mma_on = (P.cdt == FPE_C64 && plan.gsize == 128 && !FPE_NO_MMA_ITEMS) ? 1 : 0;
   plan.ngroups = (uint32_t)((n + plan.gsize - 1) / plan.gsize);
   const bool f32 = (P.cdt == FPE_R32 || P.cdt == FPE_C32);
   const size_t slot_bytes = (size_t)plan.gsize * (f32 ? sizeof(float2) : sizeof(double2));
   plan.cap = (uint32_t)(scratch_slots(n) * 1024 / slot_bytes);
   cudaMemsetAsync(gcount, 0, (kBuckets + 1) * 4, s);
-  cudaMemsetAsync(plan.ctrs, 0, 16, s);
+  cudaMemsetAsync(plan.ctrs, 0, 32, s);   // [0..3] vector items / groups / slots, [4..5] DMMA items
   switch (pk) {
     case FPE_R64: launch_classify_bucket_t<FPE_R64>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
     case FPE_C64: launch_classify_bucket_t<FPE_C64>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
@@ -985,6 +1219,20 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   bucket_finish(reinterpret_cast<const uint2*>(keys), lr, n, pts_per_cta(n), gcount, cta_base, bstart, rec, spos, pk,
                 pts, P.k_min, plan, s);
   st.mark("bucket");
+  int lm = 0;
+  if (plan.mma_on) {
+    static int grid_mma = 0;
+    if (grid_mma == 0) {
+      int per_sm = 0, dev = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_mma, kMmaWarps * 32, 0);
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      grid_mma = max(1, per_sm) * sms;
+    }
+    k_eval_mma<<<grid_mma, kMmaWarps * 32, 0, s>>>(n, static_cast<const double2*>(P.coef), (int)P.k_min, rec, plan);
+    st.mark("eval_mma");
+    lm = 1;
+  }
   int le = 0;
 #define FPE_EV(PKV, CKV) \
   le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(n, P, rec, plan, s)
@@ -1011,7 +1259,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     default: k_unsort<FPE_C64><<<(int)blocks, 256, 0, s>>>(staged, spos, n, vals, exps); break;
   }
   st.mark("unsort");
-  return 5 + le;
+  return 5 + le + lm;
 }
 
 }  // namespace fpe

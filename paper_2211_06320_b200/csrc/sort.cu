@@ -103,21 +103,40 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const PtRec* __restri
   const long long first = g * gs;
   if (first >= n) return;
   const int count = (int)min((long long)gs, n - first);
-  int lo = 0x7fffffff, hi = -1;
+  int lo = 0x7fffffff, hi = -1, clo = 0x7fffffff, chi = -1;
   for (int j = lane; j < count; j += 32) {
     const int4 h = __ldg(reinterpret_cast<const int4*>(rec + first + j));
     if (h.w >= h.z) {
-      lo = min(lo, (int)(h.z - k_min));
-      hi = max(hi, (int)(h.w - k_min));
+      const int wl = (int)(h.z - k_min), wr = (int)(h.w - k_min);
+      lo = min(lo, wl);
+      hi = max(hi, wr);
+      if (plan.mma_on) {   // the pieces this point covers whole on the tensor cores
+        const double2 z = __ldg(reinterpret_cast<const double2*>(rec + first + j) + 1);
+        const int c0 = (wl + kPiece - 1) / kPiece, c1 = (wr + 1) / kPiece - 1;
+        if (c0 <= c1 && mma_covers(wl, wr, z.x, z.y, c0)) { clo = min(clo, c0); chi = max(chi, c1); }
+      }
     }
   }
   lo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
   hi = __reduce_max_sync(0xffffffffu, hi);
+  clo = (int)__reduce_min_sync(0xffffffffu, (unsigned)clo);
+  chi = __reduce_max_sync(0xffffffffu, chi);
   if (lane != 0) return;
   GroupDesc d;
   d.p0 = (uint32_t)first;
   d.count = count;
   d.lo = lo; d.hi = hi; d.slot = 0; d.npieces = 1;
+  d.mma_p0 = 0; d.mma_np = 0; d.mma_slot = 0; d.pad = 0;
+  if (clo <= chi) {
+    const int np = chi - clo + 1;
+    const uint32_t base = atomicAdd(plan.mma_ctrs, (uint32_t)np);
+    if ((unsigned long long)base + np <= plan.mma_cap) {
+      d.mma_p0 = clo; d.mma_np = np; d.mma_slot = base;
+      for (int i = 0; i < np; ++i) plan.mma_items[base + i] = make_uint2((uint32_t)g, (uint32_t)(clo + i));
+    } else {   // DMMA scratch exhausted: these pieces stay on the vector path
+      for (uint32_t i = base; i < plan.mma_cap && i < base + (uint32_t)np; ++i) plan.mma_items[i] = make_uint2(~0u, 0u);
+    }
+  }
   if (hi >= lo && hi - lo + 1 > kPiece) {
     const int np = hi / kPiece - lo / kPiece + 1;
     const uint32_t base = atomicAdd(plan.ctrs + 2, (uint32_t)np);

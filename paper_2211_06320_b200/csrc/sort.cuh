@@ -1,6 +1,7 @@
 // sort.cuh -- work bucketing by a lambda-monotone key (sort.cu).
 #pragma once
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 namespace fpe {
@@ -42,7 +43,24 @@ struct GroupDesc {
   int32_t lo, hi;   // union of the windows
   uint32_t slot;    // first scratch slot (multi-piece groups evaluated in parallel)
   int32_t npieces;  // > 1: the pieces lo/kPiece .. hi/kPiece are separate work items
+  int32_t mma_p0;   // first kPiece-aligned piece some point covers whole (tensor cores, k_eval_mma)
+  int32_t mma_np;   // number of such pieces (0: none, or the DMMA scratch was exhausted)
+  uint32_t mma_slot;  // their first slot in the DMMA scratch
+  int32_t pad;
 };
+
+// Tensor-core coverage (k_eval_mma): point (window [wl, wr] relative to k_min, z = x + iy) has piece p
+// evaluated on the FP64 tensor cores iff its window covers the whole kPiece-aligned piece and
+// 2^-3 <= max(|x|, |y|) < 2^3 (the range of the chunk powers u^i <= z^240, w = z^256).  A property of
+// the point alone, so every point's arithmetic is independent of the batch.
+__host__ __device__ __forceinline__ bool mma_covers(int wl, int wr, double x, double y, int p) {
+  if (!(wl <= wr) || wl > p * kPiece || wr < p * kPiece + kPiece - 1) return false;
+  const double m = fmax(fabs(x), fabs(y));
+  long long b;
+  memcpy(&b, &m, sizeof(b));
+  const int e = (int)((b >> 52) & 0x7ff) - 1023;
+  return e >= -3 && e <= 2;
+}
 
 // Planner outputs (k_plan) consumed by the evaluator.
 struct Plan {
@@ -54,6 +72,12 @@ struct Plan {
   uint32_t cap;           // scratch slots
   int gsize;              // points per group (32*NP)
   uint32_t ngroups;       // ceil(n / gsize)
+  // tensor-core pieces (complex fp64 coefficients only)
+  int mma_on;             // 1: plan them
+  uint2* mma_items;       // [mma_cap] (group, piece)
+  uint32_t* mma_ctrs;     // [0] slots reserved, [1] items fetched
+  double2* mma_scratch;   // [mma_cap][gsize] partial sums of covered points, origin = piece start
+  uint32_t mma_cap;
 };
 
 // bucket starts (k_bucket_scan), records and points in bucket order (k_bucket_scatter), and the work plan
