@@ -721,8 +721,14 @@ __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(l
 #ifndef FPE_NO_MMA_ITEMS
 #define FPE_NO_MMA_ITEMS 0   // experiments: 1 keeps every piece on the vector Horner
 #endif
+#ifndef FPE_MMA_MINB
+#define FPE_MMA_MINB 2     // CTAs per SM the register budget is sized for (16 warps: 7.16 vs 7.35 ms with 1)
+#endif
+#ifndef FPE_MMA_STAGES
+#define FPE_MMA_STAGES 4
+#endif
 constexpr int kMmaWarps = 8;
-constexpr int kMmaStages = 4;
+constexpr int kMmaStages = FPE_MMA_STAGES;
 constexpr int kPieceChunks = kPiece / kChunk;
 
 __device__ __forceinline__ void cmul(double& r, double& i, double ar, double ai, double br, double bi) {
@@ -741,7 +747,7 @@ __device__ __forceinline__ void dd_sqr_c(xc_t& v) {
   v.hr = r.hi; v.er = r.lo; v.hi = i.hi; v.ei = i.lo;
 }
 
-__global__ void __launch_bounds__(kMmaWarps * 32, 1) k_eval_mma(long long n, const double2* __restrict__ coef,
+__global__ void __launch_bounds__(kMmaWarps * 32, FPE_MMA_MINB) k_eval_mma(long long n, const double2* __restrict__ coef,
                                                                 int kmin, const PtRec* __restrict__ rec, Plan plan) {
   __shared__ __align__(128) double2 ring[kMmaStages][kChunk];
   __shared__ uint64_t full[kMmaStages], empty[kMmaStages];
