@@ -835,10 +835,19 @@ __global__ void __launch_bounds__(kMmaWarps * 32, FPE_MMA_MINB) k_eval_mma(long 
 #pragma unroll
       for (int e = 0; e < 4; ++e) { cr[t][e] = 0.0; ci[t][e] = 0.0; }
     }
+    const bool busy = __any_sync(0xffffffffu, act);   // a warp without covering points only keeps the ring going
     for (int k = 0; k < kPieceChunks; ++k) {
       const int s = (int)(t_seq % kMmaStages);
       mbar_wait(full + s, (t_seq / kMmaStages) & 1u);
       const double2* cb = ring[s];
+      if (!busy) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+        ++t_seq;
+        if (tid == 0 && k + kMmaStages < kPieceChunks) issue(q0 - k - kMmaStages);
+        __syncwarp();
+        continue;
+      }
       if (k) {
 #pragma unroll
         for (int t = 0; t < 2; ++t)
