@@ -16,6 +16,7 @@ RAW_KEYS = [
     "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
     "launch__block_size", "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 
 
