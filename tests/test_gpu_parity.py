@@ -515,3 +515,22 @@ def test_analyse_intervals(fpe, worked):
                 j = np.flatnonzero((iv["lam_lo"] < lam) & (lam < iv["lam_hi"]))
                 if len(j):
                     assert [iv["l"][j[0]], iv["r"][j[0]]] == band[key]
+
+
+@pytest.mark.parametrize("real_points", [False, True])
+def test_tensor_core_pieces_and_overflow(fpe, real_points):
+    """Points near |z| = 1 on cfg3's polynomial have windows of 10^5 coefficients: most pieces are covered
+    whole and go to k_eval_mma; 400 points (4 groups) request more DMMA items than the small batch's
+    scratch holds (64), so some groups fall back to the vector Horner.  Indexing exact, values within
+    2^-45 S, against the oracle; complex and real points."""
+    a = workloads.coefficients(3)
+    P = oracle.OraclePoly(a)
+    rng = np.random.default_rng(61)
+    n = 400
+    r = np.exp2(rng.uniform(-2.0 ** -12, 2.0 ** -12, n))
+    pts = r * rng.choice([-1.0, 1.0], n) if real_points else r * np.exp(1j * rng.uniform(0, 2 * np.pi, n))
+    poly = fpe.precondition(a)
+    out = gpu_eval(poly, pts)
+    cls = check_indexing(P, pts, out["diag"])
+    assert np.median(cls["K"]) > 3 * 16384   # long windows: several whole pieces per point
+    _values_ok(P, a, pts, out, np.arange(0, n, 8), TOL64, cls)
