@@ -15,7 +15,10 @@ inline long long pts_per_cta(long long n) {
   p = (p + 1023) / 1024 * 1024;
   return p < 1024 ? 1024 : p;
 }
-constexpr int kPiece = 16384;                   // absolute coefficient pieces: a window is cut at multiples
+#ifndef FPE_KPIECE
+#define FPE_KPIECE 16384
+#endif
+constexpr int kPiece = FPE_KPIECE;                  // absolute coefficient pieces: a window is cut at multiples
                                                 // of kPiece (relative to k_min) and the piece partials are
                                                 // combined top-down, so results never depend on the batch
 
