@@ -18,7 +18,10 @@
  *    max(|re|,|im|) of the mantissa in [1/2, 1) (or all zero with exp = 0),
  *    because z^d overflows any hardware float.
  *  - Results are a pure function of (handle, z): bitwise independent of the
- *    batch, its order, and the sharding across GPUs.
+ *    batch, its order, and the sharding across GPUs.  One exception: a batch that asks
+ *    for more whole-piece tensor-core evaluations than its workspace holds (n/512 pieces
+ *    of 16384 coefficients) evaluates the excess on the vector Horner, which agrees
+ *    within the tolerance but not bit for bit.
  */
 #ifndef FPE_H_
 #define FPE_H_
