@@ -23,6 +23,9 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 #include "fpe_internal.h"
 #include "fpe_math.cuh"
 #include "fpe_polar.cuh"
@@ -1139,6 +1142,26 @@ size_t tiled_ws_bytes(long long n) {
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
 }
 
+// Persistent grids: resident CTAs per SM x SMs, per (kernel, device), computed once; the dynamic
+// shared-memory opt-in is set per device before the first launch there.
+static int persistent_grid(const void* fn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_pair(fn, dev);
+  const auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int g = max(1, per_sm) * sms;
+  cache[key] = g;
+  return g;
+}
+
 template <int CK>
 static size_t eval_smem() {
   return ring_bytes<CK>() + kWarps * kStages * sizeof(uint64_t);
@@ -1146,16 +1169,8 @@ static size_t eval_smem() {
 
 template <int PK, int CK, int OK, int NP>
 static int launch_eval_tiled_t(long long n, const PolyDev& P, PtRec* rec, const Plan& plan, cudaStream_t s) {
-  static int grid = 0;
   const size_t smem = eval_smem<CK>();
-  if (grid == 0) {
-    cudaFuncSetAttribute(k_eval_tiled<PK, CK, OK, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_tiled<PK, CK, OK, NP>, kWarps * 32, smem);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid = max(1, per_sm) * sms;
-  }
+  const int grid = persistent_grid(reinterpret_cast<const void*>(k_eval_tiled<PK, CK, OK, NP>), kWarps * 32, smem);
   k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(n, P, rec, plan);
   return 1;
 }
@@ -1190,16 +1205,8 @@ template <int PK, int CK>
 static void launch_horner_tiled_t(const void* pts, long long n, const PolyDev& P, uint32_t* ctr, void* vals,
                                   long long* exps, cudaStream_t s) {
   constexpr int NP = NPFor<PK, CK>::value, OK = NPFor<PK, CK>::OK;
-  static int grid = 0;
   const size_t smem = eval_smem<CK>();
-  if (grid == 0) {
-    cudaFuncSetAttribute(k_horner_tiled<PK, CK, OK, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_horner_tiled<PK, CK, OK, NP>, kWarps * 32, smem);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid = max(1, per_sm) * sms;
-  }
+  const int grid = persistent_grid(reinterpret_cast<const void*>(k_horner_tiled<PK, CK, OK, NP>), kWarps * 32, smem);
   cudaMemsetAsync(ctr, 0, sizeof(uint32_t), s);
   k_horner_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(pts, n, P, ctr, vals, exps);
 }
@@ -1261,14 +1268,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   st.mark("bucket");
   int lm = 0;
   if (plan.mma_on) {
-    static int grid_mma = 0;
-    if (grid_mma == 0) {
-      int per_sm = 0, dev = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_mma, kMmaWarps * 32, 0);
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      grid_mma = max(1, per_sm) * sms;
-    }
+    const int grid_mma = persistent_grid(reinterpret_cast<const void*>(k_eval_mma), kMmaWarps * 32, 0);
     k_eval_mma<<<grid_mma, kMmaWarps * 32, 0, s>>>(n, static_cast<const double2*>(P.coef), (int)P.k_min, rec, plan);
     st.mark("eval_mma");
     lm = 1;
