@@ -211,6 +211,8 @@ fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t
  * exponents out), staging through device memory owned by the handle; host<->device copies
  * are pipelined with the kernels in chunks.  Pinned host memory gives full copy bandwidth.
  * Synchronous: returns when the host outputs are written.  Not thread-safe per handle.
+ * `stream` is unused: the call runs on the handle's own streams (one copy stream each way, one
+ * kernel stream per staging slot) so that consecutive chunks overlap.
  */
 fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_dt,
                              int64_t n_points, void* values_host, int64_t* exps_host,
