@@ -432,7 +432,9 @@ def run_fpe(args):
                                      f"and writes its 32-B results over them ({64 * n / 1e9:.2f} GB); the path's "
                                      f"algorithmic bytes are 40 B/pt = {40 * n / 1e9:.2f} GB (points in, values and "
                                      "exponents out, the latter written by k_unsort)",
-                     "peak_note": "fp64 FMA: 148 SM x 64 lanes x 1.965 GHz x 2 (guide unit counts/clock)",
+                     "peak_note": "fp64 FMA: 148 SM x 64 lanes x 1.965 GHz x 2 (guide unit counts/clock); the FP64 "
+                                  "tensor cores (DMMA, k_eval_mma) run on the same datapath: 18.5T FMA/s measured "
+                                  "(profiles/r01_dmma_vs_dfma.json)",
                      "algorithmic_fma_per_launch": fma_total, "kernel_ms": dom_ms, "stages_ms": stages},
         "cpu_baseline": cpu,
         "e2e": e2e,
