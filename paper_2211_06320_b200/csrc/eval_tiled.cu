@@ -121,16 +121,10 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
       }
       if (hard) atomicAdd(hard_ctr, 1ull);
     }
-    // one shared-memory atomic per distinct bucket in the warp
-    // one shared-memory atomic per distinct bucket in the warp; every point keeps its rank inside its
-    // (CTA, bucket) slice, so the scatter needs no atomics
-    const uint32_t c = ok ? key >> (24 - kCoarseBits) : 0xffffffffu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, c);
-    const int leader = __ffs(peers) - 1;
-    uint32_t r0 = 0;
-    if (ok && lane == leader) r0 = atomicAdd(&hist[c], (uint32_t)__popc(peers));
-    r0 = __shfl_sync(0xffffffffu, r0, leader);
-    if (ok) keys[2 * i + 1] = r0 + __popc(peers & ((1u << lane) - 1));
+    // every point keeps its rank inside its (CTA, bucket) slice, so the scatter needs no atomics (one
+    // shared-memory atomic per point: buckets rarely repeat within a warp, and warp-aggregating them
+    // with __match_any_sync cost more than it saved -- 1.70 vs 1.59 ms)
+    if (ok) keys[2 * i + 1] = atomicAdd(&hist[key >> (24 - kCoarseBits)], 1u);
   }
   __syncthreads();
   // claim this CTA's slice of every bucket
