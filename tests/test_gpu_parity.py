@@ -534,3 +534,27 @@ def test_tensor_core_pieces_and_overflow(fpe, real_points):
     cls = check_indexing(P, pts, out["diag"])
     assert np.median(cls["K"]) > 3 * 16384   # long windows: several whole pieces per point
     _values_ok(P, a, pts, out, np.arange(0, n, 8), TOL64, cls)
+
+
+@pytest.mark.parametrize("coef_kind,pt_kind", [("r", "r"), ("r", "c"), ("c", "r"), ("c", "c")])
+@pytest.mark.parametrize("fp32", [False, True])
+def test_dtype_combinations(fpe, coef_kind, pt_kind, fp32):
+    """Every (coefficient, point) dtype pair the evaluator instantiates (real/complex x real/complex, fp64
+    and fp32): indexing exact, values within the dtype's tolerance, on a polynomial with zero
+    coefficients and a 2^+-40 dynamic range and points spanning |z| in [2^-6, 2^6] with a cluster at 1."""
+    rng = np.random.default_rng(81 + 2 * fp32)
+    d = 3000
+    a = rng.normal(size=d + 1) * np.exp2(rng.uniform(-40, 0, d + 1))
+    a[rng.random(d + 1) < 0.3] = 0.0
+    if coef_kind == "c":
+        a = a * np.exp(1j * rng.uniform(0, 2 * np.pi, d + 1))
+    n = 4000
+    r = np.concatenate([np.exp2(rng.uniform(-6, 6, n // 2)), np.exp2(rng.uniform(-2.0 ** -8, 2.0 ** -8, n // 2))])
+    pts = r * (np.exp(1j * rng.uniform(0, 2 * np.pi, n)) if pt_kind == "c" else rng.choice([-1.0, 1.0], n))
+    if fp32:
+        a, pts = workloads.to_fp32(a), workloads.to_fp32(pts)
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    out = gpu_eval(poly, pts)
+    cls = check_indexing(P, pts, out["diag"])
+    _values_ok(P, a, pts, out, np.arange(0, n, 4), TOL32 if fp32 else TOL64, cls)
