@@ -558,3 +558,28 @@ def test_dtype_combinations(fpe, coef_kind, pt_kind, fp32):
     out = gpu_eval(poly, pts)
     cls = check_indexing(P, pts, out["diag"])
     _values_ok(P, a, pts, out, np.arange(0, n, 4), TOL32 if fp32 else TOL64, cls)
+
+
+def test_special_points_fp32(fpe):
+    """Single-precision points at the edges of their format (subnormal, near FLT_MAX, exact powers of two,
+    within one ulp of |z| = 1, zero, NaN/inf): indexing exact, values within 2^-16 S, z = 0 gives a_0."""
+    a = workloads.to_fp32(workloads.coefficients(1, d=200))
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    f = np.float32
+    one_up, one_dn = np.nextafter(f(1), f(2)), np.nextafter(f(1), f(0))
+    sp = [0, 1, -1, 1j, -1j, 2, 0.5j, np.finfo(f).tiny, f(1e-45), np.finfo(f).max / 2, complex(3e38, 3e38),
+          complex(one_up, 0), complex(one_dn, 0), complex(one_dn, f(1e-4)), complex(0.6, 0.8), complex(1e-38, 1e-40)]
+    rng = np.random.default_rng(91)
+    for _ in range(300):
+        t = rng.uniform(0, 2 * np.pi)
+        sp.append(np.exp(1j * t) * (1 + rng.choice([-1, 1]) * 2.0 ** -rng.integers(1, 24)))
+    pts = np.array(sp, dtype=np.complex64)
+    out = gpu_eval(poly, pts)
+    cls = check_indexing(P, pts, out["diag"])
+    nz = np.flatnonzero(pts != 0)
+    _values_ok(P, a, pts, out, nz, TOL32, cls)
+    assert out["v"][0] * 2.0 ** out["e"][0] == a[0]
+    nanpts = np.array([complex(np.nan, 0), complex(np.inf, 1)], dtype=np.complex64)
+    o2 = gpu_eval(poly, nanpts)
+    assert np.all(np.isnan(o2["v"].real)) and np.all(o2["diag"]["region"] == -1)
