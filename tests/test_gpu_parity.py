@@ -583,3 +583,19 @@ def test_special_points_fp32(fpe):
     nanpts = np.array([complex(np.nan, 0), complex(np.inf, 1)], dtype=np.complex64)
     o2 = gpu_eval(poly, nanpts)
     assert np.all(np.isnan(o2["v"].real)) and np.all(o2["diag"]["region"] == -1)
+
+
+def test_tensor_core_pieces_with_k_min(fpe):
+    """Long windows on a polynomial whose first 1000 coefficients are zero (k_min = 1000; pieces and
+    chunks are relative to k_min): indexing exact, values within 2^-45 S."""
+    a = np.concatenate([np.zeros(1000, np.complex128), workloads.coefficients(3)[: (1 << 18)]])
+    P = oracle.OraclePoly(a)
+    assert P.k_min == 1000
+    rng = np.random.default_rng(62)
+    n = 1000
+    pts = np.exp2(rng.uniform(-2.0 ** -14, 2.0 ** -14, n)) * np.exp(1j * rng.uniform(0, 2 * np.pi, n))
+    poly = fpe.precondition(a)
+    out = gpu_eval(poly, pts)
+    cls = check_indexing(P, pts, out["diag"])
+    assert np.median(cls["K"]) > 2 * 16384
+    _values_ok(P, a, pts, out, np.arange(0, n, 10), TOL64, cls)
