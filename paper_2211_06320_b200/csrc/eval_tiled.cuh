@@ -2,6 +2,11 @@
 #pragma once
 #include <cuda_runtime.h>
 #include "fpe_internal.h"
+#include "sort.cuh"
+
+#ifndef FPE_NO_MMA_ITEMS
+#define FPE_NO_MMA_ITEMS 0   // experiments: 1 keeps every piece on the vector Horner
+#endif
 
 namespace fpe {
 constexpr int kChunk = kCoefPad;   // coefficients per TMA bulk copy / ring stage (dense array padded to this)
@@ -14,4 +19,6 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
 // full Horner (dense handles) with the streaming evaluator; ctr: one device uint32 of scratch
 bool run_horner_tiled(int pk, const void* pts, long long n, const PolyDev& P, uint32_t* ctr, void* vals,
                       long long* exps, cudaStream_t s);
+// whole kPiece pieces some point covers, on the FP64 tensor cores (eval_mma.cu); before the vector evaluator
+int launch_eval_mma(long long n, const PolyDev& P, const PtRec* rec, const Plan& plan, cudaStream_t s);
 }  // namespace fpe
