@@ -345,6 +345,8 @@ def run_fpe(args):
     D = fpe.diag_fields(dg)
     fma_total = algorithmic_fma(D, cplx)
     meanK = float(D["kept"].double().mean())
+    kq = torch.quantile(D["kept"].double()[:: max(1, D["kept"].numel() // (1 << 22))], torch.tensor([0.5, 0.99], dtype=torch.float64, device=D["kept"].device))
+    kept_stats = {"median": float(kq[0]), "p99": float(kq[1]), "max": int(D["kept"].max())}
     hard = int(D["hard"].sum())
     del dg, D
     torch.cuda.empty_cache()
@@ -423,6 +425,7 @@ def run_fpe(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": c["name"], "points_per_gpu": n, "degree": c["d"], "parallelism": f"points x{world}",
                    "l2": "inputs (1 GiB/rank) larger than L2; no flush", "mean_kept_terms": meanK,
+                   "kept_terms": kept_stats,
                    "hard_lambdas": hard},
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak,
