@@ -17,6 +17,7 @@ RAW_KEYS = [
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
     "launch__block_size", "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second",
     "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "derived__sm__sass_thread_inst_executed_op_dfma_pred_on_x2", "sm__ops_path_tensor_src_fp64.sum",
 ]
 
 
