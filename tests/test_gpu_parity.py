@@ -599,3 +599,30 @@ def test_tensor_core_pieces_with_k_min(fpe):
     cls = check_indexing(P, pts, out["diag"])
     assert np.median(cls["K"]) > 2 * 16384
     _values_ok(P, a, pts, out, np.arange(0, n, 10), TOL64, cls)
+
+
+def test_batch_slicing_above_2_28(fpe):
+    """fpe_evaluate slices batches above 2^28 points (the bucketing's index range): 2^28 + 4097 points,
+    the ones around the slice boundary and a random sample checked against the oracle, and the slice
+    boundary invisible in the results (the same points evaluated alone give the same bits)."""
+    a = workloads.coefficients(1)
+    P = oracle.OraclePoly(a)
+    poly = fpe.precondition(a)
+    n = (1 << 28) + 4097
+    g = torch.Generator(device="cuda").manual_seed(5)
+    t = torch.complex(torch.randn(n, device="cuda", dtype=torch.float64, generator=g),
+                      torch.randn(n, device="cuda", dtype=torch.float64, generator=g))
+    v, e, dg = poly.evaluate(t, exps=True, diag=True)
+    idx = np.concatenate([np.arange((1 << 28) - 64, (1 << 28) + 64), np.arange(n - 8, n),
+                          workloads.sample_indices(n, 2048, salt=7)])
+    idx = np.unique(idx)
+    it = torch.from_numpy(idx).cuda()
+    pts = t[it].cpu().numpy()
+    D = {k: x[it].cpu().numpy() for k, x in fpe.diag_fields(dg).items()}
+    out = {"v": v[it].cpu().numpy(), "e": e[it].cpu().numpy()}
+    del v, e, dg
+    torch.cuda.empty_cache()
+    cls = check_indexing(P, pts, D)
+    _values_ok(P, a, pts, out, np.arange(len(idx)), TOL64, cls)
+    alone = gpu_eval(poly, pts)
+    assert np.array_equal(alone["v"], out["v"]) and np.array_equal(alone["e"], out["e"])
