@@ -202,9 +202,21 @@ def test_horner_context(fpe):
         assert np.all(err <= tol), (cfg, err.max())
 
 
-def test_evaluate_host_matches_device(fpe):
-    a = workloads.coefficients(1)
-    pts = workloads.points(1)
+@pytest.mark.parametrize("kind", ["c64", "r64", "c32", "long"])
+def test_evaluate_host_matches_device(fpe, kind):
+    """fpe_evaluate_host (pipelined host buffers, several chunks and kernel streams) gives the device
+    path's bits, for complex / real / fp32 points and with tensor-core pieces (cfg3; the DMMA scratch
+    does not overflow at this distribution, see fpe.h on the one exception)."""
+    if kind == "long":   # cfg3's polynomial and point distribution: tensor-core pieces in every chunk
+        a = workloads.coefficients(3)
+        pts = workloads.points(3, (1 << 22) + (1 << 21) + 123)   # three chunks of the host pipeline
+    else:
+        a = workloads.coefficients(1)
+        pts = workloads.points(1)
+        if kind == "r64":
+            a, pts = a.real.copy(), pts.real.copy()
+        elif kind == "c32":
+            a, pts = workloads.to_fp32(a), workloads.to_fp32(pts)
     poly = fpe.precondition(a)
     out = gpu_eval(poly, pts, diag=False)
     hv, he = poly.evaluate_host(pts)
