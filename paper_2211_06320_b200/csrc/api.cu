@@ -585,6 +585,14 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   FPE_CUDA(cudaMemsetAsync(h->dstats, 0, sizeof(unsigned long long), s_in));   // before every chunk (events)
   auto ev = [&](int slot, int kind) { return static_cast<cudaEvent_t>(h->st_events[slot * 3 + kind]); };
   long long launches = 0;
+  static const bool trace = std::getenv("FPE_HOST_TRACE") != nullptr;   // debugging: per-chunk timeline
+  std::vector<cudaEvent_t> tev;
+  cudaEvent_t t0 = nullptr;
+  if (trace) { cudaEventCreate(&t0); cudaEventRecord(t0, s_in); }
+  auto mark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, st); tev.push_back(e);
+  };
   long long next = std::min<long long>(chunk, 1ll << lg_first);
   for (long long off = 0, c = 0, m = 0; off < n_points; off += m, ++c) {
     m = std::min(next, n_points - off);
@@ -597,20 +605,37 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
     long long* de = reinterpret_cast<long long*>(base + al(chunk * in_sz) + al(chunk * out_sz));
     void* wsp = base + al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8);
     if (c >= kSlots) FPE_CUDA(cudaStreamWaitEvent(s_in, ev(b, 2), 0));   // slot's previous results copied out
+    mark(s_in);
     FPE_CUDA(cudaMemcpyAsync(dp, static_cast<const char*>(points_host) + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
+    mark(s_in);
     FPE_CUDA(cudaEventRecord(ev(b, 0), s_in));
     FPE_CUDA(cudaStreamWaitEvent(s_ev, ev(b, 0), 0));
+    mark(s_ev);
     fpe_status est = evaluate_impl(h, dp, pt_dt, m, dv, exps_host ? reinterpret_cast<int64_t*>(de) : nullptr, nullptr,
                                    wsp, ws_bytes_for(chunk), s_ev, false);
+    mark(s_ev);
     if (est != FPE_OK) return est;
     launches += h->last_launches;
     FPE_CUDA(cudaEventRecord(ev(b, 1), s_ev));
     FPE_CUDA(cudaStreamWaitEvent(s_out, ev(b, 1), 0));
+    mark(s_out);
     FPE_CUDA(cudaMemcpyAsync(static_cast<char*>(values_host) + off * out_sz, dv, m * out_sz, cudaMemcpyDeviceToHost, s_out));
     if (exps_host) FPE_CUDA(cudaMemcpyAsync(exps_host + off, de, m * 8, cudaMemcpyDeviceToHost, s_out));
+    mark(s_out);
     FPE_CUDA(cudaEventRecord(ev(b, 2), s_out));
   }
   FPE_CUDA(cudaStreamSynchronize(s_out));
+  if (trace) {   // chunk: h2d [start, end], kernels [start, end], d2h [start, end] in ms from the call
+    cudaDeviceSynchronize();
+    for (size_t k = 0; k + 5 < tev.size() + 0; k += 6) {
+      float v[6];
+      for (int q = 0; q < 6; ++q) cudaEventElapsedTime(&v[q], t0, tev[k + q]);
+      std::fprintf(stderr, "chunk %zu: h2d %.2f-%.2f  eval %.2f-%.2f  d2h %.2f-%.2f\n", k / 6, v[0], v[1], v[2], v[3],
+                   v[4], v[5]);
+    }
+    for (auto e : tev) cudaEventDestroy(e);
+    cudaEventDestroy(t0);
+  }
   h->last_launches = launches;
   return FPE_OK;
 }
