@@ -494,6 +494,120 @@ void or_horner(const double* a, int64_t kmin, int64_t kmax, int is_complex,
     }
 }
 
+/* Reference P(z) by full double-double Horner ("P_ref by full double-double Horner
+ * with an exponent counter"), the plain definition P(z) = sum_k a_k z^k evaluated as
+ * b <- b z + a_k for k = k_max .. k_min, then times z^k_min.  Each component of b is an unevaluated sum
+ * hi + lo of two doubles (Dekker / Knuth error-free transformations: ~106-bit significand, relative error
+ * ~2^-104 per step); b's value is (hi + lo) 2^E with E an int64, renormalised after every step so that
+ * the larger component's hi lies in [1/2, 1); z = w 2^ez with the larger of |Re w|, |Im w| in [1/2, 1).
+ * A faster plain reference than the binary128 or_horner for the full-size value checks (d up to 2^22). */
+typedef struct { double hi, lo; } or_dd;
+static or_dd dd_two_sum(double a, double b)
+{
+    double s = a + b, bb = s - a;
+    or_dd r = { s, (a - (s - bb)) + (b - bb) };
+    return r;
+}
+static or_dd dd_add(or_dd a, or_dd b)   /* accurate double-double addition */
+{
+    or_dd s = dd_two_sum(a.hi, b.hi), t = dd_two_sum(a.lo, b.lo);
+    s.lo += t.hi;
+    s = dd_two_sum(s.hi, s.lo);
+    s.lo += t.lo;
+    return dd_two_sum(s.hi, s.lo);
+}
+static or_dd dd_mul_d(or_dd a, double b)
+{
+    double p = a.hi * b;
+    double e = fma(a.hi, b, -p) + a.lo * b;
+    return dd_two_sum(p, e);
+}
+static or_dd dd_neg(or_dd a) { or_dd r = { -a.hi, -a.lo }; return r; }
+static or_dd dd_ldexp(or_dd a, int64_t e)
+{
+    int s = e > 3000 ? 3000 : (e < -3000 ? -3000 : (int)e);
+    or_dd r = { ldexp(a.hi, s), ldexp(a.lo, s) };
+    return r;
+}
+
+void or_horner_dd(const double* a, int64_t kmin, int64_t kmax, int is_complex,
+                  const double* pts, int64_t npts, double* out, int64_t* exps)
+{
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < npts; ++q) {
+        const double zr = is_complex ? pts[2 * q] : pts[q], zi = is_complex ? pts[2 * q + 1] : 0.0;
+        or_dd br = { 0, 0 }, bi = { 0, 0 };
+        int64_t E = 0;
+        if (zr == 0 && zi == 0) {
+            if (kmin == 0) { br.hi = is_complex ? a[0] : a[0]; bi.hi = is_complex ? a[1] : 0.0; }
+            out[4 * q] = br.hi; out[4 * q + 1] = 0; out[4 * q + 2] = bi.hi; out[4 * q + 3] = 0; exps[q] = 0;
+            continue;
+        }
+        int ez;
+        (void)frexp(fabs(zr) > fabs(zi) ? zr : zi, &ez);
+        const double wr = ldexp(zr, -ez), wi = ldexp(zi, -ez);   /* exact */
+        for (int64_t k = kmax; k >= kmin; --k) {
+            /* b <- b w (value times 2^ez) */
+            or_dd nr = dd_add(dd_mul_d(br, wr), dd_neg(dd_mul_d(bi, wi)));
+            or_dd ni = dd_add(dd_mul_d(br, wi), dd_mul_d(bi, wr));
+            br = nr; bi = ni; E += ez;
+            /* + a_k: align the two exponents (the smaller operand may underflow: it is then below the
+             * larger one's rounding) */
+            const double ar = is_complex ? a[2 * k] : a[k], ai = is_complex ? a[2 * k + 1] : 0.0;
+            if (ar != 0 || ai != 0) {
+                int ea;
+                (void)frexp(fabs(ar) > fabs(ai) ? ar : ai, &ea);
+                const int bz = (br.hi == 0 && bi.hi == 0);
+                int eb = 0;
+                if (!bz) (void)frexp(fabs(br.hi) > fabs(bi.hi) ? br.hi : bi.hi, &eb);
+                if (bz || (int64_t)ea > E + eb) {      /* the coefficient is larger: work at its scale */
+                    br = dd_ldexp(br, E - ea); bi = dd_ldexp(bi, E - ea); E = ea;
+                }
+                or_dd xr = { ldexp(ar, (int)(ea - E > -3000 ? ea - E : -3000) - ea), 0 };
+                or_dd xi = { ldexp(ai, (int)(ea - E > -3000 ? ea - E : -3000) - ea), 0 };
+                br = dd_add(br, xr); bi = dd_add(bi, xi);
+            }
+            /* renormalise: the larger component's hi in [1/2, 1) */
+            const double m = fabs(br.hi) > fabs(bi.hi) ? br.hi : bi.hi;
+            if (m != 0) {
+                int e;
+                (void)frexp(m, &e);
+                br = dd_ldexp(br, -e); bi = dd_ldexp(bi, -e); E += e;
+            } else {
+                E = 0;
+            }
+        }
+        /* times z^k_min: (w 2^ez)^k_min by binary powering in double-double */
+        if (kmin > 0) {
+            or_dd pr = { 1, 0 }, pi = { 0, 0 }, qr = { wr, 0 }, qi = { wi, 0 };
+            int64_t pE = 0, qE = ez, n = kmin;
+            while (n > 0) {
+                if (n & 1) {
+                    or_dd tr = dd_add(dd_mul_d(pr, qr.hi), dd_add(dd_mul_d(pr, qr.lo), dd_neg(dd_add(dd_mul_d(pi, qi.hi), dd_mul_d(pi, qi.lo)))));
+                    or_dd ti = dd_add(dd_add(dd_mul_d(pr, qi.hi), dd_mul_d(pr, qi.lo)), dd_add(dd_mul_d(pi, qr.hi), dd_mul_d(pi, qr.lo)));
+                    pr = tr; pi = ti; pE += qE;
+                }
+                n >>= 1;
+                if (n) {
+                    or_dd tr = dd_add(dd_add(dd_mul_d(qr, qr.hi), dd_mul_d(qr, qr.lo)), dd_neg(dd_add(dd_mul_d(qi, qi.hi), dd_mul_d(qi, qi.lo))));
+                    or_dd ti = dd_add(dd_add(dd_mul_d(qr, qi.hi), dd_mul_d(qr, qi.lo)), dd_add(dd_mul_d(qi, qr.hi), dd_mul_d(qi, qr.lo)));
+                    qr = tr; qi = ti; qE *= 2;
+                }
+                int e;
+                double mp_ = fabs(pr.hi) > fabs(pi.hi) ? pr.hi : pi.hi;
+                (void)frexp(mp_, &e); pr = dd_ldexp(pr, -e); pi = dd_ldexp(pi, -e); pE += e;
+                double mq = fabs(qr.hi) > fabs(qi.hi) ? qr.hi : qi.hi;
+                (void)frexp(mq, &e); qr = dd_ldexp(qr, -e); qi = dd_ldexp(qi, -e); qE += e;
+            }
+            or_dd tr = dd_add(dd_add(dd_mul_d(br, pr.hi), dd_mul_d(br, pr.lo)), dd_neg(dd_add(dd_mul_d(bi, pi.hi), dd_mul_d(bi, pi.lo))));
+            or_dd ti = dd_add(dd_add(dd_mul_d(br, pi.hi), dd_mul_d(br, pi.lo)), dd_add(dd_mul_d(bi, pr.hi), dd_mul_d(bi, pr.lo)));
+            br = tr; bi = ti; E += pE;
+        }
+        out[4 * q] = br.hi; out[4 * q + 1] = br.lo; out[4 * q + 2] = bi.hi; out[4 * q + 3] = bi.lo;
+        exps[q] = E;
+    }
+}
+
 /* Reference P(z) as the plain sum of monomials a_k z^k (each power by binary
  * powering) over an explicit list of nonzero terms (sparse polynomials). */
 void or_direct_sum(const int64_t* idx, const double* vals, int64_t nnz, int is_complex,

@@ -51,6 +51,7 @@ def lib():
             L.or_classify_lambda.restype = None
             L.or_fpe_eval.argtypes = [P, P, C.c_int, P, i64, P, P, P, P]; L.or_fpe_eval.restype = None
             L.or_horner.argtypes = [P, i64, i64, C.c_int, P, i64, P, P]; L.or_horner.restype = None
+            L.or_horner_dd.argtypes = [P, i64, i64, C.c_int, P, i64, P, P]; L.or_horner_dd.restype = None
             L.or_direct_sum.argtypes = [P, P, i64, C.c_int, P, i64, P, P]; L.or_direct_sum.restype = None
             L.or_abs_sum.argtypes = [P, i64, i64, C.c_int, P, i64, P, P]; L.or_abs_sum.restype = None
             L.or_log2abs.argtypes = [P, i64, C.c_int, P]; L.or_log2abs.restype = None
@@ -193,6 +194,15 @@ class OraclePoly:
         out = np.empty(4 * n); e = np.empty(n, np.int64)
         lib().or_horner(_ptr(self._coef_for(cplx)), self.k_min, self.k_max, cplx, _ptr(f), n,
                         _ptr(out), _ptr(e))
+        return _unpack(out, e)
+
+    def horner_dd(self, pts):
+        """Reference P(z) by full double-double Horner with an exponent counter (the plain definition;
+        faster than horner() for the full-size value checks)."""
+        f, cplx, n = self._pts(pts)
+        out = np.empty(4 * n); e = np.empty(n, np.int64)
+        lib().or_horner_dd(_ptr(self._coef_for(cplx)), self.k_min, self.k_max, cplx, _ptr(f), n,
+                           _ptr(out), _ptr(e))
         return _unpack(out, e)
 
     def direct_sum(self, pts):

@@ -147,27 +147,30 @@ def _S(P, z):
     return sum(abs(mp.mpc(complex(c))) * abs(mp.mpc(complex(z))) ** k for k, c in enumerate(P.coeffs))
 
 
-def test_values_closed_forms():
+@pytest.mark.parametrize("method,tol", [("horner", 2.0 ** -100), ("horner_dd", 2.0 ** -90)])
+def test_values_closed_forms(method, tol):
+    """P_ref (binary128 Horner, and the double-double Horner used at full size) against closed forms."""
+    tol = mp.mpf(tol)
     rng = np.random.default_rng(13)
     zs = [complex(*rng.normal(size=2)) * 2.0 ** rng.integers(-3, 3) for _ in range(12)] + [1j, -1.0, 2.0, 0.5j]
     # geometric series sum_{k<=d} z^k = (z^(d+1) - 1)/(z - 1), exact coefficients
     for d in (1, 7, 100, 513):
         P = oracle.OraclePoly(np.ones(d + 1, dtype=np.complex128))
-        H = P.horner(np.array(zs))
+        H = getattr(P, method)(np.array(zs))
         for i, z in enumerate(zs):
             zz = mp.mpc(z.real, z.imag)
             ref = (zz ** (d + 1) - 1) / (zz - 1) if z != 1 else mp.mpf(d + 1)
             S = sum(abs(zz) ** k for k in range(d + 1))
-            assert abs(_to_mpc(H, i) - ref) <= mp.mpf(2) ** -100 * S
+            assert abs(_to_mpc(H, i) - ref) <= tol * S
     # (z - 1)^d with binomial coefficients rounded to fp64 (error <= 2^-53 S)
     for d in (5, 60, 300, 1023):
         c = np.array([float(mp.binomial(d, k)) * (-1) ** (d - k) for k in range(d + 1)])
         P = oracle.OraclePoly(c.astype(np.complex128))
-        H = P.horner(np.array(zs))
+        H = getattr(P, method)(np.array(zs))
         for i, z in enumerate(zs):
             zz = mp.mpc(z.real, z.imag)
             S = (1 + abs(zz)) ** d
-            assert abs(_to_mpc(H, i) - (zz - 1) ** d) <= (mp.mpf(2) ** -53 + mp.mpf(2) ** -100) * S
+            assert abs(_to_mpc(H, i) - (zz - 1) ** d) <= (mp.mpf(2) ** -53 + tol) * S
     # Chebyshev T_n(cos x) = cos(n x), integer coefficients exact in fp64 (n <= 40)
     for n in (3, 17, 40):
         T = [mp.mpf(0)] * (n + 1)
@@ -181,18 +184,19 @@ def test_values_closed_forms():
         coef = np.array(t1 if n >= 1 else t0, dtype=np.float64)
         P = oracle.OraclePoly(coef)
         xs = np.cos(rng.uniform(0, math.pi, size=20))
-        H = P.horner(xs)
+        H = getattr(P, method)(xs)
         for i, x in enumerate(xs):
             ref = mp.cos(n * mp.acos(mp.mpf(x)))
             assert abs(_to_mpc(H, i).real - ref) <= mp.mpf(2) ** -95 * sum(abs(v) for v in coef)
     # monomial a z^n and 1 + z
     P = oracle.OraclePoly(np.array([0] * 1000 + [0.75 - 0.5j]))
-    H = P.horner(np.array([1.5 + 0.25j]))
+    H = getattr(P, method)(np.array([1.5 + 0.25j]))
     ref = mp.mpc(0.75, -0.5) * mp.mpc(1.5, 0.25) ** 1000
-    assert abs(_to_mpc(H, 0) - ref) <= mp.mpf(2) ** -100 * abs(ref)
+    assert abs(_to_mpc(H, 0) - ref) <= tol * abs(ref)
 
 
 def test_horner_vs_mpmath_bruteforce():
+    """Both full-Horner references and the direct sum against mpmath at 300 bits (d <= 32)."""
     rng = np.random.default_rng(14)
     for _ in range(60):
         d = int(rng.integers(1, 33))
@@ -200,13 +204,24 @@ def test_horner_vs_mpmath_bruteforce():
         P = oracle.OraclePoly(a)
         zs = np.array([complex(*rng.normal(size=2)) * 2.0 ** rng.integers(-6, 6) for _ in range(4)])
         H = P.horner(zs)
+        H2 = P.horner_dd(zs)
         D = P.direct_sum(zs)
         for i, z in enumerate(zs):
             zz = mp.mpc(z.real, z.imag)
             ref = sum(mp.mpc(c.real, c.imag) * zz ** k for k, c in enumerate(a))
             S = _S(P, z)
             assert abs(_to_mpc(H, i) - ref) <= mp.mpf(2) ** -100 * S
+            assert abs(_to_mpc(H2, i) - ref) <= mp.mpf(2) ** -98 * S
             assert abs(_to_mpc(D, i) - ref) <= mp.mpf(2) ** -100 * S
+    # real polynomial at real points, zeros at both ends (k_min > 0), huge and tiny |z| (exponent counter)
+    a = np.array([0.0, 0.0, 3.0, -1.5, 0.0, 2.0 ** -600, 7.0, 0.0])
+    P = oracle.OraclePoly(a)
+    xs = np.array([0.75, -2.0 ** 300, 2.0 ** -400, -1.25])
+    H2 = P.horner_dd(xs)
+    for i, x in enumerate(xs):
+        ref = sum(mp.mpf(c) * mp.mpf(x) ** k for k, c in enumerate(a))
+        S = sum(abs(mp.mpf(c)) * abs(mp.mpf(x)) ** k for k, c in enumerate(a))
+        assert abs(_to_mpc(H2, i) - ref) <= mp.mpf(2) ** -98 * S
 
 
 def test_abs_sum():
@@ -218,6 +233,47 @@ def test_abs_sum():
     for i, z in enumerate(zs):
         ref = _S(P, z)
         assert abs(mp.mpf(m[i]) * mp.mpf(2) ** int(e[i]) - ref) <= mp.mpf(2) ** -50 * ref
+
+
+def test_log2_maxterm_vs_mpmath_and_cover():
+    """M(z) = max_k |a_k z^k| (eq:def_prec_loss), which scales the T3 self-check and the confidence test:
+    (1) against mpmath at 300 bits on random polynomials with zeros, ties and a wide dynamic range;
+    (2) against the cover: log2|a_k| lies in [s_k - 1, s_k) (eq:sigma), so log2 M lies in [N - 1, N) with
+    N = hh_i* + lambda hk_i* the sheared cover's top (eq:defN) -- a dropped or shifted
+    term, a wrong sign of k lambda or an index off by one in or_log2_maxterm fails one of them."""
+    rng = np.random.default_rng(19)
+    for fam in range(8):
+        d = int(rng.integers(5, 60))
+        a = rng.normal(size=d + 1) * np.exp2(rng.integers(-40, 40, d + 1).astype(float))
+        if fam % 2:
+            a = a * np.exp(1j * rng.uniform(0, 2 * np.pi, d + 1))
+        a[rng.random(d + 1) < 0.2] = 0
+        a[-1] = a[-1] or 3.0
+        P = oracle.OraclePoly(a)
+        r = np.exp2(rng.uniform(-6, 6, 40))
+        pts = r * np.exp(1j * rng.uniform(0, 2 * np.pi, 40)) if fam % 2 else r * rng.choice([-1.0, 1.0], 40)
+        got = P.log2_maxterm(pts)
+        for i, z in enumerate(pts):
+            zz = mp.mpc(complex(z).real, complex(z).imag)
+            ref = max(mp.log(abs(mp.mpc(complex(c).real, complex(c).imag)) * abs(zz) ** k, 2)
+                      for k, c in enumerate(a) if c != 0)
+            assert abs(got[i] - float(ref)) <= 2.0 ** -40 * max(1.0, abs(float(ref))), (fam, i)
+        c = P.classify(pts)
+        N = P.hh[c["istar"]] + c["lam"] * P.hk[c["istar"]]
+        assert np.all(got >= N - 1 - 1e-9) and np.all(got < N + 1e-9)
+    # cfg1 and cfg3 samples: the cover bound at full degree
+    for cfg in (1, 3):
+        a = workloads.coefficients(cfg) if cfg == 1 else workloads.coefficients(3, d=(1 << 14) - 1)
+        P = oracle.OraclePoly(a)
+        pts = workloads.points(cfg, 300, shard=2)
+        got = P.log2_maxterm(pts)
+        c = P.classify(pts)
+        N = P.hh[c["istar"]] + c["lam"] * P.hk[c["istar"]]
+        assert np.all(got >= N - 1 - 1e-6) and np.all(got < N + 1e-6)
+    # a monomial a z^k: log2 M = log2|a| + k log2|z| exactly
+    P = oracle.OraclePoly(np.array([0.0] * 7 + [5.0]))
+    assert np.allclose(P.log2_maxterm(np.array([2.0, 0.5, 3.0])), [math.log2(5) + 7, math.log2(5) - 7,
+                                                                  math.log2(5) + 7 * math.log2(3)], rtol=0, atol=1e-12)
 
 
 def _truncation_check(P, pts, slack=2.0 ** -20):
