@@ -338,50 +338,6 @@ __device__ __forceinline__ void classify_lambda_vp(const int2* hull, const doubl
   }
 }
 
-// log2 v for v in [1/4, 2) (normal): v = f 2^j, f in [F0, 1.41) by bit manipulation, f r_i = 1 + u with the
-// table of fpe_logtab (|u| < 2^-8.5), ln(1 + u) to u^5 in fp64 (truncation u^6/6 < 2^-53):
-// |error| < 2^-51 absolute.
-__device__ __forceinline__ double log2_fast(double v) {
-  const long long b = __double_as_longlong(v);
-  int j = (int)((b >> 52) & 0x7ff) - 1022;
-  double f = __longlong_as_double((b & 0x000fffffffffffffLL) | 0x3fe0000000000000LL);   // [1/2, 1)
-  if (f < FPE_LOGTAB_F0) { f *= 2.0; j -= 1; }
-  int i = __double2int_rn((f - FPE_LOGTAB_F0) * 256.0);
-  i = max(0, min(i, FPE_LOGTAB_N - 1));
-  const double r = fpe_logtab(i, 0), L0 = fpe_logtab(i, 1);
-  const double u = __fma_rn(f, r, -1.0);
-  double p = __fma_rn(u, 0.2, -0.25);
-  p = __fma_rn(u, p, 1.0 / 3.0);
-  p = __fma_rn(u, p, -0.5);
-  p = __fma_rn(u, p, 1.0);
-  return __fma_rn(__fma_rn(u, p, L0), FPE_INV_LN2_HI, (double)j);
-}
-
-// An enclosure of log2|z| from plain fp64 (finite nonzero z): |z|^2 4^-e in [1/4, 2) to 2^-52 relative,
-// log2_fast to 2^-51, so |error| < 2^-50 + 2^-53 |lambda|; the enclosure is widened to
-// 2^-48 + 2^-50 |lambda|.  Powers of two are taken from the exponent bits (subnormal |z| via frexp).
-__device__ __forceinline__ void lambda_enclosure(double x, double y, bool cplx, double& lo, double& hi, double& mid) {
-  double ax = fabs(x), ay = cplx ? fabs(y) : 0.0;
-  if (ay > ax) { const double t = ax; ax = ay; ay = t; }
-  int e;
-  double xs, ys;
-  if (ax >= 0x1p-1000 && ax < 0x1p1000) {
-    e = (int)((__double_as_longlong(ax) >> 52) & 0x7ff) - 1022;                 // ax = xs 2^e, xs in [1/2, 1)
-    const double sc = __longlong_as_double((long long)(1023 - e) << 52);       // 2^-e, exact
-    xs = ax * sc;
-    ys = ay * sc;
-  } else {
-    e = frexp_exp(ax);
-    xs = ldexp(ax, -e);
-    ys = ldexp(ay, -e);
-  }
-  const double v = __fma_rn(xs, xs, ys * ys);
-  mid = (double)e + 0.5 * log2_fast(v);
-  const double w = __fma_rn(fabs(mid), 0x1p-50, 0x1p-48);
-  lo = mid - w;
-  hi = mid + w;
-}
-
 __device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ a, int n, int key) {
   int lo = 0, hi = n;
   while (lo < hi) { int m = (lo + hi) >> 1; if (__ldg(a + m) < key) lo = m + 1; else hi = m; }

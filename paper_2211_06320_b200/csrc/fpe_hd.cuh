@@ -60,6 +60,15 @@ FPE_HD double fpe_bits2d(long long b) {
   return d;
 #endif
 }
+FPE_HD long long fpe_d2bits(double d) {
+#ifdef __CUDA_ARCH__
+  return __double_as_longlong(d);
+#else
+  long long b;
+  std::memcpy(&b, &d, sizeof b);
+  return b;
+#endif
+}
 FPE_HD int fpe_clzll(long long n) {
 #ifdef __CUDA_ARCH__
   return __clzll(n);

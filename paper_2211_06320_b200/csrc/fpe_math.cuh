@@ -330,4 +330,51 @@ FPE_HD xr_t xr_pow(double x, long long n) {
   return v;
 }
 
+// ------------------------------------------------------------------------------------------
+// The classifier's enclosure of log2|z| (k_classify_bucket fast path; host-tested by
+// tests/test_devmath_host.py against the oracle's correctly rounded lambda).
+// log2 v for v in [1/4, 2) (normal): v = f 2^j, f in [F0, 1.41) by bit manipulation, f r_i = 1 + u with the
+// table of fpe_logtab (|u| < 2^-8.5), ln(1 + u) to u^5 in fp64 (truncation u^6/6 < 2^-53):
+// |error| < 2^-51 absolute.
+FPE_HD double log2_fast(double v) {
+  const long long b = fpe_d2bits(v);
+  int j = (int)((b >> 52) & 0x7ff) - 1022;
+  double f = fpe_bits2d((b & 0x000fffffffffffffLL) | 0x3fe0000000000000LL);   // [1/2, 1)
+  if (f < FPE_LOGTAB_F0) { f *= 2.0; j -= 1; }
+  int i = fpe_d2i_rn((f - FPE_LOGTAB_F0) * 256.0);
+  i = (i < 0 ? 0 : (i > FPE_LOGTAB_N - 1 ? FPE_LOGTAB_N - 1 : i));
+  const double r = fpe_logtab(i, 0), L0 = fpe_logtab(i, 1);
+  const double u = fpe_fma(f, r, -1.0);
+  double p = fpe_fma(u, 0.2, -0.25);
+  p = fpe_fma(u, p, 1.0 / 3.0);
+  p = fpe_fma(u, p, -0.5);
+  p = fpe_fma(u, p, 1.0);
+  return fpe_fma(fpe_fma(u, p, L0), FPE_INV_LN2_HI, (double)j);
+}
+
+// An enclosure of log2|z| from plain fp64 (finite nonzero z): |z|^2 4^-e in [1/4, 2) to 2^-52 relative,
+// log2_fast to 2^-51, so |error| < 2^-50 + 2^-53 |lambda|; the enclosure is widened to
+// 2^-48 + 2^-50 |lambda|.  Powers of two are taken from the exponent bits (subnormal |z| via frexp).
+FPE_HD void lambda_enclosure(double x, double y, bool cplx, double& lo, double& hi, double& mid) {
+  double ax = fabs(x), ay = cplx ? fabs(y) : 0.0;
+  if (ay > ax) { const double t = ax; ax = ay; ay = t; }
+  int e;
+  double xs, ys;
+  if (ax >= 0x1p-1000 && ax < 0x1p1000) {
+    e = (int)((fpe_d2bits(ax) >> 52) & 0x7ff) - 1022;                 // ax = xs 2^e, xs in [1/2, 1)
+    const double sc = fpe_bits2d((long long)(1023 - e) << 52);       // 2^-e, exact
+    xs = ax * sc;
+    ys = ay * sc;
+  } else {
+    e = frexp_exp(ax);
+    xs = ldexp(ax, -e);
+    ys = ldexp(ay, -e);
+  }
+  const double v = fpe_fma(xs, xs, ys * ys);
+  mid = (double)e + 0.5 * log2_fast(v);
+  const double w = fpe_fma(fabs(mid), 0x1p-50, 0x1p-48);
+  lo = mid - w;
+  hi = mid + w;
+}
+
 }  // namespace fpe

@@ -46,3 +46,8 @@ extern "C" void dm_ln1p(const double* u, long long n, double* hl) {
     hl[2 * i] = v.hi; hl[2 * i + 1] = v.lo;
   }
 }
+// the classifier's enclosure of log2|z| (fpe_math.cuh lambda_enclosure): lo, hi, mid per point
+extern "C" void dm_lambda_enclosure(const double* xy, long long n, int cplx, double* lmh) {
+  for (long long i = 0; i < n; ++i)
+    lambda_enclosure(xy[2 * i], xy[2 * i + 1], cplx != 0, lmh[3 * i], lmh[3 * i + 1], lmh[3 * i + 2]);
+}

@@ -4,6 +4,9 @@ host code by tests/native/devmath_host.cu.
 * lambda_fast (quick table-driven log2 + Ziv test, fallback lambda_cr) must equal the
   oracle's correctly rounded lambda bit for bit (DESIGN.md G4; PAPER.md:1131);
 * log2abs_quick / atan2_turns accuracy against mpmath;
+* lambda_enclosure (the classifier's fast path: every window decision is taken on an fp64 enclosure
+  [lo, hi] of log2|z| and must equal the decision at the correctly rounded lambda, so the enclosure
+  must contain it) on 10^6 adversarial points against the oracle's correctly rounded lambda;
 * z^n by the polar route (the library's z^l) within 2^-50 + n 2^-76
   relative of mpmath at 200 bits (2^-49.6 at n = 2^24, the largest degree of the configs).
 """
@@ -36,6 +39,7 @@ def dm():
         getattr(L, f).argtypes = [P, C.c_longlong, C.c_int, P] + ([P] if f != "dm_log2abs" else [])
     L.dm_atan2_turns.argtypes = [P, C.c_longlong, P]
     L.dm_pow_polar.argtypes = [P, P, C.c_longlong, C.c_int, P, P]
+    L.dm_lambda_enclosure.argtypes = [P, C.c_longlong, C.c_int, P]
     return L
 
 
@@ -131,3 +135,45 @@ def test_pow_polar_accuracy(dm, cplx):
         err = abs(got - ref) / abs(ref) / (2.0 ** -50 + float(p[i]) * 2.0 ** -76)
         worst = max(worst, float(err))
     assert worst < 1.0, worst
+
+
+def _adversarial(rng, n):
+    """Points where log2|z| is hardest to bracket: |z| within 2^-1..2^-62 of a power of two (any binade,
+    incl. 1), subnormal and near-overflow moduli, near the axes and the diagonal, and random moduli."""
+    q = n // 6
+    k = rng.integers(-1070, 1020, q).astype(float)
+    eps = rng.choice([-1.0, 1.0], q) * np.exp2(-rng.integers(1, 63, q).astype(float))
+    near_pow2 = np.exp2(k) * (1 + eps)
+    near_one = 1 + rng.choice([-1.0, 1.0], q) * np.exp2(-rng.uniform(1, 62, q))
+    sub = rng.integers(1, 1 << 40, q).astype(float) * 2.0 ** -1074
+    big = np.exp2(rng.choice([-1.0, 1.0], q) * 1000 + rng.uniform(-40, 23, q))
+    rnd = np.exp2(rng.uniform(-1074, 1023, q))
+    mods = np.concatenate([near_pow2, near_one, sub, big, rnd])
+    th = rng.uniform(0, 2 * np.pi, len(mods))
+    z = mods * np.exp(1j * th)
+    m = len(mods)
+    # axes and diagonal: one coordinate tiny relative to the other, or |x| = |y| (1 + tiny)
+    a = np.exp2(rng.uniform(-1070, 1020, q))
+    axis = a + 1j * a * np.exp2(-rng.integers(1, 80, q).astype(float)) * rng.choice([-1, 1], q)
+    diag = a * (1 + 1j * (1 + rng.choice([-1, 1], q) * np.exp2(-rng.integers(1, 60, q).astype(float))))
+    z = np.concatenate([z, axis, diag])
+    z = z[np.isfinite(z) & (z != 0)]
+    return z, mods[np.isfinite(mods) & (mods > 0)] * rng.choice([-1.0, 1.0], int(np.sum(np.isfinite(mods) & (mods > 0))))
+
+
+def test_lambda_enclosure_contains_rounded_lambda(dm):
+    rng = np.random.default_rng(17)
+    zc, xr = _adversarial(rng, 1_000_000)
+    for pts, cplx in ((zc, 1), (xr, 0)):
+        xy, n = _xy(pts if cplx else pts.astype(np.complex128))
+        lmh = np.empty(3 * n)
+        dm.dm_lambda_enclosure(xy.ctypes.data, n, cplx, lmh.ctypes.data)
+        lo, hi, mid = lmh[0::3], lmh[1::3], lmh[2::3]
+        P = oracle.OraclePoly(np.array([1.0, 1.0]))
+        lam = P.classify(pts)["lam"]          # correctly rounded log2|z| (binary128, DESIGN.md G4)
+        bad = ~((lo <= lam) & (lam <= hi))
+        assert not bad.any(), (int(bad.sum()), pts[bad][:3], lam[bad][:3], lo[bad][:3], hi[bad][:3])
+        # the error the enclosure is built on (fpe_math.cuh): |mid - log2|z|| < 2^-50 + 2^-53 |lambda| (+ ulp)
+        err = np.abs(mid - lam) / (2.0 ** -50 + 2.0 ** -52 * np.abs(lam))
+        assert err.max() < 1.0, err.max()
+        assert n > 700_000 if cplx else n > 500_000
