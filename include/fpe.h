@@ -18,10 +18,13 @@
  *    max(|re|,|im|) of the mantissa in [1/2, 1) (or all zero with exp = 0),
  *    because z^d overflows any hardware float.
  *  - Results are a pure function of (handle, z): bitwise independent of the
- *    batch, its order, and the sharding across GPUs.  One exception: a batch that asks
- *    for more whole-piece tensor-core evaluations than its workspace holds (n/512 pieces
- *    of 16384 coefficients) evaluates the excess on the vector Horner, which agrees
- *    within the tolerance but not bit for bit.
+ *    batch, its order, the sharding across GPUs and the run.  (Whole 16384-coefficient
+ *    pieces of long windows run on the FP64 tensor cores; when a batch asks for more of
+ *    them than its workspace's scratch holds, the excess runs the same tensor-core
+ *    arithmetic inside the vector evaluator -- same bits, counted by fpe_workspace_stats.)
+ *  - The handle is immutable: concurrent fpe_evaluate / fpe_horner calls on one handle
+ *    are safe with distinct workspaces (except in profiling mode, fpe_set_profiling, and
+ *    fpe_evaluate_host, which use per-handle state).
  */
 #ifndef FPE_H_
 #define FPE_H_
@@ -77,10 +80,20 @@ typedef struct {
     int32_t r;
     int32_t kept;       /* K = #(G_p cap [l, r])                                           */
     int32_t hard;       /* 1 if lambda was within 2^-96 |lambda| of an fp64 rounding boundary */
-    int32_t cancel;     /* canceled bits c = s(M) - s(Q) (eq:def_prec_loss) with
-                           s(M) estimated by ceil(N_lambda), N_lambda = cover(k_lambda) + lambda k_lambda
-                           (log2 M lies in [N - 1, N]); the result has about p - c correct bits
-                           (Theorem thm:equivAlgo); INT32_MIN when Q = 0 or z is non-finite      */
+    int32_t cancel;     /* canceled bits c (eq:def_prec_loss): 0 if |Q| >= M, else
+                           s(M) - s(Q), with s(M) estimated from above by ceil(N_lambda), N_lambda =
+                           cover(k_lambda) + lambda k_lambda (log2 M lies in [N - 1, N)); the result
+                           has about p - c correct bits (Theorem thm:equivAlgo); INT32_MIN when Q = 0
+                           or z is non-finite                                                       */
+    int32_t trusted;    /* conservative number of correct leading bits of the result (the errors file,
+                           PAPER.md:2114-2118): clamp(s(Q) - err_exp, 0, p_w), p_w = 53 / 24 working
+                           bits; 0 when Q = 0 or z is non-finite                                     */
+    int32_t err_exp;    /* upper bound on the evaluation error: |value 2^exp - P(z)| <= 2^err_exp, with
+                           err_exp = ceil(N) + ceil(log2(2K + 256)) + ceil(log2 K) + 1 - p_w: rounding
+                           <= (2K + 256) u S over the K kept terms, S <= K 2^N, plus the truncation
+                           < 2^(N-p-3); clamped to the int32 range; INT32_MIN
+                           when z is non-finite                                                      */
+    int32_t pad;
 } fpe_diag;
 
 /*
@@ -184,7 +197,8 @@ fpe_status fpe_poly_export(fpe_poly h, void* dst, size_t cap, void* stream);
 fpe_status fpe_poly_from_device_buffer(const void* ptr, size_t bytes, int device,
                                        void* stream, fpe_poly* out);
 
-/* Bytes of device workspace fpe_evaluate / fpe_horner need for n_points points. */
+/* Bytes of device workspace fpe_evaluate / fpe_horner need for n_points points (the first 256 bytes
+ * hold the call's counters, fpe_workspace_stats). */
 fpe_status fpe_eval_workspace_size(fpe_poly h, int64_t n_points, size_t* bytes);
 
 /*
@@ -258,7 +272,8 @@ fpe_status fpe_newton_step(fpe_poly P, fpe_poly dP, const void* points, fpe_dtyp
 
 /*
  * Per-stage timing (measurement support for bench.py).  With fpe_set_profiling(h, 1) every
- * later fpe_evaluate / fpe_horner on h records CUDA events on its stream around each kernel;
+ * later fpe_evaluate / fpe_horner on h records CUDA events on its stream around each kernel (the
+ * events and stage names live in the handle: no concurrent calls on a profiling handle);
  * fpe_last_stage_ms (synchronising the stream of that call) returns the stage durations in
  * launch order (up to cap) and *n, and fpe_stage_name(h, i) names stage i.
  */
@@ -266,8 +281,24 @@ fpe_status fpe_set_profiling(fpe_poly h, int enable);
 fpe_status fpe_last_stage_ms(fpe_poly h, float* ms, int cap, int* n);
 const char* fpe_stage_name(fpe_poly h, int i);
 
-/* Counters of the last fpe_evaluate on this handle's stream-ordered statistics buffer:
- * stats[0] = hard-to-round lambdas, stats[1] = kernel launches.  Host array of 4. */
+/*
+ * fpe_workspace_stats -- the counters the last fpe_evaluate with this workspace wrote into its first 256
+ * bytes (the call zeroes them on its stream first).  Synchronises `stream` (the call's stream), then
+ * copies min(cap, *n) counters into the host array stats; *n receives the number of counters (5):
+ *   [0] lambdas within 2^-80 of an fp64 rounding boundary (Ziv test of the correctly rounded log2|z|;
+ *       counted for the points whose lambda was computed: all with diagnostics, the undecided ones without)
+ *   [1] (group, piece) tensor-core items planned (whole 16384-coefficient pieces, complex fp64)
+ *   [2] ... of which did not fit the workspace's DMMA scratch and ran in-warp (same arithmetic)
+ *   [3] parallel vector pieces of long windows
+ *   [4] long-window groups evaluated serially (piece scratch full; same arithmetic)
+ * Errors: INVALID_ARG, CUDA.
+ */
+fpe_status fpe_workspace_stats(const void* workspace, void* stream, int64_t* stats, int cap, int* n);
+
+/* Counters of the calling thread's last fpe_evaluate / fpe_evaluate_host / fpe_horner / fpe_newton_step
+ * (thread-local record; the workspace that call used must still be allocated): stats4[0] = hard-to-round
+ * lambdas, [1] = library kernel launches, [2] = tensor-core items, [3] = of which run in-warp.  Synchronises
+ * that call's stream.  `h` is only checked for NULL. */
 fpe_status fpe_last_stats(fpe_poly h, int64_t* stats4);
 
 void fpe_destroy(fpe_poly h);

@@ -12,6 +12,7 @@ kernels; torch provides device memory, streams and process groups only.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 
 import numpy as np
 
@@ -68,7 +69,7 @@ class Poly:
         info = FpeInfo()
         check(lib().fpe_poly_get_info(self._h, C.byref(info)), "fpe_poly_get_info")
         self.info = {f: getattr(info, f) for f, _ in FpeInfo._fields_ if f != "reserved"}
-        self._ws = None
+        self._last = threading.local()   # the workspace and stream of this thread's last call (last_stats)
 
     # -- metadata -----------------------------------------------------------
     @property
@@ -110,23 +111,30 @@ class Poly:
         return cls(h, device)
 
     # -- evaluation ---------------------------------------------------------
-    def workspace(self, n: int):
-        torch = _torch()
+    def workspace_bytes(self, n: int) -> int:
         sz = C.c_size_t()
         check(lib().fpe_eval_workspace_size(self._h, n, C.byref(sz)), "fpe_eval_workspace_size")
-        if self._ws is None or self._ws.numel() < sz.value:
-            self._ws = torch.empty(max(sz.value, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
-        return self._ws
+        return max(int(sz.value), 256)
 
-    def evaluate(self, points, exps: bool = True, diag: bool = False, out=None, stream=None):
-        """Q_lambda(z) for every point (device tensor).  Returns (values, exps[, diag])."""
-        return self._run(lib().fpe_evaluate, points, exps, diag, out, stream, "fpe_evaluate")
+    def workspace(self, n: int, stream=None):
+        """A fresh workspace for n points, allocated on `stream` (default: the current stream) by torch's
+        stream-ordered caching allocator: concurrent calls on different streams never share one."""
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(st):
+            return torch.empty(self.workspace_bytes(n), dtype=torch.uint8, device=f"cuda:{self.device}")
 
-    def horner(self, points, exps: bool = True, out=None, stream=None):
+    def evaluate(self, points, exps: bool = True, diag: bool = False, out=None, stream=None, workspace=None):
+        """Q_lambda(z) for every point (device tensor).  Returns (values, exps[, diag]).
+        workspace: optional uint8 CUDA tensor of at least workspace_bytes(n) (else one is allocated on the
+        call's stream)."""
+        return self._run(lib().fpe_evaluate, points, exps, diag, out, stream, workspace, "fpe_evaluate")
+
+    def horner(self, points, exps: bool = True, out=None, stream=None, workspace=None):
         """Full Horner over all stored coefficients (context baseline)."""
-        return self._run(lib().fpe_horner, points, exps, False, out, stream, "fpe_horner")
+        return self._run(lib().fpe_horner, points, exps, False, out, stream, workspace, "fpe_horner")
 
-    def _run(self, fn, points, want_exps, want_diag, out, stream, where):
+    def _run(self, fn, points, want_exps, want_diag, out, stream, ws, where):
         torch = _torch()
         if not points.is_cuda:
             raise ValueError("points must be a CUDA tensor (use evaluate_host for host arrays)")
@@ -134,19 +142,40 @@ class Poly:
         n = points.numel()
         pdt = _dtype_code(points)
         dev = points.device
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
         vals = out if out is not None else torch.empty(n, dtype=_out_dtype(self.info["dtype"], pdt), device=dev)
         e = torch.empty(n, dtype=torch.int64, device=dev) if want_exps else None
         dg = torch.empty((n, DIAG_BYTES), dtype=torch.uint8, device=dev) if want_diag else None
-        ws = self.workspace(n)
+        if ws is None:
+            self._last.ws = None   # let the previous call's workspace go back to the allocator first
+            ws = self.workspace(n, st)
+        elif ws.numel() < self.workspace_bytes(n):
+            raise ValueError("workspace too small")
         args = [self._h, C.c_void_p(points.data_ptr()), pdt, n, C.c_void_p(vals.data_ptr()),
                 C.c_void_p(e.data_ptr() if e is not None else 0)]
         if fn is lib().fpe_evaluate:
             args.append(C.c_void_p(dg.data_ptr() if dg is not None else 0))
-        args += [C.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, dev)]
+        args += [C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(st.cuda_stream)]
         check(fn(*args), where)
+        self._last.ws, self._last.stream = ws, st
         if want_diag:
             return vals, e, dg
         return vals, e
+
+    def workspace_stats(self, ws=None, stream=None) -> dict:
+        """Counters of the last evaluate() that used workspace `ws` (default: this thread's last call)."""
+        if ws is None:
+            ws, stream = getattr(self._last, "ws", None), getattr(self._last, "stream", None)
+            if ws is None:
+                raise ValueError("no evaluate() call on this thread yet")
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        v = np.zeros(8, np.int64)
+        cnt = C.c_int(0)
+        check(lib().fpe_workspace_stats(C.c_void_p(ws.data_ptr()), C.c_void_p(st.cuda_stream), v.ctypes.data, 8,
+                                        C.byref(cnt)), "fpe_workspace_stats")
+        names = ["hard_lambdas", "mma_items", "mma_inwarp_items", "piece_items", "serial_long_groups"]
+        return {k: int(v[i]) for i, k in enumerate(names[:cnt.value])}
 
     def evaluate_host(self, points: np.ndarray, exps: bool = True):
         """End-to-end evaluation from host memory (pinned for full bandwidth)."""
@@ -179,9 +208,12 @@ class Poly:
         return [(lib().fpe_stage_name(self._h, i).decode(), float(ms[i])) for i in range(n.value)]
 
     def last_stats(self):
+        """Counters of this thread's last library call (fpe_last_stats): hard lambdas, kernel launches,
+        tensor-core items and those run in-warp."""
         s = np.zeros(4, np.int64)
         check(lib().fpe_last_stats(self._h, s.ctypes.data), "fpe_last_stats")
-        return {"hard_lambdas": int(s[0]), "launches": int(s[1])}
+        return {"hard_lambdas": int(s[0]), "launches": int(s[1]), "mma_items": int(s[2]),
+                "mma_inwarp_items": int(s[3])}
 
     def close(self):
         if self._h:
@@ -338,9 +370,11 @@ def header_fields(buf: np.ndarray) -> dict:
 
 
 def diag_fields(dg):
-    """Split a (n, 32) uint8 diag tensor into named tensors (lambda, region, l, r, kept, hard, cancel)."""
+    """Split a (n, DIAG_BYTES) uint8 diag tensor into named tensors (lambda, region, l, r, kept, hard, cancel,
+    trusted, err_exp)."""
     raw = dg.contiguous()
     lam = raw[:, 0:8].contiguous().view(_torch().float64).reshape(-1)
-    ints = raw[:, 8:32].contiguous().view(_torch().int32).reshape(-1, 6)
+    ints = raw[:, 8:44].contiguous().view(_torch().int32).reshape(-1, 9)
     return {"lambda": lam, "region": ints[:, 0], "l": ints[:, 1], "r": ints[:, 2],
-            "kept": ints[:, 3], "hard": ints[:, 4], "cancel": ints[:, 5]}
+            "kept": ints[:, 3], "hard": ints[:, 4], "cancel": ints[:, 5], "trusted": ints[:, 6],
+            "err_exp": ints[:, 7]}

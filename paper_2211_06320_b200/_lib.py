@@ -23,7 +23,7 @@ class FpeInfo(C.Structure):
                 ("sparse", C.c_int32), ("dtype", C.c_int32), ("reserved", C.c_int32), ("bytes", C.c_size_t)]
 
 
-DIAG_BYTES = 32  # fpe_diag: double lambda; int32 region, l, r, kept, hard, pad
+DIAG_BYTES = 48  # fpe_diag: double lambda; int32 region, l, r, kept, hard, cancel, trusted, err_exp, pad
 
 _lock = threading.Lock()
 _lib = None
@@ -58,6 +58,7 @@ SIGNATURES = {
     "fpe_evaluate_host": (C.c_int, [_P, _P, C.c_int, _I64, _P, _P, _P]),
     "fpe_horner": (C.c_int, [_P, _P, C.c_int, _I64, _P, _P, _P, _SZ, _P]),
     "fpe_last_stats": (C.c_int, [_P, _P]),
+    "fpe_workspace_stats": (C.c_int, [_P, _P, _P, C.c_int, C.POINTER(C.c_int)]),
     "fpe_precondition_derivative": (C.c_int, [_P, _I64, C.c_int, _I32, _I32, C.c_int, _P, C.POINTER(_P)]),
     "fpe_newton_workspace_size": (C.c_int, [_P, _P, _I64, C.POINTER(_SZ)]),
     "fpe_newton_step": (C.c_int, [_P, _P, _P, C.c_int, _I64, _P, _P, _P, _SZ, _P]),

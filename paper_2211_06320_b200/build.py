@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = EXTRA + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
            "--expt-relaxed-constexpr", "-I", os.path.join(HERE, "..", "include")]
 SOURCES = ["api.cu", "kernels.cu", "sort.cu", "eval_tiled.cu", "precondition.cpp", "precondition_gpu.cu", "eval_mma.cu"]
-HEADERS = ["fpe_internal.h", "fpe_hd.cuh", "fpe_polar.cuh", "fpe_math.cuh", "kernels.cuh", "log_table.h", "device_common.cuh", "sort.cuh", "eval_tiled.cuh", "tma.cuh"]
+HEADERS = ["fpe_internal.h", "fpe_hd.cuh", "fpe_polar.cuh", "fpe_math.cuh", "kernels.cuh", "log_table.h", "device_common.cuh", "sort.cuh", "eval_tiled.cuh", "tma.cuh", "mma_piece.cuh"]
 
 
 def _newer(src: list[str], dst: str) -> bool:

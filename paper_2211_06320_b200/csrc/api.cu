@@ -13,6 +13,8 @@
 #include "kernels.cuh"
 #include "eval_tiled.cuh"
 
+static_assert(sizeof(fpe_diag) == 48, "fpe_diag layout (paper_2211_06320_b200/_lib.py DIAG_BYTES)");
+
 namespace fpe {
 
 static thread_local char g_err[512] = "";
@@ -50,24 +52,41 @@ struct DeviceGuard {
 // internal batch: the radix scan handles up to 2^28 points at a time
 constexpr long long kMaxBatch = 1ll << 28;
 
+// workspace = kWsHeader bytes of counters (kStat*) + the path's scratch
 static size_t ws_bytes_for(long long n) {
   long long b = n < kMaxBatch ? n : kMaxBatch;
   size_t naive = ((size_t)b * sizeof(int2) + 255) & ~size_t(255);
   size_t tiled = tiled_ws_bytes(b);
-  return naive > tiled ? naive : tiled;
+  return kWsHeader + (naive > tiled ? naive : tiled);
 }
 
+// The calling thread's last evaluation (fpe_last_stats): which workspaces hold its counters, the stream
+// to synchronise, and the number of library kernels it launched.  Thread-local, so the handle itself is
+// never written by fpe_evaluate / fpe_horner (fpe.h: concurrent calls on one handle with distinct
+// workspaces are safe).
+struct LastCall {
+  const void* ws[fpe_poly_s::kHostSlots] = {};
+  int nws = 0;
+  void* stream = nullptr;
+  int device = 0;
+  long long launches = 0;
+};
+static thread_local LastCall g_last;
+
+// Profiling events are recorded only on a handle with fpe_set_profiling on (a debugging mode that writes
+// the handle: not for concurrent calls).
 Stage::Stage(fpe_poly h_, void* s_) : h(h_), stream(s_) {
+  if (!h->profiling) return;
   h->n_stages = 0;
   h->prof_stream = s_;
-  if (h->profiling) cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[0]), static_cast<cudaStream_t>(s_));
+  cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[0]), static_cast<cudaStream_t>(s_));
 }
 void Stage::mark(const char* name) {
+  if (!h->profiling) return;
   if (h->n_stages < 15) {
     h->stage_names[h->n_stages] = name;
     ++h->n_stages;
-    if (h->profiling)
-      cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[h->n_stages]), static_cast<cudaStream_t>(stream));
+    cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[h->n_stages]), static_cast<cudaStream_t>(stream));
   }
 }
 
@@ -96,8 +115,7 @@ fpe::PolyDev fpe_poly_s::view() const {
 using namespace fpe;
 
 static fpe_status finish_handle(fpe_poly h) {
-  FPE_CUDA(cudaMalloc(&h->dstats, 4 * sizeof(unsigned long long)));
-  FPE_CUDA(cudaMemset(h->dstats, 0, 4 * sizeof(unsigned long long)));
+  (void)h;
   return FPE_OK;
 }
 
@@ -122,7 +140,6 @@ void fpe_destroy(fpe_poly h) {
   if (!h) return;
   DeviceGuard g(h->device);
   if (h->dbuf) cudaFree(h->dbuf);
-  if (h->dstats) cudaFree(h->dstats);
   if (h->st_dev) cudaFree(h->st_dev);
   for (void* s : h->st_streams) if (s) cudaStreamDestroy(static_cast<cudaStream_t>(s));
   for (void* e : h->st_events) if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
@@ -404,9 +421,30 @@ fpe_status fpe_poly_device_buffer(fpe_poly h, const void** dptr, size_t* bytes) 
   return FPE_OK;
 }
 
+// A header received from elsewhere (another rank, a file): every field the library indexes with must be in
+// range and every section inside the buffer, so that no later read leaves it.
+static bool header_valid(const Header& H, size_t bytes) {
+  if (H.magic != kMagic || H.version != kVersion || H.bytes != bytes) return false;
+  if (!dtype_ok(H.dtype) || H.n_coeffs < 1 || H.n_coeffs > (1ll << 31) - 2) return false;
+  if (H.k_min < 0 || H.k_min > H.k_max || H.k_max >= H.n_coeffs) return false;
+  const long long d_eff = H.k_max - H.k_min;
+  if (H.n_hull < 1 || H.n_hull > d_eff + 1 || H.n_good < 1 || H.n_good > d_eff + 1) return false;
+  if (H.p < 1 || H.drop < 1 || (H.sparse != 0 && H.sparse != 1) || (H.all_good != 0 && H.all_good != 1)) return false;
+  auto inside = [&](uint64_t off, uint64_t len) { return off >= sizeof(Header) && off <= bytes && len <= bytes - off; };
+  const uint64_t csz = dtype_size(H.dtype);
+  const uint64_t n_coef = H.sparse ? (uint64_t)H.n_good : (uint64_t)(d_eff + 1 + kCoefPad - 1) / kCoefPad * kCoefPad;
+  if (!inside(H.off_hull, (uint64_t)H.n_hull * sizeof(int2)) || !inside(H.off_coef, n_coef * csz)) return false;
+  if (!H.sparse && !H.all_good && !inside(H.off_prefix, (uint64_t)(d_eff + 2) * sizeof(int32_t))) return false;
+  if (H.sparse && !inside(H.off_sidx, (uint64_t)H.n_good * sizeof(int32_t))) return false;
+  return true;
+}
+
 fpe_status fpe_poly_from_device_buffer(const void* dptr, size_t bytes, int device, void* stream, fpe_poly* out) {
   if (!dptr || !out || bytes < sizeof(Header)) { set_error("fpe_poly_from_device_buffer: invalid argument"); return FPE_ERR_INVALID_ARG; }
   *out = nullptr;
+  int ndev = 0;
+  FPE_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) { set_error("fpe_poly_from_device_buffer: bad device %d", device); return FPE_ERR_INVALID_ARG; }
   DeviceGuard g(device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   fpe_poly h = new (std::nothrow) fpe_poly_s();
@@ -415,13 +453,22 @@ fpe_status fpe_poly_from_device_buffer(const void* dptr, size_t bytes, int devic
   cudaError_t e = cudaMemcpyAsync(&h->hdr, dptr, sizeof(Header), cudaMemcpyDefault, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) { set_error("header read failed: %s", cudaGetErrorString(e)); delete h; return FPE_ERR_CUDA; }
-  if (h->hdr.magic != kMagic || h->hdr.version != kVersion || h->hdr.bytes != bytes) {
-    set_error("fpe_poly_from_device_buffer: not an fpe buffer (magic/version/size mismatch)");
+  if (!header_valid(h->hdr, bytes)) {
+    set_error("fpe_poly_from_device_buffer: not a valid fpe buffer (magic/version/size/section bounds)");
     delete h;
     return FPE_ERR_INVALID_ARG;
   }
   if (cudaMalloc(&h->dbuf, bytes) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc failed"); delete h; return FPE_ERR_OOM; }
-  std::vector<int2> hull(h->hdr.n_hull);
+  std::vector<int2> hull;
+  try {
+    hull.resize(h->hdr.n_hull);
+    h->hk.reserve(h->hdr.n_hull);
+    h->hh.reserve(h->hdr.n_hull);
+  } catch (const std::bad_alloc&) {
+    set_error("out of host memory");
+    fpe_destroy(h);
+    return FPE_ERR_OOM;
+  }
   e = cudaMemcpyAsync(h->dbuf, dptr, bytes, cudaMemcpyDefault, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hull.data(), static_cast<const char*>(dptr) + h->hdr.off_hull,
                                             hull.size() * sizeof(int2), cudaMemcpyDefault, s);
@@ -453,11 +500,14 @@ static fpe_status check_eval_args(fpe_poly h, const void* points, fpe_dtype pt_d
   return FPE_OK;
 }
 
-// reset_stats: clear the hard-lambda counter first (fpe_evaluate); fpe_evaluate_host clears it once and
-// lets its chunks, whose kernels run on several streams, accumulate into it.
+// reset_stats: clear the workspace's counters first (fpe_evaluate); fpe_evaluate_host clears its staging
+// slots' counters once and lets the chunks accumulate into them.  *launches receives the number of library
+// kernels enqueued.
 static fpe_status evaluate_impl(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
                                 void* values_out, int64_t* exps_out, fpe_diag* diag_out,
-                                void* workspace, size_t ws_bytes, void* stream, bool reset_stats) {
+                                void* workspace, size_t ws_bytes, void* stream, bool reset_stats,
+                                long long* launches_out) {
+  *launches_out = 0;
   fpe_status st = check_eval_args(h, points, pt_dt, n_points, values_out);
   if (st != FPE_OK) return st;
   if (n_points == 0) return FPE_OK;
@@ -468,8 +518,9 @@ static fpe_status evaluate_impl(fpe_poly h, const void* points, fpe_dtype pt_dt,
   DeviceGuard g(h->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PolyDev P = h->view();
-  int2* lr = static_cast<int2*>(workspace);
-  if (reset_stats) FPE_CUDA(cudaMemsetAsync(h->dstats, 0, sizeof(unsigned long long), s));
+  unsigned long long* stats = static_cast<unsigned long long*>(workspace);
+  void* scratch = static_cast<char*>(workspace) + kWsHeader;
+  if (reset_stats) FPE_CUDA(cudaMemsetAsync(stats, 0, kWsHeader, s));
   Stage stg(h, s);
   long long launches = 0;
   for (long long off = 0; off < n_points; off += kMaxBatch) {
@@ -483,13 +534,13 @@ static fpe_status evaluate_impl(fpe_poly h, const void* points, fpe_dtype pt_dt,
     long long* ee = exps_out ? reinterpret_cast<long long*>(exps_out) + off : nullptr;
     fpe_diag* dd = diag_out ? diag_out + off : nullptr;
     if (!P.sparse) {
-      int l = run_tiled(pt_dt, pp, m, P, vv, ee, dd, workspace, h->dstats, stg, s);
+      int l = run_tiled(pt_dt, pp, m, P, vv, ee, dd, scratch, stats, stg, s);
       if (l < 0) { set_error("fpe_evaluate: tiled path rejected the launch"); return FPE_ERR_INVALID_ARG; }
       launches += l;
       if (dd) { launch_confidence(out_kind, m, P, vv, ee, dd, s); launches += 1; }
     } else {
-      int2* lr = static_cast<int2*>(workspace);
-      launch_classify(pt_dt, pp, m, P, lr, dd, h->dstats, s);
+      int2* lr = static_cast<int2*>(scratch);
+      launch_classify(pt_dt, pp, m, P, lr, dd, stats + kStatHard, s);
       stg.mark("classify");
       launch_eval_sparse(pt_dt, pp, m, P, lr, vv, ee, s);
       stg.mark("eval_sparse");
@@ -497,7 +548,7 @@ static fpe_status evaluate_impl(fpe_poly h, const void* points, fpe_dtype pt_dt,
       if (dd) { launch_confidence(out_kind, m, P, vv, ee, dd, s); launches += 1; }
     }
   }
-  h->last_launches = launches;       // kernels of this library (memsets not counted)
+  *launches_out = launches;       // kernels of this library (memsets not counted)
   FPE_CUDA(cudaGetLastError());
   return FPE_OK;
 }
@@ -505,7 +556,15 @@ static fpe_status evaluate_impl(fpe_poly h, const void* points, fpe_dtype pt_dt,
 fpe_status fpe_evaluate(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
                         void* values_out, int64_t* exps_out, fpe_diag* diag_out,
                         void* workspace, size_t ws_bytes, void* stream) {
-  return evaluate_impl(h, points, pt_dt, n_points, values_out, exps_out, diag_out, workspace, ws_bytes, stream, true);
+  long long launches = 0;
+  const fpe_status st = evaluate_impl(h, points, pt_dt, n_points, values_out, exps_out, diag_out, workspace, ws_bytes,
+                                      stream, true, &launches);
+  if (st == FPE_OK) {
+    g_last = LastCall{};
+    g_last.ws[0] = workspace; g_last.nws = n_points > 0 ? 1 : 0;
+    g_last.stream = stream; g_last.device = h->device; g_last.launches = launches;
+  }
+  return st;
 }
 
 fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n_points,
@@ -528,7 +587,8 @@ fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n
                      reinterpret_cast<long long*>(exps_out), s);
   }
   stg.mark("horner_full");
-  h->last_launches = 1;
+  g_last = LastCall{};
+  g_last.stream = stream; g_last.device = h->device; g_last.launches = 1;
   FPE_CUDA(cudaGetLastError());
   return FPE_OK;
 }
@@ -564,7 +624,7 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t per = al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8) + ws_bytes_for(chunk);
   if (h->st_bytes < kSlots * per) {
-    if (h->st_dev) { cudaFree(h->st_dev); h->st_dev = nullptr; h->st_bytes = 0; }
+    if (h->st_dev) { cudaDeviceSynchronize(); cudaFree(h->st_dev); h->st_dev = nullptr; h->st_bytes = 0; }
     if (cudaMalloc(&h->st_dev, kSlots * per) != cudaSuccess) { cudaGetLastError(); set_error("staging cudaMalloc failed"); return FPE_ERR_OOM; }
     h->st_bytes = kSlots * per;
   }
@@ -582,49 +642,78 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
     }
   cudaStream_t s_in = static_cast<cudaStream_t>(h->st_streams[0]);
   cudaStream_t s_out = static_cast<cudaStream_t>(h->st_streams[1]);
-  FPE_CUDA(cudaMemsetAsync(h->dstats, 0, sizeof(unsigned long long), s_in));   // before every chunk (events)
+  auto slot_base = [&](int b) { return static_cast<char*>(h->st_dev) + b * per; };
+  auto slot_ws = [&](int b) { return slot_base(b) + al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8); };
+  const int used = (int)std::min<long long>(kSlots, (n_points - std::min<long long>(chunk, 1ll << lg_first) + chunk - 1) / chunk + 1);
+  for (int b = 0; b < used; ++b) FPE_CUDA(cudaMemsetAsync(slot_ws(b), 0, kWsHeader, s_in));   // counters, before every chunk
   auto ev = [&](int slot, int kind) { return static_cast<cudaEvent_t>(h->st_events[slot * 3 + kind]); };
   long long launches = 0;
   static const bool trace = std::getenv("FPE_HOST_TRACE") != nullptr;   // debugging: per-chunk timeline
   std::vector<cudaEvent_t> tev;
   cudaEvent_t t0 = nullptr;
   if (trace) { cudaEventCreate(&t0); cudaEventRecord(t0, s_in); }
-  auto mark = [&](cudaStream_t st) {
+  auto mark = [&](cudaStream_t st_) {
     if (!trace) return;
-    cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, st); tev.push_back(e);
+    cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, st_); tev.push_back(e);
   };
+  auto release_trace = [&]() {
+    for (auto e : tev) cudaEventDestroy(e);
+    tev.clear();
+    if (t0) { cudaEventDestroy(t0); t0 = nullptr; }
+  };
+  // On an error after work was enqueued, wait for every stream of the pipeline before returning: copies
+  // still queued point at the caller's host buffers.
+  auto fail = [&](fpe_status e) {
+    for (auto sp : h->st_streams) if (sp) cudaStreamSynchronize(static_cast<cudaStream_t>(sp));
+    release_trace();
+    return e;
+  };
+#define FPE_CUDA_P(call)                                                                           \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      fpe::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return fail(FPE_ERR_CUDA);                                                                   \
+    }                                                                                              \
+  } while (0)
   long long next = std::min<long long>(chunk, 1ll << lg_first);
   for (long long off = 0, c = 0, m = 0; off < n_points; off += m, ++c) {
     m = std::min(next, n_points - off);
     next = chunk;
     const int b = (int)(c % kSlots);
     cudaStream_t s_ev = static_cast<cudaStream_t>(h->st_streams[2 + b]);
-    char* base = static_cast<char*>(h->st_dev) + b * per;
+    char* base = slot_base(b);
     void* dp = base;
     void* dv = base + al(chunk * in_sz);
     long long* de = reinterpret_cast<long long*>(base + al(chunk * in_sz) + al(chunk * out_sz));
-    void* wsp = base + al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8);
-    if (c >= kSlots) FPE_CUDA(cudaStreamWaitEvent(s_in, ev(b, 2), 0));   // slot's previous results copied out
+    void* wsp = slot_ws(b);
+    if (c >= kSlots) FPE_CUDA_P(cudaStreamWaitEvent(s_in, ev(b, 2), 0));   // slot's previous results copied out
     mark(s_in);
-    FPE_CUDA(cudaMemcpyAsync(dp, static_cast<const char*>(points_host) + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
+    FPE_CUDA_P(cudaMemcpyAsync(dp, static_cast<const char*>(points_host) + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
     mark(s_in);
-    FPE_CUDA(cudaEventRecord(ev(b, 0), s_in));
-    FPE_CUDA(cudaStreamWaitEvent(s_ev, ev(b, 0), 0));
+    FPE_CUDA_P(cudaEventRecord(ev(b, 0), s_in));
+    FPE_CUDA_P(cudaStreamWaitEvent(s_ev, ev(b, 0), 0));
     mark(s_ev);
+    long long l = 0;
     fpe_status est = evaluate_impl(h, dp, pt_dt, m, dv, exps_host ? reinterpret_cast<int64_t*>(de) : nullptr, nullptr,
-                                   wsp, ws_bytes_for(chunk), s_ev, false);
+                                   wsp, ws_bytes_for(chunk), s_ev, false, &l);
     mark(s_ev);
-    if (est != FPE_OK) return est;
-    launches += h->last_launches;
-    FPE_CUDA(cudaEventRecord(ev(b, 1), s_ev));
-    FPE_CUDA(cudaStreamWaitEvent(s_out, ev(b, 1), 0));
+    if (est != FPE_OK) return fail(est);
+    launches += l;
+    FPE_CUDA_P(cudaEventRecord(ev(b, 1), s_ev));
+    FPE_CUDA_P(cudaStreamWaitEvent(s_out, ev(b, 1), 0));
     mark(s_out);
-    FPE_CUDA(cudaMemcpyAsync(static_cast<char*>(values_host) + off * out_sz, dv, m * out_sz, cudaMemcpyDeviceToHost, s_out));
-    if (exps_host) FPE_CUDA(cudaMemcpyAsync(exps_host + off, de, m * 8, cudaMemcpyDeviceToHost, s_out));
+    FPE_CUDA_P(cudaMemcpyAsync(static_cast<char*>(values_host) + off * out_sz, dv, m * out_sz, cudaMemcpyDeviceToHost, s_out));
+    if (exps_host) FPE_CUDA_P(cudaMemcpyAsync(exps_host + off, de, m * 8, cudaMemcpyDeviceToHost, s_out));
     mark(s_out);
-    FPE_CUDA(cudaEventRecord(ev(b, 2), s_out));
+    FPE_CUDA_P(cudaEventRecord(ev(b, 2), s_out));
   }
-  FPE_CUDA(cudaStreamSynchronize(s_out));
+#undef FPE_CUDA_P
+  const cudaError_t se = cudaStreamSynchronize(s_out);
+  if (se != cudaSuccess) {
+    set_error("fpe_evaluate_host: %s", cudaGetErrorString(se));
+    return fail(FPE_ERR_CUDA);
+  }
   if (trace) {   // chunk: h2d [start, end], kernels [start, end], d2h [start, end] in ms from the call
     cudaDeviceSynchronize();
     for (size_t k = 0; k + 5 < tev.size() + 0; k += 6) {
@@ -633,10 +722,12 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
       std::fprintf(stderr, "chunk %zu: h2d %.2f-%.2f  eval %.2f-%.2f  d2h %.2f-%.2f\n", k / 6, v[0], v[1], v[2], v[3],
                    v[4], v[5]);
     }
-    for (auto e : tev) cudaEventDestroy(e);
-    cudaEventDestroy(t0);
+    release_trace();
   }
-  h->last_launches = launches;
+  g_last = LastCall{};
+  for (int b = 0; b < used; ++b) g_last.ws[b] = slot_ws(b);
+  g_last.nws = used;
+  g_last.stream = s_out; g_last.device = h->device; g_last.launches = launches;
   return FPE_OK;
 }
 
@@ -719,14 +810,14 @@ fpe_status fpe_newton_step(fpe_poly P, fpe_poly dP, const void* points, fpe_dtyp
   }
   st = fpe_evaluate(P, points, pt_dt, n_points, v1, e1, nullptr, p, ws, stream);
   if (st != FPE_OK) return st;
-  long long launches = P->last_launches;
+  long long launches = g_last.launches;
   st = fpe_evaluate(dP, points, pt_dt, n_points, v2, e2, nullptr, p, ws, stream);
   if (st != FPE_OK) return st;
-  launches += dP->last_launches;
+  launches += g_last.launches;
   const int ok = is_f32(pt_dt) ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
   launch_newton(pt_dt, ok, n_points, points, v1, reinterpret_cast<const long long*>(e1), v2,
                 reinterpret_cast<const long long*>(e2), points_out, incr_out, s);
-  P->last_launches = launches + 1;
+  g_last.launches = launches + 1;   // counters: those of the P' evaluation (the workspace is reused)
   FPE_CUDA(cudaGetLastError());
   return FPE_OK;
 }
@@ -761,14 +852,39 @@ const char* fpe_stage_name(fpe_poly h, int i) {
   return h->stage_names[i];
 }
 
+static fpe_status read_counters(const void* ws, cudaStream_t s, unsigned long long* v) {
+  FPE_CUDA(cudaStreamSynchronize(s));
+  FPE_CUDA(cudaMemcpy(v, ws, kStatCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return FPE_OK;
+}
+
+fpe_status fpe_workspace_stats(const void* workspace, void* stream, int64_t* stats, int cap, int* n) {
+  if (!workspace || !n || (cap > 0 && !stats) || cap < 0) {
+    set_error("fpe_workspace_stats: invalid argument");
+    return FPE_ERR_INVALID_ARG;
+  }
+  unsigned long long v[kStatCount];
+  fpe_status st = read_counters(workspace, static_cast<cudaStream_t>(stream), v);
+  if (st != FPE_OK) return st;
+  *n = kStatCount;
+  for (int i = 0; i < kStatCount && i < cap; ++i) stats[i] = (int64_t)v[i];
+  return FPE_OK;
+}
+
 fpe_status fpe_last_stats(fpe_poly h, int64_t* stats4) {
   if (!h || !stats4) { set_error("fpe_last_stats: invalid argument"); return FPE_ERR_INVALID_ARG; }
-  DeviceGuard g(h->device);
-  unsigned long long v[4];
-  FPE_CUDA(cudaMemcpy(v, h->dstats, sizeof(v), cudaMemcpyDeviceToHost));
-  stats4[0] = (int64_t)v[0];
-  stats4[1] = h->last_launches;
-  stats4[2] = 0; stats4[3] = 0;
+  DeviceGuard g(g_last.device);
+  unsigned long long tot[kStatCount] = {};
+  for (int b = 0; b < g_last.nws; ++b) {
+    unsigned long long v[kStatCount];
+    fpe_status st = read_counters(g_last.ws[b], static_cast<cudaStream_t>(g_last.stream), v);
+    if (st != FPE_OK) return st;
+    for (int i = 0; i < kStatCount; ++i) tot[i] += v[i];
+  }
+  stats4[0] = (int64_t)tot[kStatHard];
+  stats4[1] = g_last.launches;
+  stats4[2] = (int64_t)tot[kStatMmaItems];
+  stats4[3] = (int64_t)tot[kStatMmaInWarp];
   return FPE_OK;
 }
 

@@ -6,6 +6,7 @@
 #include "sort.cuh"
 #include "tma.cuh"
 #include "eval_tiled.cuh"
+#include "mma_piece.cuh"
 
 namespace fpe {
 
@@ -33,30 +34,14 @@ namespace fpe {
 #endif
 constexpr int kMmaWarps = 8;
 constexpr int kMmaStages = FPE_MMA_STAGES;
-constexpr int kPieceChunks = kPiece / kChunk;
-
-__device__ __forceinline__ void cmul(double& r, double& i, double ar, double ai, double br, double bi) {
-  const double t = fma(ar, br, -ai * bi);
-  i = fma(ar, bi, ai * br);
-  r = t;
-}
-__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b) {
-  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
-               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
-               : "d"(a0), "d"(a1), "d"(b));
-}
-__device__ __forceinline__ void dd_sqr_c(xc_t& v) {
-  xc_sqr(v);
-  const dd_t r = two_sum(v.hr, v.er), i = two_sum(v.hi, v.ei);
-  v.hr = r.hi; v.er = r.lo; v.hi = i.hi; v.ei = i.lo;
-}
+constexpr int kPieceChunks = kMmaPieceChunks;
 
 __global__ void __launch_bounds__(kMmaWarps * 32, FPE_MMA_MINB) k_eval_mma(long long n, const double2* __restrict__ coef,
                                                                 int kmin, const PtRec* __restrict__ rec, Plan plan) {
   __shared__ __align__(128) double2 ring[kMmaStages][kChunk];
   __shared__ uint64_t full[kMmaStages], empty[kMmaStages];
   __shared__ uint2 item_sh;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, c = lane & 3;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < kMmaStages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, kMmaWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -101,112 +86,21 @@ __global__ void __launch_bounds__(kMmaWarps * 32, FPE_MMA_MINB) k_eval_mma(long 
       if (h.w >= h.z) { wl = h.z - kmin; wr = h.w - kmin; }
     }
     const int act = mma_covers(wl, wr, x, y, p) ? 1 : 0;
-    // u = z^16, u^4, w = z^256 of the lane's point (double-double squarings, one rounding each)
-    double ur, ui, u4r, u4i, wwr, wwi;
-    {
-      xc_t v{act ? x : 1.0, act ? y : 0.0, 0.0, 0.0, 0};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dd_sqr_c(v);
-      ur = v.hr + v.er; ui = v.hi + v.ei;
-      dd_sqr_c(v); dd_sqr_c(v);
-      u4r = v.hr + v.er; u4i = v.hi + v.ei;
-      dd_sqr_c(v); dd_sqr_c(v);
-      wwr = v.hr + v.er; wwi = v.hi + v.ei;
-    }
-    double vr[2][4], vi[2][4], cwr[2][2], cwi[2][2], cr[2][4], ci[2][4];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int src = 8 * t + g;                   // the point of B column g
-      const double qr = __shfl_sync(0xffffffffu, ur, src), qi = __shfl_sync(0xffffffffu, ui, src);
-      const double q4r = __shfl_sync(0xffffffffu, u4r, src), q4i = __shfl_sync(0xffffffffu, u4i, src);
-      const int on = __shfl_sync(0xffffffffu, act, src);
-      double pr = 1.0, pi = 0.0;                   // u^c
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-        if (i < c) cmul(pr, pi, pr, pi, qr, qi);
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {             // B row c of k-step ks: u^(4 ks + c); inactive column: 0
-        if (ks) cmul(pr, pi, pr, pi, q4r, q4i);
-        vr[t][ks] = on ? pr : 0.0;
-        vi[t][ks] = on ? pi : 0.0;
-      }
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {                // w of the C columns 2c, 2c + 1
-        const int s2 = 8 * t + 2 * c + e;
-        cwr[t][e] = __shfl_sync(0xffffffffu, wwr, s2);
-        cwi[t][e] = __shfl_sync(0xffffffffu, wwi, s2);
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) { cr[t][e] = 0.0; ci[t][e] = 0.0; }
-    }
+    MmaFrag F;
+    mma_setup(F, x, y, act);
     const bool busy = __any_sync(0xffffffffu, act);   // a warp without covering points only keeps the ring going
     for (int k = 0; k < kPieceChunks; ++k) {
       const int s = (int)(t_seq % kMmaStages);
       mbar_wait(full + s, (t_seq / kMmaStages) & 1u);
-      const double2* cb = ring[s];
-      if (!busy) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + s);
-        ++t_seq;
-        if (tid == 0 && k + kMmaStages < kPieceChunks) issue(q0 - k - kMmaStages);
-        __syncwarp();
-        continue;
-      }
-      if (k) {
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) cmul(cr[t][e], ci[t][e], cr[t][e], ci[t][e], cwr[t][e & 1], cwi[t][e & 1]);
-      }
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const double2 a0 = cb[64 * ks + 16 * c + g], a1 = cb[64 * ks + 16 * c + g + 8];   // A[g|g+8][4ks + c]
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          dmma(cr[t], a0.x, a1.x, vr[t][ks]);      // Re: ar vr - ai vi
-          dmma(cr[t], -a0.y, -a1.y, vi[t][ks]);
-          dmma(ci[t], a0.x, a1.x, vi[t][ks]);      // Im: ar vi + ai vr
-          dmma(ci[t], a0.y, a1.y, vr[t][ks]);
-        }
-      }
+      if (busy) mma_chunk(F, ring[s], k == 0);
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
       ++t_seq;
       if (tid == 0 && k + kMmaStages < kPieceChunks) issue(q0 - k - kMmaStages);
       __syncwarp();
     }
-    // sum_m z^m R_m: rows g and g + 8 in the thread, then a tree over g (lane bits 2..4)
-    double hr[2][2], hi[2][2];
-#pragma unroll
-    for (int t = 0; t < 2; ++t)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int src = 8 * t + 2 * c + e;
-        const double zr = __shfl_sync(0xffffffffu, x, src), zi = __shfl_sync(0xffffffffu, y, src);
-        double z2r, z2i, z4r, z4i, z8r, z8i;
-        cmul(z2r, z2i, zr, zi, zr, zi);
-        cmul(z4r, z4i, z2r, z2i, z2r, z2i);
-        cmul(z8r, z8i, z4r, z4i, z4r, z4i);
-        double pr = cr[t][e], pi = ci[t][e];
-        pr = fma(cr[t][e + 2], z8r, fma(-ci[t][e + 2], z8i, pr));
-        pi = fma(cr[t][e + 2], z8i, fma(ci[t][e + 2], z8r, pi));
-        double nr = __shfl_xor_sync(0xffffffffu, pr, 4), ni = __shfl_xor_sync(0xffffffffu, pi, 4);
-        pr = fma(nr, zr, fma(-ni, zi, pr)); pi = fma(nr, zi, fma(ni, zr, pi));
-        nr = __shfl_xor_sync(0xffffffffu, pr, 8); ni = __shfl_xor_sync(0xffffffffu, pi, 8);
-        pr = fma(nr, z2r, fma(-ni, z2i, pr)); pi = fma(nr, z2i, fma(ni, z2r, pi));
-        nr = __shfl_xor_sync(0xffffffffu, pr, 16); ni = __shfl_xor_sync(0xffffffffu, pi, 16);
-        pr = fma(nr, z4r, fma(-ni, z4i, pr)); pi = fma(nr, z4i, fma(ni, z4r, pi));
-        hr[t][e] = pr; hi[t][e] = pi;              // valid in lanes 0..3 (g = 0)
-      }
-    double orr = 0.0, oi = 0.0;
-#pragma unroll
-    for (int t = 0; t < 2; ++t)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const double a = __shfl_sync(0xffffffffu, hr[t][e], (lane & 7) >> 1);
-        const double b = __shfl_sync(0xffffffffu, hi[t][e], (lane & 7) >> 1);
-        if (((lane >> 3) & 1) == t && (lane & 1) == e) { orr = a; oi = b; }
-      }
+    double orr, oi;
+    mma_finish(F, x, y, orr, oi);
     if (lane < 16 && act) {
       const GroupDesc d = plan.desc[grp];
       plan.mma_scratch[(size_t)(d.mma_slot + (p - d.mma_p0)) * plan.gsize + q] = make_double2(orr, oi);

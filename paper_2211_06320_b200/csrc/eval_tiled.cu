@@ -31,6 +31,7 @@
 #include "eval_tiled.cuh"
 #include "kernels.cuh"
 #include "tma.cuh"
+#include "mma_piece.cuh"
 
 namespace fpe {
 
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
       if (diag) {
         fpe_diag dg;
         dg.lambda = lam; dg.region = istar; dg.l = l; dg.r = r;
-        dg.kept = kept_count(P, l, r); dg.hard = hard; dg.cancel = INT32_MIN;
+        dg.kept = kept_count(P, l, r); dg.hard = hard; dg.cancel = INT32_MIN; dg.trusted = 0;
+        dg.err_exp = INT32_MIN; dg.pad = 0;
         diag[i] = dg;
       }
       if (hard) atomicAdd(hard_ctr, 1ull);
@@ -238,6 +240,28 @@ __device__ __forceinline__ void ring_release(Ring<CK>& R) {
   __syncwarp();
   ++R.g;
   if (R.q_next >= R.q_end) ring_issue_n(R, 1);
+}
+
+// The in-warp tensor-core pass of piece p for 16 points (x, y, act: the point of lane & 15, as in
+// k_eval_mma's warp layout): the piece's 64 chunks through this warp's ring, the same mma_piece.cuh
+// arithmetic as k_eval_mma, so the partial is bitwise k_eval_mma's.  Used only by groups whose items did
+// not fit the DMMA scratch (GroupDesc::mma_slot == kMmaInWarp); kept out of line (rare path).
+struct MmaPassOut {
+  Ring<FPE_C64> R;
+  double r, i;   // the partial of point lane (lanes 0..15)
+};
+__device__ __noinline__ MmaPassOut mma_pass_inwarp(Ring<FPE_C64> R, double x, double y, int act, int p) {
+  MmaFrag F;
+  mma_setup(F, x, y, act);
+  ring_begin(R, p * kPiece, p * kPiece + kPiece - 1);
+  for (int k = 0; k < kMmaPieceChunks; ++k) {
+    mma_chunk(F, ring_wait(R), k == 0);
+    ring_release(R);
+  }
+  MmaPassOut o;
+  mma_finish(F, x, y, o.r, o.i);
+  o.R = R;
+  return o;
 }
 
 // Horner over the coefficient range [lo, hi] (relative, descending) for the NP points of every lane:
@@ -468,7 +492,9 @@ __device__ __forceinline__ void load_group(Pts<NP>& S, uint32_t g, long long n, 
 // The Horner sums of piece p = [rlo, rhi] for the NP points of every lane (b = 0 on entry).  Points that
 // cover the whole piece on the tensor cores (mma_covers; complex fp64 coefficients) take k_eval_mma's
 // partial from its scratch instead; the others stream the part of the piece their windows need.
-template <int CK, int NP, bool CPLX>
+// INWARP (k_eval_overflow only): the group's tensor-core pieces did not fit the DMMA scratch and are run
+// here with k_eval_mma's arithmetic; k_eval_tiled never sees such groups, so its code has no DMMA path.
+template <int CK, int NP, bool CPLX, bool INWARP = false>
 __device__ __forceinline__ void eval_piece(Ring<CK>& R, const Pts<NP>& S, int rlo, int rhi, int p, const GroupDesc& d,
                                            const Plan& plan, typename Step<CK>::W (&br)[NP],
                                            typename Step<CK>::W (&bi)[NP]) {
@@ -494,11 +520,31 @@ __device__ __forceinline__ void eval_piece(Ring<CK>& R, const Pts<NP>& S, int rl
         ring_begin(R, v_lo, v_hi);
         stream_range<CK, NP, CPLX>(R, v_lo, v_hi, wl, wr, zr, zi, br, bi);
       }
-      const double2* scr = plan.mma_scratch + (size_t)(d.mma_slot + (p - d.mma_p0)) * plan.gsize;
       const int lane = threadIdx.x & 31;
+      if constexpr (!INWARP) {   // k_eval_mma's partials
+        const double2* scr = plan.mma_scratch + (size_t)(d.mma_slot + (p - d.mma_p0)) * plan.gsize;
 #pragma unroll
-      for (int j = 0; j < NP; ++j)
-        if (cov[j]) { const double2 v = __ldcg(scr + j * 32 + lane); br[j] = v.x; bi[j] = v.y; }
+        for (int j = 0; j < NP; ++j)
+          if (cov[j]) { const double2 v = __ldcg(scr + j * 32 + lane); br[j] = v.x; bi[j] = v.y; }
+      } else {
+      // DMMA scratch was full: the same passes in this warp, 16 points (positions 16 w .. 16 w + 15 of the
+      // group, w = 2 j + h) at a time, exactly k_eval_mma's layout
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        if (!__any_sync(0xffffffffu, cov[j])) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int src = 16 * h + (lane & 15);
+          const int act = __shfl_sync(0xffffffffu, cov[j] ? 1 : 0, src);
+          if (!__any_sync(0xffffffffu, act)) continue;
+          const double x = __shfl_sync(0xffffffffu, S.x[j], src), y = __shfl_sync(0xffffffffu, S.y[j], src);
+          const MmaPassOut o = mma_pass_inwarp(R, x, y, act, p);
+          R = o.R;
+          const double vr = __shfl_sync(0xffffffffu, o.r, lane & 15), vi = __shfl_sync(0xffffffffu, o.i, lane & 15);
+          if ((lane >> 4) == h && cov[j]) { br[j] = vr; bi[j] = vi; }
+        }
+      }
+      }
       return;
     }
   }
@@ -552,7 +598,7 @@ __device__ __forceinline__ void group_unpack(Pts<NP>& S, const GroupCtx<NP>& c, 
   }
 }
 
-template <int PK, int CK, int OK, int NP, typename Prefetch>
+template <int PK, int CK, int OK, int NP, typename Prefetch, bool INWARP = false>
 __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c, long long n, const PolyDev& P,
                                              const Plan& plan, PtOut* out, Prefetch prefetch) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
@@ -569,7 +615,7 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c,
     for (int p = p_hi; p >= p_lo; --p) {
       const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
       W br[NP], bi[NP];
-      eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, p, d, plan, br, bi);
+      eval_piece<CK, NP, CPLX, INWARP>(R, S, rlo, rhi, p, d, plan, br, bi);
 #pragma unroll
       for (int j = 0; j < NP; ++j)
         if (S.wl[j] <= S.wr[j] && S.wl[j] <= p * kPiece + kPiece - 1 && S.wr[j] >= p * kPiece)
@@ -685,9 +731,43 @@ __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(l
       group_load<PK, NP>(nx, gid(__shfl_sync(0xffffffffu, nxt, 0)), n, plan, rec, kmin);
       if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
     };
-    if (cur.d.npieces > 1) fetch_next();   // evaluated as parallel pieces (multi_piece)
+    if (cur.d.npieces > 1 || (cur.d.mma_np > 0 && cur.d.mma_slot == kMmaInWarp))
+      fetch_next();   // evaluated as parallel pieces (multi_piece), or by k_eval_overflow
     else single_group<PK, CK, OK, NP>(R, cur, n, P, plan, out, fetch_next);
     cur = nx;
+  }
+}
+
+// Groups whose tensor-core items did not fit the DMMA scratch (k_plan's overflow list): one warp per group,
+// every piece top-down as single_group does, the covered whole pieces by in-warp DMMA passes with
+// k_eval_mma's arithmetic (eval_piece<INWARP>) -- so these points get the bits they would get in any batch.
+// Launched after k_eval_tiled whenever tensor-core items are planned; exits at once when the list is empty.
+template <int PK, int CK, int OK, int NP>
+__global__ void __launch_bounds__(kWarps * 32) k_eval_overflow(long long n, PolyDev P, PtRec* rec, Plan plan) {
+  using CT = typename Step<CK>::CT;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t n_ovf = plan.mma_ctrs[2];
+  if (n_ovf == 0) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  CT* ring_buf = reinterpret_cast<CT*>(smem) + (size_t)wib * kStages * kChunk;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes<CK>()) + wib * kStages;
+  if (lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0};
+  PtOut* const out = reinterpret_cast<PtOut*>(rec);
+  const int kmin = (int)P.k_min;
+  for (;;) {
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(plan.mma_ctrs + 3, 1u);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= n_ovf) break;
+    GroupCtx<NP> c;
+    group_load<PK, NP>(c, plan.ovf_groups[it], n, plan, rec, kmin);
+    auto none = []() {};
+    single_group<PK, CK, OK, NP, decltype(none), true>(R, c, n, P, plan, out, none);
   }
 }
 
@@ -891,7 +971,7 @@ size_t tiled_ws_bytes(long long n) {
   return al256(n * sizeof(int2)) + al256(n * sizeof(uint2)) + al256(n * sizeof(PtRec)) + al256(n * 4) +
          al256(mma_cap(n) * sizeof(uint2)) + al256(mma_cap(n) * 128 * sizeof(double2)) +
          al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) +
-         al256(max_groups(n) * sizeof(GroupDesc)) + al256(max_groups(n) * sizeof(uint32_t)) +
+         al256(max_groups(n) * sizeof(GroupDesc)) + 2 * al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
 }
 
@@ -905,6 +985,14 @@ static int launch_eval_tiled_t(long long n, const PolyDev& P, PtRec* rec, const 
   const size_t smem = eval_smem<CK>();
   const int grid = persistent_grid(reinterpret_cast<const void*>(k_eval_tiled<PK, CK, OK, NP>), kWarps * 32, smem);
   k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(n, P, rec, plan);
+  return 1;
+}
+
+template <int PK, int CK, int OK, int NP>
+static int launch_eval_overflow_t(long long n, const PolyDev& P, PtRec* rec, const Plan& plan, cudaStream_t s) {
+  const size_t smem = eval_smem<CK>();
+  const int grid = persistent_grid(reinterpret_cast<const void*>(k_eval_overflow<PK, CK, OK, NP>), kWarps * 32, smem);
+  k_eval_overflow<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(n, P, rec, plan);
   return 1;
 }
 
@@ -961,7 +1049,8 @@ bool run_horner_tiled(int pk, const void* pts, long long n, const PolyDev& P, ui
 }
 
 int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
-              fpe_diag* diag, void* ws, unsigned long long* hard, Stage& st, cudaStream_t s) {
+              fpe_diag* diag, void* ws, unsigned long long* stats, Stage& st, cudaStream_t s) {
+  unsigned long long* hard = stats + kStatHard;
   char* p = static_cast<char*>(ws);
   int2* lr = reinterpret_cast<int2*>(p); p += al256(n * sizeof(int2));          // {l, r} of input point i
   uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += al256(n * 8);            // {key, rank in (CTA, bucket)}
@@ -973,11 +1062,13 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   Plan plan;
   plan.desc = reinterpret_cast<GroupDesc*>(p); p += al256(max_groups(n) * sizeof(GroupDesc));
   plan.gcnt = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
+  plan.ovf_groups = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
   plan.items = reinterpret_cast<uint2*>(p); p += al256(scratch_slots(n) * sizeof(uint2));
   plan.scratch = p; p += al256(scratch_slots(n) * 1024);
   plan.mma_items = reinterpret_cast<uint2*>(p); p += al256(mma_cap(n) * sizeof(uint2));
   plan.mma_scratch = reinterpret_cast<double2*>(p); p += al256(mma_cap(n) * 128 * sizeof(double2));
   plan.mma_cap = (uint32_t)mma_cap(n);
+  plan.stats = stats;
   plan.ctrs = reinterpret_cast<uint32_t*>(p);
   plan.mma_ctrs = plan.ctrs + 4;
   const int np = np_for(pk, P.cdt);
@@ -1021,6 +1112,11 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   }
 #undef FPE_EV
   st.mark("eval_tiled");
+  if (plan.mma_on) {   // groups whose tensor-core items overflowed the DMMA scratch (usually none)
+    if (pk == FPE_C64) le += launch_eval_overflow_t<FPE_C64, FPE_C64, NPFor<FPE_C64, FPE_C64>::OK, 4>(n, P, rec, plan, s);
+    else le += launch_eval_overflow_t<FPE_R64, FPE_C64, NPFor<FPE_R64, FPE_C64>::OK, 4>(n, P, rec, plan, s);
+    st.mark("eval_overflow");
+  }
   const long long blocks = std::min<long long>((n + 4 * 256 - 1) / (4 * 256), 148ll * 16);
   const PtOut* staged = reinterpret_cast<const PtOut*>(rec);
   switch (pk * 4 + P.cdt) {   // the output kind follows NPFor<PK, CK>::OK

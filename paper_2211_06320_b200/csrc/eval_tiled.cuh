@@ -13,9 +13,10 @@ constexpr int kChunk = kCoefPad;   // coefficients per TMA bulk copy / ring stag
 constexpr int kLongWin = 4096;     // windows longer than this sort into the "long" half of the key space
 
 size_t tiled_ws_bytes(long long n);
-// classify + sort + plan + evaluate (dense handles).  Returns the number of kernel launches or -1.
+// classify + sort + plan + evaluate (dense handles); stats: the call's kStat* counters (device).  Returns
+// the number of kernel launches or -1.
 int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
-              fpe_diag* diag, void* ws, unsigned long long* hard, Stage& st, cudaStream_t s);
+              fpe_diag* diag, void* ws, unsigned long long* stats, Stage& st, cudaStream_t s);
 // full Horner (dense handles) with the streaming evaluator; ctr: one device uint32 of scratch
 bool run_horner_tiled(int pk, const void* pts, long long n, const PolyDev& P, uint32_t* ctr, void* vals,
                       long long* exps, cudaStream_t s);

@@ -32,6 +32,18 @@ struct Header {
 };
 static_assert(sizeof(Header) == 256, "header must be 256 bytes");
 
+// Counters of one fpe_evaluate call, in the first kWsHeader bytes of its workspace (zeroed by the call on
+// its stream; fpe_workspace_stats / fpe_last_stats read them).
+constexpr size_t kWsHeader = 256;
+enum : int {
+  kStatHard = 0,          // lambdas within 2^-80 of an fp64 rounding boundary (Ziv test; counted when computed)
+  kStatMmaItems = 1,      // (group, piece) tensor-core items planned
+  kStatMmaInWarp = 2,     // ... of which the DMMA scratch could not hold: run in-warp by the vector evaluator
+  kStatPieceItems = 3,    // parallel vector pieces of long windows
+  kStatPieceSerial = 4,   // long-window groups evaluated serially (piece scratch full)
+  kStatCount = 5
+};
+
 // Kernel-side view of a handle.
 struct PolyDev {
   const int2* hull;
@@ -50,8 +62,6 @@ struct fpe_poly_s {
   int device = 0;
   void* dbuf = nullptr;                 // flat device buffer (owned)
   std::vector<int32_t> hk, hh;          // host copy of the cover
-  unsigned long long* dstats = nullptr; // device counters (hard-to-round lambdas)
-  long long last_launches = 0;
   // per-stage timing (fpe_set_profiling)
   bool profiling = false;
   void* prof_events[16] = {};

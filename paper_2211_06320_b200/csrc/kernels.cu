@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) k_classify(const void* __restrict__ pts, 
     if (diag) {
       fpe_diag d;
       d.lambda = lam; d.region = istar; d.l = l; d.r = r;
-      d.kept = kept_count(P, l, r); d.hard = hard; d.cancel = INT32_MIN;
+      d.kept = kept_count(P, l, r); d.hard = hard; d.cancel = INT32_MIN; d.trusted = 0; d.err_exp = INT32_MIN; d.pad = 0;
       diag[i] = d;
     }
     if (hard) atomicAdd(hard_ctr, 1ull);
@@ -184,15 +184,18 @@ __global__ void __launch_bounds__(128) k_horner_full(const void* __restrict__ pt
 
 // ------------------------------------------------------------------------------------------
 // Per-point confidence (eq:def_prec_loss; the errors file of P:2114-2118): after the
-// evaluation, c = ceil(N_lambda) - s(Q) with N_lambda = hh_i* + lambda hk_i* (the sheared cover's top,
-// log2 max_k |a_k z^k| in [N - 1, N]) and s(Q) the exact scale of the result (value = m 2^e with
-// max(|m_re|, |m_im|) in [1/2, 1): s = e + [m_re^2 + m_im^2 >= 1]).  Written into fpe_diag::cancel.
+// evaluation, c = max(0, ceil(N_lambda) - s(Q)) with N_lambda = hh_i* + lambda hk_i* (the sheared cover's
+// top, log2 max_k |a_k z^k| in [N - 1, N)) and s(Q) the exact scale of the result (value = m 2^e with
+// max(|m_re|, |m_im|) in [1/2, 1): s = e + [m_re^2 + m_im^2 >= 1]); c = 0 when |Q| >= M (the first case
+// of eq:def_prec_loss; ceil(N) >= s(M), so the clamp only removes the overestimate).  The error bound
+// err_exp and the trusted bits follow fpe.h (fpe_diag).  Written into the point's fpe_diag.
 template <int OK>
 __global__ void __launch_bounds__(256) k_confidence(long long n, PolyDev P, const void* __restrict__ vals,
                                                     const long long* __restrict__ exps, fpe_diag* __restrict__ diag) {
+  constexpr int pw = (OK == FPE_R32 || OK == FPE_C32) ? 24 : 53;   // working precision (bits)
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     fpe_diag d = diag[i];
-    int c = INT32_MIN;
+    int c = INT32_MIN, trusted = 0, eexp = INT32_MIN;
     if (d.region >= 0 && isfinite(d.lambda)) {
       double mr, mi;
       if constexpr (OK == FPE_R64) { mr = static_cast<const double*>(vals)[i]; mi = 0.0; }
@@ -200,17 +203,25 @@ __global__ void __launch_bounds__(256) k_confidence(long long n, PolyDev P, cons
       else if constexpr (OK == FPE_R32) { mr = static_cast<const float*>(vals)[i]; mi = 0.0; }
       else { const float2 v = static_cast<const float2*>(vals)[i]; mr = v.x; mi = v.y; }
       long long e = exps ? exps[i] : 0;
+      const int2 v = P.hull[d.region];
+      const double N = __fma_rn(d.lambda, (double)v.x, (double)v.y);
+      const double K = (double)max(d.kept, 1);
+      const double E = ceil(N) + ceil(log2(2.0 * K + 256.0)) + ceil(log2(K)) + 1.0 - pw;
+      eexp = (int)max(-2147483647.0, min(2147483647.0, E));
       const double m = fmax(fabs(mr), fabs(mi));
       if (m != 0.0 && isfinite(m)) {
         const int k = frexp_exp(m);       // renormalise (plain-float outputs)
         mr = ldexp(mr, -k); mi = ldexp(mi, -k); e += k;
         const long long sQ = e + ((__fma_rn(mr, mr, mi * mi) >= 1.0) ? 1 : 0);
-        const int2 v = P.hull[d.region];
-        const double N = __fma_rn(d.lambda, (double)v.x, (double)v.y);
-        c = (int)max(-2000000000.0, min(2000000000.0, ceil(N) - (double)sQ));
+        c = (int)max(0.0, min(2000000000.0, ceil(N) - (double)sQ));
+        trusted = (int)max(0.0, min((double)pw, (double)sQ - E));
       }
+    } else if (d.region >= 0) {   // z = 0: the value a_0 is exact
+      c = 0; trusted = pw; eexp = INT32_MIN;
     }
     diag[i].cancel = c;
+    diag[i].trusted = trusted;
+    diag[i].err_exp = eexp;
   }
 }
 

@@ -1,0 +1,151 @@
+// mma_piece.cuh -- the per-warp arithmetic of a whole kPiece piece on the FP64 tensor cores, shared by
+// k_eval_mma (eval_mma.cu: CTA-shared TMA ring, one warp per 16 points) and the vector evaluator's
+// in-warp fallback (eval_tiled.cu: a group whose tensor-core items did not fit the DMMA scratch runs the
+// same functions over its private ring).  Both call exactly these functions with the same per-point
+// inputs, so a point's piece partial is bitwise the same whichever kernel computed it: results stay a
+// pure function of (z, handle), whatever the batch (fpe.h).
+//
+// Phase split: over whole 256-coefficient chunks the piece sum is
+//   sum_{k in piece} a_k z^{k-k0} = sum_{m<16} z^m R_m,  R_m = sum_t a_{k0+16t+m} u^t,  u = z^16,
+// and chunk q is C <- C (.) w + A V with A[m][i] = a_{256q+16i+m}, V[i][p] = u_p^i, w_p = z_p^256.
+// Lane layout (m16n8k4 fragments): lanes 0..15 own the warp's 16 points (lanes 16..31 mirror them);
+// thread (g = lane >> 2, c = lane & 3) holds B rows c of the two 8-point column tiles t and C columns 2c, 2c+1.
+#pragma once
+#include <cuda_runtime.h>
+#include "fpe_math.cuh"
+#include "fpe_internal.h"
+#include "sort.cuh"
+
+namespace fpe {
+
+constexpr int kMmaPieceChunks = kPiece / kCoefPad;   // 256-coefficient chunks per piece
+// GroupDesc::mma_slot of a group whose tensor-core items did not fit the DMMA scratch: the vector
+// evaluator runs them in-warp (eval_tiled.cu mma_pass_inwarp)
+constexpr uint32_t kMmaInWarp = 0xffffffffu;
+
+__device__ __forceinline__ void mma_cmul(double& r, double& i, double ar, double ai, double br, double bi) {
+  const double t = fma(ar, br, -ai * bi);
+  i = fma(ar, bi, ai * br);
+  r = t;
+}
+__device__ __forceinline__ void mma_dmma(double (&c)[4], double a0, double a1, double b) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b));
+}
+__device__ __forceinline__ void mma_dd_sqr_c(xc_t& v) {
+  xc_sqr(v);
+  const dd_t r = two_sum(v.hr, v.er), i = two_sum(v.hi, v.ei);
+  v.hr = r.hi; v.er = r.lo; v.hi = i.hi; v.ei = i.lo;
+}
+
+// Fragments of one warp's 16 points for one piece.
+struct MmaFrag {
+  double vr[2][4], vi[2][4];     // B: u^(4 ks + c) of the column tiles (0 for inactive columns)
+  double cwr[2][2], cwi[2][2];   // w = z^256 of the C columns 2c, 2c + 1
+  double cr[2][4], ci[2][4];     // C: Re / Im of R_m (rows g, g + 8; columns 2c, 2c + 1)
+};
+
+// (x, y, act): the point of lane & 15 (act: it covers the piece, mma_covers).  u = z^16, u^4, w = z^256 by
+// double-double squarings, rounded once each.
+__device__ __forceinline__ void mma_setup(MmaFrag& F, double x, double y, int act) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+  double ur, ui, u4r, u4i, wwr, wwi;
+  {
+    xc_t v{act ? x : 1.0, act ? y : 0.0, 0.0, 0.0, 0};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mma_dd_sqr_c(v);
+    ur = v.hr + v.er; ui = v.hi + v.ei;
+    mma_dd_sqr_c(v); mma_dd_sqr_c(v);
+    u4r = v.hr + v.er; u4i = v.hi + v.ei;
+    mma_dd_sqr_c(v); mma_dd_sqr_c(v);
+    wwr = v.hr + v.er; wwi = v.hi + v.ei;
+  }
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int src = 8 * t + g;                   // the point of B column g
+    const double qr = __shfl_sync(0xffffffffu, ur, src), qi = __shfl_sync(0xffffffffu, ui, src);
+    const double q4r = __shfl_sync(0xffffffffu, u4r, src), q4i = __shfl_sync(0xffffffffu, u4i, src);
+    const int on = __shfl_sync(0xffffffffu, act, src);
+    double pr = 1.0, pi = 0.0;                   // u^c
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (i < c) mma_cmul(pr, pi, pr, pi, qr, qi);
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {             // B row c of k-step ks: u^(4 ks + c); inactive column: 0
+      if (ks) mma_cmul(pr, pi, pr, pi, q4r, q4i);
+      F.vr[t][ks] = on ? pr : 0.0;
+      F.vi[t][ks] = on ? pi : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {                // w of the C columns 2c, 2c + 1
+      const int s2 = 8 * t + 2 * c + e;
+      F.cwr[t][e] = __shfl_sync(0xffffffffu, wwr, s2);
+      F.cwi[t][e] = __shfl_sync(0xffffffffu, wwi, s2);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { F.cr[t][e] = 0.0; F.ci[t][e] = 0.0; }
+  }
+}
+
+// One 256-coefficient chunk (cb: its first coefficient; chunks are fed highest first, `first` for the
+// piece's top chunk): C <- C (.) w + A V.
+__device__ __forceinline__ void mma_chunk(MmaFrag& F, const double2* cb, bool first) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+  if (!first) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) mma_cmul(F.cr[t][e], F.ci[t][e], F.cr[t][e], F.ci[t][e], F.cwr[t][e & 1], F.cwi[t][e & 1]);
+  }
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const double2 a0 = cb[64 * ks + 16 * c + g], a1 = cb[64 * ks + 16 * c + g + 8];   // A[g|g+8][4ks + c]
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      mma_dmma(F.cr[t], a0.x, a1.x, F.vr[t][ks]);      // Re: ar vr - ai vi
+      mma_dmma(F.cr[t], -a0.y, -a1.y, F.vi[t][ks]);
+      mma_dmma(F.ci[t], a0.x, a1.x, F.vi[t][ks]);      // Im: ar vi + ai vr
+      mma_dmma(F.ci[t], a0.y, a1.y, F.vr[t][ks]);
+    }
+  }
+}
+
+// sum_m z^m R_m for the warp's 16 points: rows g and g + 8 in the thread, then a tree over g (lane bits
+// 2..4).  (x, y): the point of lane & 15.  The result of point lane is returned in lanes 0..15.
+__device__ __forceinline__ void mma_finish(const MmaFrag& F, double x, double y, double& orr, double& oi) {
+  const int lane = threadIdx.x & 31, c = lane & 3;
+  double hr[2][2], hi[2][2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int src = 8 * t + 2 * c + e;
+      const double zr = __shfl_sync(0xffffffffu, x, src), zi = __shfl_sync(0xffffffffu, y, src);
+      double z2r, z2i, z4r, z4i, z8r, z8i;
+      mma_cmul(z2r, z2i, zr, zi, zr, zi);
+      mma_cmul(z4r, z4i, z2r, z2i, z2r, z2i);
+      mma_cmul(z8r, z8i, z4r, z4i, z4r, z4i);
+      double pr = F.cr[t][e], pi = F.ci[t][e];
+      pr = fma(F.cr[t][e + 2], z8r, fma(-F.ci[t][e + 2], z8i, pr));
+      pi = fma(F.cr[t][e + 2], z8i, fma(F.ci[t][e + 2], z8r, pi));
+      double nr = __shfl_xor_sync(0xffffffffu, pr, 4), ni = __shfl_xor_sync(0xffffffffu, pi, 4);
+      pr = fma(nr, zr, fma(-ni, zi, pr)); pi = fma(nr, zi, fma(ni, zr, pi));
+      nr = __shfl_xor_sync(0xffffffffu, pr, 8); ni = __shfl_xor_sync(0xffffffffu, pi, 8);
+      pr = fma(nr, z2r, fma(-ni, z2i, pr)); pi = fma(nr, z2i, fma(ni, z2r, pi));
+      nr = __shfl_xor_sync(0xffffffffu, pr, 16); ni = __shfl_xor_sync(0xffffffffu, pi, 16);
+      pr = fma(nr, z4r, fma(-ni, z4i, pr)); pi = fma(nr, z4i, fma(ni, z4r, pi));
+      hr[t][e] = pr; hi[t][e] = pi;              // valid in lanes 0..3 (g = 0)
+    }
+  orr = 0.0; oi = 0.0;
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const double a = __shfl_sync(0xffffffffu, hr[t][e], (lane & 7) >> 1);
+      const double b = __shfl_sync(0xffffffffu, hi[t][e], (lane & 7) >> 1);
+      if (((lane >> 3) & 1) == t && (lane & 1) == e) { orr = a; oi = b; }
+    }
+}
+
+}  // namespace fpe

@@ -14,6 +14,7 @@
 #include <cstdint>
 #include "sort.cuh"
 #include "fpe_internal.h"
+#include "mma_piece.cuh"
 
 namespace fpe {
 
@@ -129,22 +130,29 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const PtRec* __restri
   d.mma_p0 = 0; d.mma_np = 0; d.mma_slot = 0; d.pad = 0;
   if (clo <= chi) {
     const int np = chi - clo + 1;
+    d.mma_p0 = clo; d.mma_np = np;
+    atomicAdd(plan.stats + kStatMmaItems, (unsigned long long)np);
     const uint32_t base = atomicAdd(plan.mma_ctrs, (uint32_t)np);
     if ((unsigned long long)base + np <= plan.mma_cap) {
-      d.mma_p0 = clo; d.mma_np = np; d.mma_slot = base;
+      d.mma_slot = base;
       for (int i = 0; i < np; ++i) plan.mma_items[base + i] = make_uint2((uint32_t)g, (uint32_t)(clo + i));
-    } else {   // DMMA scratch exhausted: these pieces stay on the vector path
+    } else {   // DMMA scratch exhausted: k_eval_overflow runs the same DMMA passes in-warp (bitwise equal)
+      d.mma_slot = kMmaInWarp;
+      atomicAdd(plan.stats + kStatMmaInWarp, (unsigned long long)np);
+      plan.ovf_groups[atomicAdd(plan.mma_ctrs + 2, 1u)] = (uint32_t)g;
       for (uint32_t i = base; i < plan.mma_cap && i < base + (uint32_t)np; ++i) plan.mma_items[i] = make_uint2(~0u, 0u);
     }
   }
-  if (hi >= lo && hi - lo + 1 > kPiece) {
+  if (hi >= lo && hi - lo + 1 > kPiece && d.mma_slot != kMmaInWarp) {   // (overflow groups: one warp each)
     const int np = hi / kPiece - lo / kPiece + 1;
     const uint32_t base = atomicAdd(plan.ctrs + 2, (uint32_t)np);
     if ((unsigned long long)base + np <= plan.cap) {
       d.slot = base; d.npieces = np;
       plan.gcnt[g] = 0;
+      atomicAdd(plan.stats + kStatPieceItems, (unsigned long long)np);
       for (int i = 0; i < np; ++i) plan.items[base + i] = make_uint2((uint32_t)g, (uint32_t)(lo / kPiece + i));
     } else {   // scratch exhausted: evaluated serially by one warp (bitwise the same result)
+      atomicAdd(plan.stats + kStatPieceSerial, 1ull);
       for (uint32_t i = base; i < plan.cap && i < base + (uint32_t)np; ++i) plan.items[i] = make_uint2(~0u, 0u);
     }
   }

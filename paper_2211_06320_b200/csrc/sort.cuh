@@ -78,9 +78,11 @@ struct Plan {
   // tensor-core pieces (complex fp64 coefficients only)
   int mma_on;             // 1: plan them
   uint2* mma_items;       // [mma_cap] (group, piece)
-  uint32_t* mma_ctrs;     // [0] slots reserved, [1] items fetched
+  uint32_t* mma_ctrs;     // [0] slots reserved, [1] items fetched, [2] overflow groups, [3] ... fetched
+  uint32_t* ovf_groups;   // [max_groups] groups whose items did not fit the scratch (k_eval_overflow)
   double2* mma_scratch;   // [mma_cap][gsize] partial sums of covered points, origin = piece start
   uint32_t mma_cap;
+  unsigned long long* stats;   // the call's counters (workspace header, kStat*)
 };
 
 // bucket starts (k_bucket_scan), records and points in bucket order (k_bucket_scatter), and the work plan

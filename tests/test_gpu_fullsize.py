@@ -1,0 +1,143 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times (one fpe_evaluate
+over the whole batch), against the oracle:
+
+- indexing (lambda, region = k_lambda vertex, l, r, K) bit-exact on EVERY point of cfg2, cfg3, cfg4, cfg5
+  and cfg5-fp32 (the oracle classifies the host copy of the same points chunk by chunk);
+- values against the plain definition P_ref = the oracle's full double-double Horner (cfg4: the direct
+  sum of its 4096 nonzero terms) on seeded subsamples of 2^12 (cfg2), 2^10 (cfg3), 2^10 (cfg4), 2^9 (cfg5):
+  |P_gpu - P_ref| <= 2^-45 S (fp64) or 2^-16 S (fp32), S = sum_k |a_k||z|^k (BASELINE.json north_star);
+- sharding: 2^28 cfg5 points evaluated as 8 contiguous shards of 2^25 give the unsharded run's bits
+  (SURVEY.md §8(c) "sharding" pin; per-point purity, fpe.h).
+
+The maximum err/S per config is printed (pytest -s shows it).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from parity import abs_sum_log2, rel_err_vs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL64 = 2.0 ** -45
+TOL32 = 2.0 ** -16
+CHUNK = 1 << 22
+
+# (cfg, fp32, value-sample size)
+FULL = [(2, False, 1 << 12), (3, False, 1 << 10), (4, False, 1 << 10), (5, False, 1 << 9), (5, True, 1 << 9)]
+
+
+@pytest.fixture(scope="module")
+def fpe():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2211_06320_b200 import build
+    build.build()
+    import paper_2211_06320_b200 as m
+    return m
+
+
+@pytest.mark.parametrize("cfg,fp32,n_val", FULL, ids=[f"cfg{c}{'_fp32' if f else ''}" for c, f, _ in FULL])
+def test_full_size(fpe, cfg, fp32, n_val):
+    a = workloads.coefficients(cfg)
+    pts = workloads.points(cfg)
+    if fp32:
+        a, pts = workloads.to_fp32(a), workloads.to_fp32(pts)
+    n = len(pts)
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    t = torch.from_numpy(pts).cuda()
+    v, e, dg = poly.evaluate(t, exps=True, diag=True)
+    st = poly.workspace_stats()
+    del t
+    D = fpe.diag_fields(dg)
+    # -- indexing on every point ------------------------------------------------------------------------
+    nbad = 0
+    hard = 0
+    for lo in range(0, n, CHUNK):
+        hi = min(n, lo + CHUNK)
+        g = {k: x[lo:hi].cpu().numpy() for k, x in D.items() if k in ("lambda", "region", "l", "r", "kept", "hard")}
+        c = P.classify(pts[lo:hi])
+        ok = c["l"] >= 0
+        bad = (g["region"] != c["istar"]) | (ok & ((g["lambda"] != c["lam"]) | (g["l"] != c["l"]) |
+                                                   (g["r"] != c["r"]) | (g["kept"] != c["K"])))
+        if bad.any():
+            i = int(np.flatnonzero(bad)[0])
+            raise AssertionError(f"cfg{cfg}: indexing mismatch at point {lo + i}: gpu (lam {g['lambda'][i]!r}, "
+                                 f"i* {g['region'][i]}, l {g['l'][i]}, r {g['r'][i]}, K {g['kept'][i]}) oracle "
+                                 f"(lam {c['lam'][i]!r}, i* {c['istar'][i]}, l {c['l'][i]}, r {c['r'][i]}, "
+                                 f"K {c['K'][i]}); {int(bad.sum())} in this chunk")
+        nbad += int(bad.sum())
+        hard += int(c["hard"].sum()) + int(g["hard"].sum())
+    assert nbad == 0 and hard == 0
+    # -- values against the full Horner (plain definition) on a seeded subsample --------------------------
+    idx = workloads.sample_indices(n, n_val, salt=100 + cfg + 10 * fp32)
+    it = torch.from_numpy(idx).cuda()
+    out_v, out_e = v[it].cpu().numpy(), e[it].cpu().numpy()
+    del v, e, dg, D
+    torch.cuda.empty_cache()
+    sub = pts[idx]
+    ref = P.direct_sum(sub) if cfg == 4 else P.horner_dd(sub)
+    l2S = abs_sum_log2(a, sub)
+    err = rel_err_vs(ref, out_v, out_e, l2S)
+    tol = TOL32 if fp32 else TOL64
+    fin = np.isfinite(l2S)
+    print(f"\ncfg{cfg}{'_fp32' if fp32 else ''}: {n} points indexed bit-exact; max |P_gpu - P_ref|/S over "
+          f"{len(idx)} points = 2^{np.log2(max(err[fin].max(), 2.0 ** -200)):.1f} (tolerance 2^{np.log2(tol):.0f}); "
+          f"counters {st}")
+    assert np.all(err[fin] <= tol), (err[fin].max(), idx[np.argmax(np.where(fin, err, 0))])
+    assert st["hard_lambdas"] == 0
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+def test_sharding_bitwise_cfg5(fpe, fp32):
+    """2^28 cfg5 points: the unsharded evaluation and 8 contiguous shards of 2^25 (dist.shard_range, as each
+    of 8 ranks would evaluate them) give the same bits, values and exponents."""
+    from paper_2211_06320_b200 import dist as fdist
+    a = workloads.coefficients(5)
+    pts = workloads.points(5)
+    if fp32:
+        a, pts = workloads.to_fp32(a), workloads.to_fp32(pts)
+    poly = fpe.precondition(a)
+    t = torch.from_numpy(pts).cuda()
+    del pts
+    v, e = poly.evaluate(t, exps=True)
+    full_stats = poly.workspace_stats()
+    n = t.numel()
+    for r in range(8):
+        lo, hi = fdist.shard_range(n, r, 8)
+        vs, es = poly.evaluate(t[lo:hi], exps=True)
+        assert torch.equal(vs, v[lo:hi]) and torch.equal(es, e[lo:hi]), f"shard {r} differs"
+    print(f"\ncfg5{'_fp32' if fp32 else ''}: 8 shards bitwise equal to the unsharded run; counters {full_stats}")
+
+
+def test_mma_overflow_bitwise(fpe):
+    """Points near |z| = 1 on cfg3's polynomial have windows of ~10^5 coefficients (several whole
+    tensor-core pieces each); a batch of 2000 of them asks for more tensor-core items than its workspace's
+    DMMA scratch holds, so some groups run the DMMA passes in-warp (k_eval_overflow).  Every point must get
+    the bits it gets when evaluated in batches of 16 (no overflow), and two runs must agree."""
+    a = workloads.coefficients(3)
+    rng = np.random.default_rng(63)
+    n = 2000
+    r = np.exp2(rng.uniform(-2.0 ** -12, 2.0 ** -12, n))
+    pts = r * np.exp(1j * rng.uniform(0, 2 * np.pi, n))
+    poly = fpe.precondition(a)
+    t = torch.from_numpy(pts).cuda()
+    v1, e1 = poly.evaluate(t, exps=True)
+    st = poly.workspace_stats()
+    assert st["mma_inwarp_items"] > 0 and st["mma_items"] > st["mma_inwarp_items"], st
+    v2, e2 = poly.evaluate(t, exps=True)
+    assert torch.equal(v1, v2) and torch.equal(e1, e2)
+    for lo in range(0, n, 16):
+        vs, es = poly.evaluate(t[lo:lo + 16], exps=True)
+        assert poly.workspace_stats()["mma_inwarp_items"] == 0
+        assert torch.equal(vs, v1[lo:lo + 16]) and torch.equal(es, e1[lo:lo + 16]), lo
+    # real points on the same polynomial (complex coefficients, real z)
+    tr = torch.from_numpy(r * rng.choice([-1.0, 1.0], n)).cuda()
+    w1, f1 = poly.evaluate(tr, exps=True)
+    assert poly.workspace_stats()["mma_inwarp_items"] > 0
+    for lo in range(0, n, 16):
+        ws_, fs = poly.evaluate(tr[lo:lo + 16], exps=True)
+        assert torch.equal(ws_, w1[lo:lo + 16]) and torch.equal(fs, f1[lo:lo + 16]), lo

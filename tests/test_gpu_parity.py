@@ -277,15 +277,19 @@ def test_diag_and_plain_paths_agree(fpe):
 
 
 def test_confidence_cancel_bits(fpe):
-    """fpe_diag::cancel (PAPER.md:1278-1285, eq:def_prec_loss): c = s(M) - s(P(z)), M = max_k |a_k z^k|.
-    The library estimates s(M) by ceil(N_lambda) (log2 M in [N - 1, N]) and takes s of its own result;
-    against the oracle's s(M) and s(P_ref) it may differ by 1 for each estimate."""
+    """fpe_diag::cancel (PAPER.md:1278-1285, eq:def_prec_loss): c = 0 if |P(z)| >= M, else s(M) - s(P(z)),
+    M = max_k |a_k z^k|.  The library estimates s(M) by ceil(N_lambda) (log2 M in [N - 1, N)) and takes s of
+    its own result; against the oracle's s(M) and s(P_ref) it may differ by 1 for each estimate.  The error
+    bound err_exp must hold against the oracle's full Horner, and trusted = s(Q) - err_exp (clamped)."""
     cases = [(workloads.coefficients(1), workloads.points(1, 4096, shard=4))]
     # heavy cancellation: (z - 1)^40 near z = 1 loses many bits
     from math import comb
     a = np.array([comb(40, k) * (-1.0) ** (40 - k) for k in range(41)], dtype=np.complex128)
     zc = 1 + 2.0 ** -np.arange(1, 30) * np.exp(1j * np.linspace(0, 6, 29))
     cases.append((a, np.concatenate([zc, workloads.points(1, 500, shard=5)])))
+    # a dominant term: |P(z)| >= M happens (c = 0 by the first case of eq:def_prec_loss)
+    b = np.zeros(30, np.complex128); b[0] = 1.0; b[29] = 1e-3
+    cases.append((b, workloads.points(1, 500, shard=6) * 0.5))
     for a, pts in cases:
         poly = fpe.precondition(a)
         P = oracle.OraclePoly(a)
@@ -294,10 +298,23 @@ def test_confidence_cancel_bits(fpe):
         H = P.horner(pts)
         sP = H.e + (np.abs(H.hi) >= 1.0)
         sM = 1 + np.floor(P.log2_maxterm(pts)).astype(np.int64)
-        c_ref = sM - sP
-        ok = np.isfinite(P.log2_maxterm(pts)) & (c_ref < 40)
+        l2M = P.log2_maxterm(pts)
+        absP_ge_M = (np.log2(np.abs(H.hi)) + H.e) >= l2M
+        c_ref = np.where(absP_ge_M, 0, sM - sP)
+        ok = np.isfinite(l2M) & (c_ref < 40)
+        assert np.all(c_gpu[ok] >= 0)
         assert np.all(np.abs(c_gpu[ok] - c_ref[ok]) <= 2), (c_gpu[ok][:10], c_ref[ok][:10])
         assert np.any(c_ref[ok] > 10) or a.shape[0] != 41   # the (z-1)^40 case does exercise cancellation
+        # the error bound holds: |P_gpu - P_ref| <= 2^err_exp (relative to 2^err_exp, exponents aligned)
+        ee = out["diag"]["err_exp"].astype(np.int64)
+        sh = np.clip(out["e"] - ee, -2000, 2000)
+        g = np.ldexp(out["v"].real, sh) + 1j * np.ldexp(out["v"].imag, sh)
+        diff = np.abs(g - H.scaled(ee))
+        assert np.all(diff[ok] <= 1.0), diff[ok].max()
+        sQ = out["e"] + (np.abs(out["v"]) >= 1.0)
+        tr = out["diag"]["trusted"]
+        assert np.all(tr == np.clip(sQ - ee, 0, 53))
+        assert np.median(tr[ok & (c_ref == 0)]) >= 20 or a.shape[0] == 41
 
 
 def test_newton_step_paper_example(fpe):
@@ -533,7 +550,7 @@ def test_analyse_intervals(fpe, worked):
 def test_tensor_core_pieces_and_overflow(fpe, real_points):
     """Points near |z| = 1 on cfg3's polynomial have windows of 10^5 coefficients: most pieces are covered
     whole and go to k_eval_mma; 400 points (4 groups) request more DMMA items than the small batch's
-    scratch holds (64), so some groups fall back to the vector Horner.  Indexing exact, values within
+    scratch holds (64), so some groups run them in-warp (k_eval_overflow).  Indexing exact, values within
     2^-45 S, against the oracle; complex and real points."""
     a = workloads.coefficients(3)
     P = oracle.OraclePoly(a)
@@ -638,3 +655,54 @@ def test_batch_slicing_above_2_28(fpe):
     _values_ok(P, a, pts, out, np.arange(len(idx)), TOL64, cls)
     alone = gpu_eval(poly, pts)
     assert np.array_equal(alone["v"], out["v"]) and np.array_equal(alone["e"], out["e"])
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+def test_coherent_long_windows(fpe, fp32):
+    """Coherent terms (a_k = 1, d = 2^20 - 1) at z within 2^-14 of 1 with small argument, complex and real:
+    every term has nearly the same phase, so the Horner rounding errors of a 16384-coefficient piece add up
+    like sum_j u |b_j| instead of cancelling at random -- the hardest case for the window evaluator's
+    accuracy, against the oracle's full binary128 Horner (the plain definition), tolerance 2^-45 S (fp64) /
+    2^-16 S (fp32).  Complex points take the tensor-core pieces (k_eval_mma) in fp64."""
+    d = (1 << 20) - 1
+    a = np.ones(d + 1, np.complex128)
+    rng = np.random.default_rng(71)
+    m = 24
+    eps = rng.uniform(-2.0 ** -14, 2.0 ** -14, m)
+    th = rng.uniform(-2.0 ** -14, 2.0 ** -14, m)
+    zc = (1 + eps) * np.exp(1j * th)
+    zc[:4] = [1.0, 1 + 2.0 ** -14, 1 - 2.0 ** -14, np.exp(1j * 2.0 ** -14)]
+    zr = 1 + rng.uniform(-2.0 ** -14, 2.0 ** -14, m)
+    tol = TOL32 if fp32 else TOL64
+    worst = {}
+    for kind, pts, coef in (("complex", zc, a), ("real", zr, a.real.copy())):
+        if fp32:
+            coef, pts = workloads.to_fp32(coef), workloads.to_fp32(pts)
+        poly = fpe.precondition(coef)
+        P = oracle.OraclePoly(coef)
+        out = gpu_eval(poly, pts)
+        check_indexing(P, pts, out["diag"])
+        H = P.horner_dd(pts)
+        l2S = abs_sum_log2(coef, pts)
+        err = rel_err_vs(H, out["v"], out["e"], l2S)
+        worst[kind] = float(np.log2(max(err.max(), 2.0 ** -200)))
+        assert np.all(err <= tol), (kind, err.max())
+    print(f"\ncoherent a_k = 1, d = 2^20 - 1, {'fp32' if fp32 else 'fp64'}: max err/S = 2^{worst}")
+
+
+def test_cfg5_fp32_near_unit_circle(fpe):
+    """cfg5-fp32 (d = 2^22 - 1, the longest fp32 windows: ~4 10^5 terms) at points within 2^-12 of
+    |z| = 1: values against the oracle's full Horner within 2^-16 S."""
+    a = workloads.to_fp32(workloads.coefficients(5))
+    rng = np.random.default_rng(72)
+    m = 48
+    pts = workloads.to_fp32(np.exp2(rng.uniform(-2.0 ** -12, 2.0 ** -12, m)) * np.exp(1j * rng.uniform(0, 2 * np.pi, m)))
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    out = gpu_eval(poly, pts)
+    cls = check_indexing(P, pts, out["diag"])
+    assert np.median(cls["K"]) > 1e5
+    H = P.horner_dd(pts)
+    err = rel_err_vs(H, out["v"], out["e"], abs_sum_log2(a, pts))
+    print(f"\ncfg5-fp32 near |z| = 1: median K = {int(np.median(cls['K']))}, max err/S = 2^{np.log2(err.max()):.1f}")
+    assert np.all(err <= TOL32), err.max()
