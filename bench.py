@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """bench.py -- FPE multi-point evaluation throughput on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fpe|reference] [--config 3]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fpe|reference] [--config 3] [--fp32]
     torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
 
 A step is one pass of the whole hot path -- fpe_evaluate: classification (lambda, k_lambda,
@@ -10,7 +10,10 @@ already resident in HBM.  Workload (default): BASELINE.json configs[2], complex 
 d = 2^20 - 1, |a_k| = 2^(200 sin(pi k/d) + N(0,4)), 2^26 points uniform on the Riemann
 sphere per rank (weak scaling: every rank evaluates its own 2^26-point batch; the
 preconditioned polynomial is replicated once with an NCCL broadcast, untimed).
-Points (1 GiB/rank) exceed the 126 MB L2, so no flush is needed between steps.
+--config 5 [--fp32] is BASELINE.json configs[4], the scaling run: complex fp64 (or fp32)
+d = 2^22 - 1, N = 2^28 points in total, each rank evaluating its contiguous shard of
+ceil(N/G) points (strong scaling; every rank generates exactly its slice of the seeded
+sequence).  Points exceed the 126 MB L2, so no flush is needed between steps.
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -39,7 +42,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fpe", choices=["fpe", "reference"])
     ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--points", type=int, default=0, help="override points per rank")
+    ap.add_argument("--fp32", action="store_true", help="the fp32 variant (coefficients and points rounded)")
+    ap.add_argument("--points", type=int, default=0,
+                    help="override points per rank (weak scaling) or in total (--config 5, strong scaling)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0)
@@ -99,13 +104,15 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     pg = None
-    if world > 1:
-        import torch.distributed as dist
-        backend = "nccl" if args.impl == "fpe" else "gloo"
-        dist.init_process_group(backend=backend)
-        pg = dist
     if args.impl == "fpe":
         torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        if args.impl == "fpe":   # bind the NCCL communicator to this rank's GPU (eager init)
+            dist.init_process_group(backend="nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend="gloo")
+        pg = dist
     return world, rank, local, pg
 
 
@@ -138,7 +145,7 @@ def algorithmic_fma(diag_fields, cplx: bool) -> float:
     return float((c * (K + pw)).sum())
 
 
-def cpu_baseline(cfg: int, sample: int):
+def cpu_baseline(cfg: int, sample: int, fp32: bool = False):
     """The oracle as it stands (oracle/, binary128, OpenMP over all host cores), timed on a
     bounded sample of the same workload: classification + Q_lambda for `sample` points."""
     import numpy as np
@@ -146,10 +153,14 @@ def cpu_baseline(cfg: int, sample: int):
     import oracle
     import workloads
     a = workloads.coefficients(cfg)
+    if fp32:
+        a = workloads.to_fp32(a)
     t0 = time.perf_counter()
     P = oracle.OraclePoly(a)
     t_pre = time.perf_counter() - t0
     pts = workloads.points(cfg, sample, shard=977)
+    if fp32:
+        pts = workloads.to_fp32(pts)
     t0 = time.perf_counter()
     c = P.classify(pts)
     P.fpe_eval(pts, c)
@@ -271,8 +282,10 @@ def run_reference(args):
     cfg = args.config
     sample = args.cpu_sample or 8192
     a = workloads.coefficients(cfg)
-    P = oracle.OraclePoly(a)
     pts = workloads.points(cfg, sample, shard=977)
+    if args.fp32:
+        a, pts = workloads.to_fp32(a), workloads.to_fp32(pts)
+    P = oracle.OraclePoly(a)
     for _ in range(args.warmup):
         P.fpe_eval(pts[:64], P.classify(pts[:64]))
     times = []
@@ -284,9 +297,11 @@ def run_reference(args):
     val = sample / (ms * 1e-3)
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     line = {"metric": METRIC, "value": val, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if cfg == 5 else "weak",
             "vs_baseline": None, "dtype": "f128", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workloads.CONFIGS[cfg]["name"], "points_per_step": sample, "sample": True},
+            "config": {"workload": workloads.CONFIGS[cfg]["name"] + ("_fp32" if args.fp32 else ""),
+                       "points_per_step": sample, "sample": True},
             "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": "oracle",
                              "sample": f"{sample} points of cfg{cfg} per step (binary128 oracle)"},
             "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -324,21 +339,34 @@ def run_fpe(args):
     dev = torch.device("cuda", local)
     cfg = args.config
     c = workloads.CONFIGS[cfg]
-    n = args.points or c["n_points"]
+    fp32 = bool(args.fp32)
+    strong = cfg == 5   # BASELINE configs[4]: N points in total, sharded by point
+    if strong:
+        n_total = args.points or c["n_points"]
+        lo, hi = fdist.shard_range(n_total, rank, world)
+        n = hi - lo
+        pts_np = workloads.points(cfg, n, start=lo)
+    else:
+        n = args.points or c["n_points"]
+        pts_np = workloads.points(cfg, n, shard=rank)
+    if fp32:
+        pts_np = workloads.to_fp32(pts_np)
     # -- replicate the preconditioned polynomial (rank 0 builds, NCCL broadcast; untimed) --
     poly = None
     if rank == 0:
-        poly = fpe.precondition(workloads.coefficients(cfg), device=local)
+        a = workloads.coefficients(cfg)
+        poly = fpe.precondition(workloads.to_fp32(a) if fp32 else a, device=local)
     poly = fdist.replicate(poly, src=0, device=local) if pg is not None else poly
     cplx = c["dtype"].startswith("c")
-    pts_np = workloads.points(cfg, n, shard=rank)
     pts = torch.from_numpy(pts_np).to(dev)
-    vals = torch.empty(n, dtype=torch.complex128 if cplx else torch.float64, device=dev)
+    vdt = (torch.complex64 if cplx else torch.float32) if fp32 else (torch.complex128 if cplx else torch.float64)
+    vals = torch.empty(n, dtype=vdt, device=dev)
     exps = torch.empty(n, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
+    ws = poly.workspace(n, stream)
 
     def step():
-        poly.evaluate(pts, exps=True, out=vals)
+        poly.evaluate(pts, exps=True, out=vals, workspace=ws)
 
     # algorithmic work from one untimed diagnostic pass
     _, _, dg = poly.evaluate(pts, exps=True, diag=True)
@@ -373,6 +401,7 @@ def run_fpe(args):
     total_points = reduce_sum(pg, float(n), dev)
     value = total_points / (ms * 1e-3)
     launches = poly.last_stats()["launches"]
+    counters = poly.workspace_stats(ws, stream)
 
     # -- per-kernel durations, live, on the launch stream (profiling events) --------------------
     poly.set_profiling(True)
@@ -385,11 +414,11 @@ def run_fpe(args):
     stages = {k: statistics.mean(v) for k, v in stage_acc.items()}
     # the window evaluator: the tensor-core pieces (k_eval_mma) and the vector Horner (k_eval_tiled)
     # together do the algorithmic work, so the roofline takes their summed duration
-    ev_keys = [k for k in ("eval_mma", "eval_tiled") if k in stages]
+    ev_keys = [k for k in ("eval_mma", "eval_tiled", "eval_overflow") if k in stages]
     dom = "+".join(ev_keys) if ev_keys else max(stages, key=stages.get)
     dom_ms = sum(stages[k] for k in ev_keys) if ev_keys else stages[dom]
     achieved = 2.0 * fma_total / (dom_ms * 1e-3) / 1e12        # TFLOP/s (2 flops per FMA)
-    peak = 2.0 * FP64_FMA_PEAK / 1e12
+    peak = 2.0 * FP64_FMA_PEAK * (2 if fp32 else 1) / 1e12   # fp32: 128 FMA lanes / SM / clk
 
     # -- end to end through the public API with host buffers (pinned) ---------------------------
     e2e = None
@@ -397,7 +426,7 @@ def run_fpe(args):
         hp = torch.from_numpy(pts_np).pin_memory()
         hv = torch.empty(n, dtype=vals.dtype).pin_memory()
         he = torch.empty(n, dtype=torch.int64).pin_memory()
-        pdt = 1 if cplx else 0
+        pdt = (3 if cplx else 2) if fp32 else (1 if cplx else 0)
         poly.evaluate_host_ptr(hp.data_ptr(), pdt, n, hv.data_ptr(), he.data_ptr())
         if pg is not None:
             pg.barrier()
@@ -413,7 +442,7 @@ def run_fpe(args):
         return
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cpu = cpu_baseline(cfg, args.cpu_sample or 65536)
+        cpu = cpu_baseline(cfg, args.cpu_sample or 65536, fp32)
     context = None
     if not args.no_extra and world == 1:
         del pts, vals, exps
@@ -421,21 +450,25 @@ def run_fpe(args):
         context = extra_context(local)
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": c["name"], "points_per_gpu": n, "degree": c["d"], "parallelism": f"points x{world}",
-                   "l2": "inputs (1 GiB/rank) larger than L2; no flush", "mean_kept_terms": meanK,
-                   "kept_terms": kept_stats,
-                   "hard_lambdas": hard},
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": "f32" if fp32 else "f64", "data": "synthetic",
+        "config": {"workload": c["name"] + ("_fp32" if fp32 else ""), "points_per_gpu": n,
+                   "points_total": int(total_points), "degree": c["d"],
+                   "parallelism": f"points x{world}" + (" (contiguous shards of N)" if strong else ""),
+                   "l2": f"inputs ({n * pts.element_size() / 2**30:.2f} GiB/rank) larger than L2; no flush",
+                   "mean_kept_terms": meanK, "kept_terms": kept_stats, "hard_lambdas": hard,
+                   "counters": counters},
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak,
-                     "traffic": (profiled_traffic() or {}).get("bytes"),
+                     "traffic": (profiled_traffic() or {}).get("bytes") if (cfg == 3 and not fp32) else None,
                      "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of k_eval_mma + k_eval_tiled "
                                      "(profiles/r01_ncu_eval_tiled_cfg3.json): it reads the 32-B bucket-order records "
                                      f"and writes its 32-B results over them ({64 * n / 1e9:.2f} GB); the path's "
                                      f"algorithmic bytes are 40 B/pt = {40 * n / 1e9:.2f} GB (points in, values and "
                                      "exponents out, the latter written by k_unsort)",
-                     "peak_note": "fp64 FMA: 148 SM x 64 lanes x 1.965 GHz x 2 (guide unit counts/clock); the FP64 "
+                     "peak_note": ("fp32 FMA: 148 SM x 128 lanes x 1.965 GHz x 2; " if fp32 else "") +
+                                  "fp64 FMA: 148 SM x 64 lanes x 1.965 GHz x 2 (guide unit counts/clock); the FP64 "
                                   "tensor cores (DMMA, k_eval_mma) run on the same datapath: 18.5T FMA/s measured "
                                   "(profiles/r01_dmma_vs_dfma.json)",
                      "algorithmic_fma_per_launch": fma_total, "kernel_ms": dom_ms, "stages_ms": stages},

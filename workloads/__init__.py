@@ -86,28 +86,41 @@ def sparse_coefficients(cfg: int = 4, d: int | None = None):
     return idx.astype(np.int64), a[idx]
 
 
-def sphere_points(cfg: int, n: int, shard: int = 0) -> np.ndarray:
-    """n points uniform on the Riemann sphere, stereographically projected."""
-    u = _rng(cfg, 2, shard).random(n)
+def _prng(cfg: int, stream: int, shard: int, start: int) -> np.random.Generator:
+    """The point stream's generator advanced past `start` draws: every point draw below takes exactly one
+    64-bit output per value (random() / uniform()), so point i of a batch comes from draw i of each stream
+    and any contiguous slice [lo, hi) can be generated alone (multi-GPU shards, bench.py)."""
+    g = _rng(cfg, stream, shard)
+    if start:
+        g.bit_generator.advance(start)
+    return g
+
+
+def sphere_points(cfg: int, n: int, shard: int = 0, start: int = 0) -> np.ndarray:
+    """n points uniform on the Riemann sphere, stereographically projected (points start..start+n-1 of the
+    seeded sequence)."""
+    u = _prng(cfg, 2, shard, start).random(n)
     u = np.where(u == 0.0, 0.5, u)  # open interval (0,1); u==0 has probability 2^-53
     r = np.sqrt(u / (1.0 - u))
-    phi = _rng(cfg, 3, shard).uniform(0.0, 2.0 * np.pi, size=n)
+    phi = _prng(cfg, 3, shard, start).uniform(0.0, 2.0 * np.pi, size=n)
     return _as_complex(r * np.cos(phi), r * np.sin(phi))
 
 
-def points(cfg: int, n: int | None = None, shard: int = 0) -> np.ndarray:
-    """Evaluation points of configuration ``cfg`` (complex128 or float64)."""
+def points(cfg: int, n: int | None = None, shard: int = 0, start: int = 0) -> np.ndarray:
+    """Evaluation points of configuration ``cfg`` (complex128 or float64): points start..start+n-1 of the
+    seeded sequence (n defaults to the configuration's N - start), so points(cfg, hi - lo, start=lo) equals
+    points(cfg)[lo:hi]."""
     c = CONFIGS[cfg]
-    n = c["n_points"] if n is None else int(n)
+    n = c["n_points"] - start if n is None else int(n)
     if cfg in (1, 3, 5):
-        return sphere_points(cfg, n, shard)
+        return sphere_points(cfg, n, shard, start)
     if cfg == 2:
-        t = _rng(cfg, 2, shard).uniform(-8.0, 8.0, size=n)
-        sgn = np.where(_rng(cfg, 3, shard).random(n) < 0.5, -1.0, 1.0)
+        t = _prng(cfg, 2, shard, start).uniform(-8.0, 8.0, size=n)
+        sgn = np.where(_prng(cfg, 3, shard, start).random(n) < 0.5, -1.0, 1.0)
         return sgn * np.exp2(t)
     if cfg == 4:
-        t = _rng(cfg, 2, shard).uniform(-2.0, 2.0, size=n)
-        phi = _rng(cfg, 3, shard).uniform(0.0, 2.0 * np.pi, size=n)
+        t = _prng(cfg, 2, shard, start).uniform(-2.0, 2.0, size=n)
+        phi = _prng(cfg, 3, shard, start).uniform(0.0, 2.0 * np.pi, size=n)
         r = np.exp2(t)
         return _as_complex(r * np.cos(phi), r * np.sin(phi))
     raise KeyError(cfg)
