@@ -402,6 +402,7 @@ def run_fpe(args):
     value = total_points / (ms * 1e-3)
     launches = poly.last_stats()["launches"]
     counters = poly.workspace_stats(ws, stream)
+    in_bytes = n * pts.element_size()
 
     # -- per-kernel durations, live, on the launch stream (profiling events) --------------------
     poly.set_profiling(True)
@@ -435,7 +436,7 @@ def run_fpe(args):
             poly.evaluate_host_ptr(hp.data_ptr(), pdt, n, hv.data_ptr(), he.data_ptr())
         dt = (time.perf_counter() - t0) / args.e2e_steps
         dt = reduce_max(pg, dt, dev)
-        e2e = {"value": total_points / dt, "unit": "evals/s", "h2d_bytes_per_step": int(n * pts.element_size()),
+        e2e = {"value": total_points / dt, "unit": "evals/s", "h2d_bytes_per_step": int(in_bytes),
                "d2h_bytes_per_step": int(n * (vals.element_size() + 8)), "ms_per_step": dt * 1e3}
 
     if rank != 0:
@@ -445,7 +446,7 @@ def run_fpe(args):
         cpu = cpu_baseline(cfg, args.cpu_sample or 65536, fp32)
     context = None
     if not args.no_extra and world == 1:
-        del pts, vals, exps
+        del pts, vals, exps, ws
         torch.cuda.empty_cache()
         context = extra_context(local)
     line = {
@@ -456,7 +457,7 @@ def run_fpe(args):
         "config": {"workload": c["name"] + ("_fp32" if fp32 else ""), "points_per_gpu": n,
                    "points_total": int(total_points), "degree": c["d"],
                    "parallelism": f"points x{world}" + (" (contiguous shards of N)" if strong else ""),
-                   "l2": f"inputs ({n * pts.element_size() / 2**30:.2f} GiB/rank) larger than L2; no flush",
+                   "l2": f"inputs ({in_bytes / 2**30:.2f} GiB/rank) larger than L2; no flush",
                    "mean_kept_terms": meanK, "kept_terms": kept_stats, "hard_lambdas": hard,
                    "counters": counters},
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

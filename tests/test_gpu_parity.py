@@ -706,3 +706,32 @@ def test_cfg5_fp32_near_unit_circle(fpe):
     err = rel_err_vs(H, out["v"], out["e"], abs_sum_log2(a, pts))
     print(f"\ncfg5-fp32 near |z| = 1: median K = {int(np.median(cls['K']))}, max err/S = 2^{np.log2(err.max()):.1f}")
     assert np.all(err <= TOL32), err.max()
+
+
+def test_replicate_and_evaluate_shard_nccl_world1(fpe):
+    """dist.replicate (export + NCCL broadcast + fpe_poly_from_device_buffer) and dist.evaluate_shard through
+    a real NCCL process group (world size 1 on the one GPU of this box): the imported handle evaluates
+    bitwise like the source, and from a host precondition_buffer as well."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2211_06320_b200 import dist as fdist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        a = workloads.coefficients(3, d=(1 << 16) - 1)
+        poly = fpe.precondition(a)
+        pts = workloads.points(3, 1 << 15)
+        (lo, hi), v, e = fdist.evaluate_shard(poly, pts)
+        assert (lo, hi) == (0, len(pts))
+        rep = fdist.replicate(fpe.precondition_buffer(a), src=0, device=0)
+        v2, e2 = rep.evaluate(torch.from_numpy(pts).cuda(), exps=True)
+        assert torch.equal(v, v2) and torch.equal(e, e2)
+        assert torch.equal(fdist.gather_shards(v, len(pts)), v)
+    finally:
+        dist.destroy_process_group()
