@@ -346,7 +346,7 @@ def precondition_buffer(coeffs: np.ndarray, p: int | None = None, drop: int | No
 
 _HDR = np.dtype([("magic", "<u8"), ("version", "<u4"), ("dtype", "<i4"), ("n_coeffs", "<i8"), ("k_min", "<i8"),
                  ("k_max", "<i8"), ("n_hull", "<i8"), ("n_good", "<i8"), ("p", "<i4"), ("drop", "<i4"),
-                 ("shift", "<i4"), ("sparse", "<i4"), ("all_good", "<i4"), ("pad0", "<i4"), ("off_hull", "<u8"),
+                 ("shift", "<i4"), ("sparse", "<i4"), ("all_good", "<i4"), ("wide", "<i4"), ("off_hull", "<u8"),
                  ("off_coef", "<u8"), ("off_prefix", "<u8"), ("off_sidx", "<u8"), ("bytes", "<u8")])
 
 

@@ -101,7 +101,7 @@ fpe::PolyDev fpe_poly_s::view() const {
   P.sidx = hdr.off_sidx ? reinterpret_cast<const int32_t*>(b + hdr.off_sidx) : nullptr;
   P.k_min = hdr.k_min; P.k_max = hdr.k_max; P.n_good = hdr.n_good;
   P.nv = (int)hdr.n_hull; P.drop = hdr.drop; P.shift = hdr.shift;
-  P.sparse = hdr.sparse; P.all_good = hdr.all_good; P.cdt = hdr.dtype;
+  P.sparse = hdr.sparse; P.all_good = hdr.all_good; P.cdt = hdr.dtype; P.wide = hdr.wide;
   long long hmin = 0, hmax = 0;
   for (size_t i = 0; i < hh.size(); ++i) {
     hmin = i ? std::min<long long>(hmin, hh[i]) : hh[i];
@@ -429,7 +429,8 @@ static bool header_valid(const Header& H, size_t bytes) {
   if (H.k_min < 0 || H.k_min > H.k_max || H.k_max >= H.n_coeffs) return false;
   const long long d_eff = H.k_max - H.k_min;
   if (H.n_hull < 1 || H.n_hull > d_eff + 1 || H.n_good < 1 || H.n_good > d_eff + 1) return false;
-  if (H.p < 1 || H.drop < 1 || (H.sparse != 0 && H.sparse != 1) || (H.all_good != 0 && H.all_good != 1)) return false;
+  if (H.p < 1 || H.drop < 1 || (H.sparse != 0 && H.sparse != 1) || (H.all_good != 0 && H.all_good != 1) ||
+      (H.wide != 0 && H.wide != 1)) return false;
   auto inside = [&](uint64_t off, uint64_t len) { return off >= sizeof(Header) && off <= bytes && len <= bytes - off; };
   const uint64_t csz = dtype_size(H.dtype);
   const uint64_t n_coef = H.sparse ? (uint64_t)H.n_good : (uint64_t)(d_eff + 1 + kCoefPad - 1) / kCoefPad * kCoefPad;

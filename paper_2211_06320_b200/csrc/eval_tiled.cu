@@ -772,6 +772,113 @@ __global__ void __launch_bounds__(kWarps * 32) k_eval_overflow(long long n, Poly
 }
 
 // ------------------------------------------------------------------------------------------------
+// Wide handles (PolyDev::wide: the good scales span more than one common power-of-two shift can hold in
+// the working format; the coefficients are stored as given): the window sum by an exponent-rescaled Horner
+// (north_star "exponent-rescaled Horner ... frexp/ldexp rescaling to avoid overflow").
+// One thread per point of the bucket order; the same absolute kPiece pieces, folded top-down with the same
+// acc_fold powers, so the decomposition (and its error bound) is the fast path's.  Inside a piece
+// b = m 2^E with max(|m_re|, |m_im|) in [1/2, 1) after every step; z = w 2^ez with max(|w_re|, |w_im|) in
+// [1/2, 1), so m w never overflows; a coefficient larger than b by more than 2^60 moves b to the
+// coefficient's scale first (b may then underflow: it is below the coefficient's rounding).  All in fp64
+// (fp32 handles too: more accurate than their 2^-16 tolerance needs).
+struct XAcc { double r, i; long long E; int base; bool started; };
+
+__device__ __forceinline__ void xnorm(double& r, double& i, long long& E) {
+  const double m = fmax(fabs(r), fabs(i));
+  if (m != 0.0 && isfinite(m)) { const int e = frexp_exp(m); r = ldexp(r, -e); i = ldexp(i, -e); E += e; }
+  else if (m == 0.0) E = 0;
+}
+
+template <int CK, bool CPLX>
+__device__ __forceinline__ void wide_piece(const PolyDev& P, int lo, int hi, double wr, double wi, int ez,
+                                           double& br, double& bi, long long& E) {
+  br = 0.0; bi = 0.0; E = 0;
+  bool nz = false;
+  for (int k = hi; k >= lo; --k) {
+    if (nz) {   // b <- b w (value times 2^ez)
+      if constexpr (CPLX) { const double t = __fma_rn(br, wr, -bi * wi); bi = __fma_rn(br, wi, bi * wr); br = t; }
+      else br = br * wr;
+      E += ez;
+    }
+    double cr, ci;
+    if constexpr (PtTraits<CK>::f32) { float a, b; Coef<CK>::get(P.coef, k, a, b); cr = a; ci = b; }
+    else Coef<CK>::get(P.coef, k, cr, ci);
+    if (cr != 0.0 || ci != 0.0) {
+      const int ec = frexp_exp(fmax(fabs(cr), fabs(ci)));
+      if (!nz || (long long)ec > E + 60) {   // b negligible next to a_k: continue at a_k's scale
+        const long long sh = nz ? E - ec : 0;
+        const int s = (int)max(-2200ll, min(2200ll, sh));
+        br = ldexp(br, s); bi = ldexp(bi, s); E = ec;
+      }
+      const int s = (int)max(-2200ll, -E);
+      br += ldexp(cr, s); bi += ldexp(ci, s);
+    }
+    xnorm(br, bi, E);
+    nz = (br != 0.0 || bi != 0.0);
+  }
+}
+
+// A <- A z^(A.base - pbase) + (hr + i hi) 2^hE, all in extended range (acc_fold with exponents).
+template <bool CPLX>
+__device__ __noinline__ void xacc_fold(XAcc& A, double hr, double hi, long long hE, int pbase, double x, double y) {
+  if (!A.started) { A.r = hr; A.i = hi; A.E = hE; A.base = pbase; A.started = true; return; }
+  const int gap = A.base - pbase;
+  const xc_t m = (gap == kPiece) ? power_piece<CPLX>(x, y) : power_polar<CPLX>(x, y, gap);
+  double r = __fma_rn(A.r, m.hr, __fma_rn(-A.i, m.hi, __fma_rn(A.r, m.er, -A.i * m.ei)));
+  double i = __fma_rn(A.r, m.hi, __fma_rn(A.i, m.hr, __fma_rn(A.r, m.ei, A.i * m.er)));
+  long long E = A.E + m.E;
+  xnorm(r, i, E);
+  if (hr != 0.0 || hi != 0.0) {   // align and add
+    if (r == 0.0 && i == 0.0) { r = hr; i = hi; E = hE; }
+    else if (hE > E) { const int s = (int)max(-2200ll, E - hE); r = ldexp(r, s) + hr; i = ldexp(i, s) + hi; E = hE; }
+    else { const int s = (int)max(-2200ll, hE - E); r += ldexp(hr, s); i += ldexp(hi, s); }
+    xnorm(r, i, E);
+  }
+  A.r = r; A.i = i; A.E = E; A.base = pbase;
+}
+
+template <int PK, int CK, int OK>
+__global__ void __launch_bounds__(256) k_eval_wide(long long n, PolyDev P, PtRec* rec) {
+  constexpr bool CPLX = PtTraits<OK>::cplx;
+  PtOut* const out = reinterpret_cast<PtOut*>(rec);
+  const int kmin = (int)P.k_min;
+  for (long long pos = blockIdx.x * (long long)blockDim.x + threadIdx.x; pos < n; pos += (long long)gridDim.x * blockDim.x) {
+    const int4 h = __ldcg(reinterpret_cast<const int4*>(rec + pos));
+    const double2 z = __ldcg(reinterpret_cast<const double2*>(rec + pos) + 1);
+    const double x = z.x, y = z.y;
+    XAcc A{0.0, 0.0, 0, 0, false};
+    if (h.w >= h.z && isfinite(x) && isfinite(y) && (x != 0.0 || y != 0.0)) {
+      const int wl = h.z - kmin, wr_ = h.w - kmin;
+      const int ez = frexp_exp(fmax(fabs(x), fabs(y)));
+      const double ux = ldexp(x, -ez), uy = ldexp(y, -ez);
+      for (int p = wr_ / kPiece; p >= wl / kPiece; --p) {
+        const int lo = max(wl, p * kPiece), hi = min(wr_, p * kPiece + kPiece - 1);
+        double br, bi;
+        long long E;
+        wide_piece<CK, CPLX>(P, lo, hi, ux, uy, ez, br, bi, E);
+        xacc_fold<CPLX>(A, br, bi, E, lo, x, y);
+      }
+    }
+    // Q = A z^(base + k_min) (finalize's polar power; z = 0 and non-finite z as finalize)
+    Fin f;
+    if (!A.started) {
+      Acc a0{0.0, 0.0, 0, false};
+      f = finalize<CPLX>(x, y, a0, P);
+      if (x == 0.0 && y == 0.0 && h.w >= h.z) {   // z = 0: a_0 (window {k_min})
+        double cr = 0.0, ci = 0.0;
+        a0_value<CK>(P, cr, ci);
+        f = Fin{cr, ci, (cr == 0.0 && ci == 0.0) ? 0 : (long long)P.shift};
+      }
+    } else {
+      Acc a{A.r, A.i, A.base, true};
+      f = finalize<CPLX>(x, y, a, P);
+      f.E += A.E;
+    }
+    stage_value(out, pos, f.re, f.im, f.E);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // Full Horner over all coefficients (the context baseline), with the evaluator's
 // streaming: warps take 64 consecutive input points (2 per lane) and stream every coefficient chunk
 // through the TMA ring.  Without the band there is no magnitude bound, so after every chunk each point
@@ -988,6 +1095,13 @@ static int launch_eval_tiled_t(long long n, const PolyDev& P, PtRec* rec, const 
   return 1;
 }
 
+template <int PK, int CK, int OK>
+static int launch_eval_wide_t(long long n, const PolyDev& P, PtRec* rec, cudaStream_t s) {
+  const long long blocks = std::min<long long>((n + 255) / 256, 148ll * 16);
+  k_eval_wide<PK, CK, OK><<<(int)std::max(1ll, blocks), 256, 0, s>>>(n, P, rec);
+  return 1;
+}
+
 template <int PK, int CK, int OK, int NP>
 static int launch_eval_overflow_t(long long n, const PolyDev& P, PtRec* rec, const Plan& plan, cudaStream_t s) {
   const size_t smem = eval_smem<CK>();
@@ -1073,7 +1187,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   plan.mma_ctrs = plan.ctrs + 4;
   const int np = np_for(pk, P.cdt);
   plan.gsize = 32 * np;
-  plan.mma_on = (P.cdt == FPE_C64 && plan.gsize == 128 && !FPE_NO_MMA_ITEMS) ? 1 : 0;
+  plan.mma_on = (P.cdt == FPE_C64 && plan.gsize == 128 && !FPE_NO_MMA_ITEMS && !P.wide) ? 1 : 0;
   plan.ngroups = (uint32_t)((n + plan.gsize - 1) / plan.gsize);
   const bool f32 = (P.cdt == FPE_R32 || P.cdt == FPE_C32);
   const size_t slot_bytes = (size_t)plan.gsize * (f32 ? sizeof(float2) : sizeof(double2));
@@ -1097,8 +1211,9 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     lm = 1;
   }
   int le = 0;
-#define FPE_EV(PKV, CKV) \
-  le = launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(n, P, rec, plan, s)
+#define FPE_EV(PKV, CKV)                                                                                  \
+  le = P.wide ? launch_eval_wide_t<PKV, CKV, NPFor<PKV, CKV>::OK>(n, P, rec, s)                              \
+              : launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(n, P, rec, plan, s)
   switch (pk * 4 + P.cdt) {
     case FPE_R64 * 4 + FPE_R64: FPE_EV(FPE_R64, FPE_R64); break;
     case FPE_R64 * 4 + FPE_C64: FPE_EV(FPE_R64, FPE_C64); break;
@@ -1111,7 +1226,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     default: return -1;
   }
 #undef FPE_EV
-  st.mark("eval_tiled");
+  st.mark(P.wide ? "eval_wide" : "eval_tiled");
   if (plan.mma_on) {   // groups whose tensor-core items overflowed the DMMA scratch (usually none)
     if (pk == FPE_C64) le += launch_eval_overflow_t<FPE_C64, FPE_C64, NPFor<FPE_C64, FPE_C64>::OK, 4>(n, P, rec, plan, s);
     else le += launch_eval_overflow_t<FPE_R64, FPE_C64, NPFor<FPE_R64, FPE_C64>::OK, 4>(n, P, rec, plan, s);

@@ -26,7 +26,7 @@ struct Header {
   uint32_t version;
   int32_t dtype;        // fpe_dtype of the stored coefficients
   int64_t n_coeffs, k_min, k_max, n_hull, n_good;
-  int32_t p, drop, shift, sparse, all_good, pad0;
+  int32_t p, drop, shift, sparse, all_good, wide;   // wide: scales beyond one common shift (raw a_k, shift 0)
   uint64_t off_hull, off_coef, off_prefix, off_sidx, bytes;
   uint8_t reserved[136];
 };
@@ -52,6 +52,7 @@ struct PolyDev {
   const int32_t* sidx;
   long long k_min, k_max, n_good;
   int nv, drop, shift, sparse, all_good, cdt;
+  int wide;     // evaluate with per-step exponent tracking (k_eval_wide): shift = 0, raw coefficients
   int dbl_ok;   // band predicates exact in doubles: d_eff < 2^26 and (2 H + D) d_eff < 2^52
 };
 

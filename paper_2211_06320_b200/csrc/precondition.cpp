@@ -127,12 +127,13 @@ fpe_status precondition_host(const void* coeffs, int64_t n, fpe_dtype dt, int32_
   for (int64_t i = 0; i < nv; ++i) hmax = std::max(hmax, hh[i]);
   for (int64_t k = k_min; k <= k_max; ++k)
     if (good[k - k_min]) smin = std::min(smin, s[k]);
-  const int32_t shift = hmax;
+  // Beyond the format's range for one common shift (good scales spanning more than 1000 / 100 bits, or a
+  // drop D too large for the K 2^D bound) the handle is "wide": the coefficients are stored as given
+  // (shift 0) and evaluated with per-step exponent tracking (k_eval_wide; north_star "exponent-rescaled
+  // Horner", PAPER.md:2361-2373 on the exponent range of hardware formats).
   const int32_t limit = f32 ? 100 : 1000;
-  if ((int64_t)shift - smin > limit || drop + 30 > (f32 ? 120 : 1000)) {
-    set_error("coefficient scales of G_p span %d bits (limit %d for this dtype)", shift - smin, limit);
-    return FPE_ERR_UNSUPPORTED;
-  }
+  const bool wide = ((int64_t)hmax - smin > limit || drop + 30 > (f32 ? 120 : 1000));
+  const int32_t shift = wide ? 0 : hmax;
 
   // 5. flat buffer
   const size_t csz = f32 ? (cplx ? 8 : 4) : (cplx ? 16 : 8);
@@ -142,6 +143,7 @@ fpe_status precondition_host(const void* coeffs, int64_t n, fpe_dtype dt, int32_
   hdr.magic = kMagic; hdr.version = kVersion; hdr.dtype = dt;
   hdr.n_coeffs = n; hdr.k_min = k_min; hdr.k_max = k_max; hdr.n_hull = nv; hdr.n_good = n_good;
   hdr.p = p; hdr.drop = drop; hdr.shift = shift; hdr.sparse = sparse; hdr.all_good = all_good;
+  hdr.wide = wide;
   size_t off = align256(sizeof(Header));
   hdr.off_hull = off; off = align256(off + nv * sizeof(int2));
   hdr.off_coef = off; off = align256(off + n_coef_alloc * csz);

@@ -387,12 +387,9 @@ fpe_status cover_finish(const CoverDev& cv, int32_t p_bits, int32_t drop_overrid
   const long long n_good = st.n_good;
   const bool all_good = (n_good == d_eff + 1);
   const bool sparse = (n_good * 32 < d_eff + 1);
-  const int32_t shift = st.hmax;
-  const int32_t limit = f32 ? 100 : 1000;
-  if ((long long)shift - st.smin > limit || drop + 30 > (f32 ? 120 : 1000)) {
-    set_error("coefficient scales of G_p span %d bits (limit %d for this dtype)", shift - st.smin, limit);
-    return FPE_ERR_UNSUPPORTED;
-  }
+  const int32_t limit = f32 ? 100 : 1000;   // as precondition_host: "wide" handles keep shift 0
+  const bool wide = ((long long)st.hmax - st.smin > limit || drop + 30 > (f32 ? 120 : 1000));
+  const int32_t shift = wide ? 0 : st.hmax;
 
   // layout (as precondition_host)
   const size_t csz = f32 ? (cplx ? 8 : 4) : (cplx ? 16 : 8);
@@ -402,6 +399,7 @@ fpe_status cover_finish(const CoverDev& cv, int32_t p_bits, int32_t drop_overrid
   hdr.magic = kMagic; hdr.version = kVersion; hdr.dtype = dt;
   hdr.n_coeffs = n; hdr.k_min = k_min; hdr.k_max = k_max; hdr.n_hull = nv; hdr.n_good = n_good;
   hdr.p = p; hdr.drop = drop; hdr.shift = shift; hdr.sparse = sparse; hdr.all_good = all_good;
+  hdr.wide = wide;
   size_t off = align256(sizeof(Header));
   hdr.off_hull = off; off = align256(off + nv * sizeof(int2));
   hdr.off_coef = off; off = align256(off + n_coef_alloc * csz);

@@ -112,14 +112,25 @@ def test_degenerate_polys(fpe):
             a[0] = 1
         cases.append(a)
         cases.append(a * np.exp(1j * rng.uniform(0, 6.3, d + 1)))
+    for cplx in (False, True):   # coefficients at 2^+-900: wide handles
+        a = rng.normal(size=501) * np.exp2(rng.integers(-900, 900, size=501))
+        a[0], a[-1] = 2.0 ** -950, 3 * 2.0 ** 950        # cover endpoints 1900 bits apart
+        cases.append(a * np.exp(1j * rng.uniform(0, 6.3, 501)) if cplx else a)
+    n_wide = 0
     for a in cases:
-        try:
-            _check_against_oracle(fpe, a)
-        except fpe.FpeError as e:
-            assert e.status == 4   # UNSUPPORTED: dynamic range beyond fp64 (documented)
-            s = oracle.scales(a)
-            g = s[s != oracle.NEG_INF_SCALE]
-            assert g.max() - g.min() > 900
+        h, P = _check_against_oracle(fpe, a)
+        g = P.s[P.good.astype(bool)]
+        # scales of G_p spanning more than 1000 bits: a "wide" handle (raw coefficients, exponent-tracked
+        # evaluation); otherwise one common shift maps the cover's top to 2^0
+        assert h["wide"] == int(g.max() - g.min() > 1000)
+        assert h["shift"] == (0 if h["wide"] else P.hh.max())
+        n_wide += h["wide"]
+    assert n_wide >= 3
+    # single precision: spans beyond 100 bits are wide (the fp32 working range)
+    a = (rng.normal(size=300) * np.exp2(rng.integers(-100, 100, size=300))).astype(np.float32)
+    h, P = _check_against_oracle(fpe, a)
+    g = P.s[P.good.astype(bool)]
+    assert h["wide"] == int(g.max() - g.min() > 100) == 1 and h["shift"] == 0
 
 
 def test_errors(fpe):
