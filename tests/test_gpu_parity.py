@@ -793,3 +793,31 @@ def test_wide_dynamic_range(fpe, fp32):
             assert np.array_equal(hv, out["v"]) and np.array_equal(he, out["e"])
             print(f"\nwide {'fp32' if fp32 else 'fp64'} case {ci} {'complex' if cplx else 'real'}: "
                   f"median K {int(np.median(cls['K']))}, max err/S 2^{np.log2(max(err.max(), 1e-300)):.1f}")
+
+
+@pytest.mark.parametrize("pset", ["rbar", "disk"])
+def test_second_point_sets(fpe, pset):
+    """points uniform on R-bar (real polynomial, the Cauchy law; eq:compAlgoRe) and on
+    the unit disk (complex polynomial; rmk:case_disk) -- on the cfg2 / cfg1 families and the half-circle
+    family: indexing bit-exact, values within 2^-45 S against the oracle, mean band below the paper's bound
+    (1.7673 / 2.3141)."""
+    d = 1000
+    nn = np.arange(d + 1)
+    half = np.exp2(np.sqrt((nn + 1.0) * (d + 1.0 - nn)))
+    if pset == "rbar":
+        cases = [(workloads.coefficients(2, d=(1 << 16) - 1), workloads.rbar_points(2, 1 << 14)),
+                 (half, workloads.rbar_points(2, 1 << 14, shard=1))]
+        C = 1.7673
+    else:
+        cases = [(workloads.coefficients(1), workloads.disk_points(1, 1 << 14)),
+                 (workloads.coefficients(5, d=(1 << 16) - 1), workloads.disk_points(5, 1 << 14)),
+                 (half.astype(np.complex128), workloads.disk_points(1, 1 << 14, shard=1))]
+        C = 2.3141
+    for a, pts in cases:
+        poly = fpe.precondition(a)
+        P = oracle.OraclePoly(a)
+        out = gpu_eval(poly, pts)
+        cls = check_indexing(P, pts, out["diag"])
+        width = cls["r"] - cls["l"] + 1
+        assert width.mean() < 1 + C * math.sqrt(P.d_eff * P.drop)
+        _values_ok(P, a, pts, out, np.arange(0, len(pts), 4), TOL64, cls)

@@ -347,3 +347,30 @@ def test_half_circle_family_complexity():
     assert all(r < 1.9046 for r in ratios)
     assert ratios[0] < ratios[1] < ratios[2] < 1.32178
     assert ratios[2] > 1.25
+
+
+def test_second_point_sets_average_window():
+    """Theorem thm:algo / eq:compAlgoRe and remark rmk:case_disk: the mean
+    band width #[l, r] is below 1 + C sqrt(d_eff D) with C = 1.7673 for a real polynomial at points uniform on
+    R-bar (the Cauchy law) and C = 2.3141 for a complex polynomial at points uniform on the unit disk --
+    for any polynomial, so also for the half-circle family (the paper's slowest)."""
+    import workloads
+    d = 1000
+    nn = np.arange(d + 1)
+    half = np.exp2(np.sqrt((nn + 1.0) * (d + 1.0 - nn)))
+    for a, pts, C in (
+            (workloads.coefficients(2, d=4095), workloads.rbar_points(2, 1 << 15), 1.7673),
+            (half, workloads.rbar_points(2, 1 << 15, shard=1), 1.7673),
+            (workloads.coefficients(1), workloads.disk_points(1, 1 << 15), 2.3141),
+            (half.astype(np.complex128), workloads.disk_points(1, 1 << 15, shard=1), 2.3141)):
+        P = oracle.OraclePoly(a)
+        c = P.classify(pts)
+        width = (c["r"] - c["l"] + 1).astype(float)
+        bound = 1 + C * math.sqrt(P.d_eff * P.drop)
+        assert width.mean() < bound, (width.mean(), bound)
+        assert np.all(c["K"] <= width)
+    # the generators' laws: Cauchy quartiles at +-1, disk radii with P(r < 1/2) = 1/4
+    x = workloads.rbar_points(3, 1 << 16)
+    assert abs(np.mean(np.abs(x) < 1) - 0.5) < 0.01
+    z = workloads.disk_points(3, 1 << 16)
+    assert np.all(np.abs(z) < 1) and abs(np.mean(np.abs(z) < 0.5) - 0.25) < 0.01

@@ -10,7 +10,8 @@ as fixed by /root/repo/BASELINE.json ``configs``.
 
 Seeds: ``2211063200 + 10*cfg + stream`` with streams
 0 = coefficient values, 1 = coefficient phases / indices,
-2 = point radii / log-moduli, 3 = point angles / signs.
+2 = point radii / log-moduli, 3 = point angles / signs (SURVEY.md §8(d));
+the second point sets of SURVEY.md §8(f) row 4 use 4, 5 (unit disk) and 6 (R-bar).
 
 Riemann-sphere sampling: the
 uniform measure on the sphere pushed to C by stereographic projection has
@@ -104,6 +105,23 @@ def sphere_points(cfg: int, n: int, shard: int = 0, start: int = 0) -> np.ndarra
     r = np.sqrt(u / (1.0 - u))
     phi = _prng(cfg, 3, shard, start).uniform(0.0, 2.0 * np.pi, size=n)
     return _as_complex(r * np.cos(phi), r * np.sin(phi))
+
+
+def disk_points(cfg: int, n: int, shard: int = 0) -> np.ndarray:
+    """n points uniform on the unit disk D(0, 1) (rmk:case_disk): r = sqrt(u),
+    u ~ U(0, 1), argument uniform on [0, 2 pi).  Streams 4 (radii) and 5 (angles)."""
+    r = np.sqrt(_rng(cfg, 4, shard).random(n))
+    phi = _rng(cfg, 5, shard).uniform(0.0, 2.0 * np.pi, size=n)
+    return _as_complex(r * np.cos(phi), r * np.sin(phi))
+
+
+def rbar_points(cfg: int, n: int, shard: int = 0) -> np.ndarray:
+    """n real points uniform on the circle R-bar = R u {inf} (eq:compAlgoRe; weight
+    omega-tilde): the uniform measure on the projective line is the Cauchy law
+    dx / (pi (1 + x^2)), x = tan(pi (u - 1/2)) with u ~ U(0, 1) open.  Stream 6."""
+    u = _rng(cfg, 6, shard).random(n)
+    u = np.where(u == 0.0, 0.5, u)
+    return np.tan(np.pi * (u - 0.5))
 
 
 def points(cfg: int, n: int | None = None, shard: int = 0, start: int = 0) -> np.ndarray:
