@@ -361,7 +361,7 @@ __device__ __forceinline__ void store_value(void* __restrict__ vals, long long* 
     E = 0;
   } else {
     int e = frexp_exp(m);
-    re = ldexp(re, -e); im = ldexp(im, -e);
+    re = ldexp_fast(re, -e); im = ldexp_fast(im, -e);
     E += e;
   }
   if (!exps) {   // plain floats: value * 2^E, saturating

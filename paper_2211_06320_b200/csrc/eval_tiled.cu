@@ -365,7 +365,7 @@ __device__ __forceinline__ void mul_ext(double& re, double& im, const xc_t& p) {
   double r = __fma_rn(re, p.hr, __fma_rn(-im, p.hi, __fma_rn(re, p.er, -im * p.ei)));
   double i = __fma_rn(re, p.hi, __fma_rn(im, p.hr, __fma_rn(re, p.ei, im * p.er)));
   int sc = (int)max(-3000ll, min(3000ll, p.E));
-  re = ldexp(r, sc); im = ldexp(i, sc);
+  re = ldexp_fast(r, sc); im = ldexp_fast(i, sc);
 }
 
 template <bool CPLX>
@@ -785,7 +785,7 @@ struct XAcc { double r, i; long long E; int base; bool started; };
 
 __device__ __forceinline__ void xnorm(double& r, double& i, long long& E) {
   const double m = fmax(fabs(r), fabs(i));
-  if (m != 0.0 && isfinite(m)) { const int e = frexp_exp(m); r = ldexp(r, -e); i = ldexp(i, -e); E += e; }
+  if (m != 0.0 && isfinite(m)) { const int e = frexp_exp(m); r = ldexp_fast(r, -e); i = ldexp_fast(i, -e); E += e; }
   else if (m == 0.0) E = 0;
 }
 
@@ -795,24 +795,30 @@ __device__ __forceinline__ void wide_piece(const PolyDev& P, int lo, int hi, dou
   br = 0.0; bi = 0.0; E = 0;
   bool nz = false;
   for (int k = hi; k >= lo; --k) {
-    if (nz) {   // b <- b w (value times 2^ez)
-      if constexpr (CPLX) { const double t = __fma_rn(br, wr, -bi * wi); bi = __fma_rn(br, wi, bi * wr); br = t; }
-      else br = br * wr;
-      E += ez;
-    }
+    long long E1 = nz ? E + ez : E;   // the exponent of b w
     double cr, ci;
     if constexpr (PtTraits<CK>::f32) { float a, b; Coef<CK>::get(P.coef, k, a, b); cr = a; ci = b; }
     else Coef<CK>::get(P.coef, k, cr, ci);
+    double sr = 0.0, si = 0.0;
     if (cr != 0.0 || ci != 0.0) {
       const int ec = frexp_exp(fmax(fabs(cr), fabs(ci)));
-      if (!nz || (long long)ec > E + 60) {   // b negligible next to a_k: continue at a_k's scale
-        const long long sh = nz ? E - ec : 0;
-        const int s = (int)max(-2200ll, min(2200ll, sh));
-        br = ldexp(br, s); bi = ldexp(bi, s); E = ec;
+      if (!nz || (long long)ec > E1 + 60) {   // b negligible next to a_k: continue at a_k's scale
+        if (nz) {
+          const int s = (int)max(-2200ll, min(2200ll, E1 - ec));
+          br = ldexp_fast(br, s); bi = ldexp_fast(bi, s);
+        }
+        E1 = ec;
       }
-      const int s = (int)max(-2200ll, -E);
-      br += ldexp(cr, s); bi += ldexp(ci, s);
+      const int s = (int)max(-2200ll, -E1);
+      sr = ldexp_fast(cr, s); si = ldexp_fast(ci, s);
     }
+    if (nz) {   // b <- b w + a_k 2^-E1: the fast path's fused steps (Step<>::apply)
+      if constexpr (CPLX) { const double t = __fma_rn(br, wr, __fma_rn(-bi, wi, sr)); bi = __fma_rn(br, wi, __fma_rn(bi, wr, si)); br = t; }
+      else br = __fma_rn(br, wr, sr);
+    } else {
+      br = sr; bi = si;
+    }
+    E = E1;
     xnorm(br, bi, E);
     nz = (br != 0.0 || bi != 0.0);
   }
@@ -830,8 +836,8 @@ __device__ __noinline__ void xacc_fold(XAcc& A, double hr, double hi, long long 
   xnorm(r, i, E);
   if (hr != 0.0 || hi != 0.0) {   // align and add
     if (r == 0.0 && i == 0.0) { r = hr; i = hi; E = hE; }
-    else if (hE > E) { const int s = (int)max(-2200ll, E - hE); r = ldexp(r, s) + hr; i = ldexp(i, s) + hi; E = hE; }
-    else { const int s = (int)max(-2200ll, hE - E); r += ldexp(hr, s); i += ldexp(hi, s); }
+    else if (hE > E) { const int s = (int)max(-2200ll, E - hE); r = ldexp_fast(r, s) + hr; i = ldexp_fast(i, s) + hi; E = hE; }
+    else { const int s = (int)max(-2200ll, hE - E); r += ldexp_fast(hr, s); i += ldexp_fast(hi, s); }
     xnorm(r, i, E);
   }
   A.r = r; A.i = i; A.E = E; A.base = pbase;

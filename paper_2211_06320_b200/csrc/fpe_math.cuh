@@ -66,10 +66,17 @@ FPE_HD dd_t dd_div(dd_t a, dd_t b) {
 FPE_HD double pow2i(int e) {
   return fpe_bits2d((long long)(e + 1023) << 52);
 }
+// x 2^e, exact when the scale factor is a normal double (one multiplication), else ldexp.
+FPE_HD double ldexp_fast(double x, int e) {
+  return (e >= -1022 && e <= 1023) ? fpe_mul(x, pow2i(e)) : ldexp(x, e);
+}
 // Exponent e with |x| = m 2^e, m in [1/2, 1), for finite nonzero normal or subnormal x.
 FPE_HD int frexp_exp(double x) {
+  const long long b = fpe_d2bits(x);
+  const int be = (int)((b >> 52) & 0x7ff);
+  if (be != 0 && be != 0x7ff) return be - 1022;   // normal: read the exponent field
   int e;
-  (void)frexp(x, &e);
+  (void)frexp(x, &e);                              // zero, subnormal, inf, NaN
   return e;
 }
 

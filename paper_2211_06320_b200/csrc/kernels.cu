@@ -23,20 +23,42 @@ template <int PK>
 __global__ void __launch_bounds__(256) k_classify(const void* __restrict__ pts, long long n, PolyDev P,
                                                   int2* __restrict__ lr, fpe_diag* __restrict__ diag,
                                                   unsigned long long* __restrict__ hard_ctr) {
-  extern __shared__ int2 s_hull[];
+  // the cover in shared memory, also as exact doubles when small (the fast path of k_classify_bucket:
+  // searches on an fp64 enclosure of log2|z|, the correctly rounded lambda only for undecided points)
+  extern __shared__ __align__(16) unsigned char s_cls[];
+  const bool dbl = P.nv <= kSmemHullDbl;
+  double2* hv = reinterpret_cast<double2*>(s_cls);
+  int2* sh = reinterpret_cast<int2*>(s_cls + (dbl ? (size_t)P.nv * sizeof(double2) : 0));
   const int2* hull = P.hull;
   if (P.nv <= kSmemHullMax) {
-    for (int i = threadIdx.x; i < P.nv; i += blockDim.x) s_hull[i] = P.hull[i];
+    for (int i = threadIdx.x; i < P.nv; i += blockDim.x) {
+      const int2 v = P.hull[i];
+      sh[i] = v;
+      if (dbl) hv[i] = make_double2((double)v.x, (double)v.y);
+    }
     __syncthreads();
-    hull = s_hull;
+    hull = sh;
   }
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     double x, y;
     load_point<PK>(pts, i, x, y);
-    int hard;
-    double lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
+    int hard = 0;
+    double lam = 0.0;
     int istar, l, r;
-    classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
+    bool done = false;
+    if (dbl && P.dbl_ok && isfinite(x) && isfinite(y) && (x != 0.0 || (PtTraits<PK>::cplx && y != 0.0))) {
+      double lo, hi;
+      lambda_enclosure(x, y, PtTraits<PK>::cplx, lo, hi, lam);
+      bool amb = false;
+      classify_lambda_vp(hull, hv, P.nv, P.drop, LamIv{lo, hi, &amb}, istar, l, r);
+      done = !amb;
+      if (done && diag) lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
+    }
+    if (!done) {
+      lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
+      if (dbl && P.dbl_ok) classify_lambda_v<true>(hull, hv, P.nv, P.drop, lam, istar, l, r);
+      else classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
+    }
     lr[i] = make_int2(l, r);
     if (diag) {
       fpe_diag d;
@@ -56,11 +78,11 @@ __global__ void __launch_bounds__(256) k_classify(const void* __restrict__ pts, 
 __device__ __forceinline__ void xadd(double& sr, double& si, long long& se, double tr, double ti, long long te) {
   if (tr == 0.0 && ti == 0.0) return;
   if (sr == 0.0 && si == 0.0) { sr = tr; si = ti; se = te; return; }
-  if (te > se) { const long long d = te - se; const int s = (int)min(d, 2000ll); sr = ldexp(sr, -s); si = ldexp(si, -s); se = te; }
-  else if (te < se) { const long long d = se - te; const int s = (int)min(d, 2000ll); tr = ldexp(tr, -s); ti = ldexp(ti, -s); }
+  if (te > se) { const long long d = te - se; const int s = (int)min(d, 2000ll); sr = ldexp_fast(sr, -s); si = ldexp_fast(si, -s); se = te; }
+  else if (te < se) { const long long d = se - te; const int s = (int)min(d, 2000ll); tr = ldexp_fast(tr, -s); ti = ldexp_fast(ti, -s); }
   sr += tr; si += ti;
   const double m = fmax(fabs(sr), fabs(si));
-  if (m != 0.0) { const int e = frexp_exp(m); sr = ldexp(sr, -e); si = ldexp(si, -e); se += e; }
+  if (m != 0.0) { const int e = frexp_exp(m); sr = ldexp_fast(sr, -e); si = ldexp_fast(si, -e); se += e; }
 }
 
 constexpr int kSparseSmemIdx = 8192;   // good indices staged in shared memory (32 KiB)
@@ -74,6 +96,7 @@ constexpr int kSparseSmemIdx = 8192;   // good indices staged in shared memory (
 // same whatever points share its warp.
 constexpr int kSpWarps = 8;
 constexpr int kSpRound = 128;   // terms per warp and round in shared memory
+constexpr int kSpTab = 4096;    // buckets of the good-index table
 struct SpTerm { double r, i; long long e; };
 
 template <int CK, bool CPLX>
@@ -105,11 +128,25 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
   polar_t* pol = reinterpret_cast<polar_t*>(sp_smem + sizeof(SpTerm) * kSpWarps * kSpRound);      // [warps][32]
   int* offs = reinterpret_cast<int*>(pol + kSpWarps * 32);                                         // [warps][33]
   int* firsts = offs + kSpWarps * 33;                                                              // [warps][32]
-  int* sidx_s = firsts + kSpWarps * 32;
+  int* tab = firsts + kSpWarps * 32;               // [kSpTab + 1] bucket -> first good index position
+  int* sidx_s = tab + kSpTab + 1;
   const int32_t* sidx = P.sidx;
   const int ng = (int)P.n_good;
-  if (ng <= kSparseSmemIdx) {
+  const bool staged = ng <= kSparseSmemIdx;
+  // the good indices in shared memory, and a bucket table over [k_min, k_max] (buckets of 2^tb indices):
+  // the first good index >= k lies in [tab[b], tab[b + 1]] for b = (k - k_min) >> tb, so each window
+  // bound costs a search over ~ng / kSpTab entries instead of log2(ng) steps
+  int tb = 0;
+  while (((P.k_max - P.k_min) >> tb) >= kSpTab) ++tb;
+  const int nb = (int)((P.k_max - P.k_min) >> tb) + 1;
+  if (staged) {
     for (int i = threadIdx.x; i < ng; i += blockDim.x) sidx_s[i] = P.sidx[i];
+    for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+      const long long key = P.k_min + ((long long)b << tb);
+      int lo = 0, hi = ng;
+      while (lo < hi) { const int m = (lo + hi) >> 1; if ((long long)__ldg(P.sidx + m) < key) lo = m + 1; else hi = m; }
+      tab[b] = lo;
+    }
     sidx = sidx_s;
   }
   __syncthreads();
@@ -129,9 +166,14 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
       if (wv.y < wv.x) state = 1;
       else if (x == 0.0 && y == 0.0) state = 2;
       else {
-        int lo = 0, hi = ng;   // first good index >= l
+        int lo = 0, hi = ng, lo2, hi2 = ng;   // first good index >= l, first good index > r
+        if (staged) {
+          const int bl = (int)((wv.x - P.k_min) >> tb), br_ = (int)((wv.y - P.k_min) >> tb);
+          lo = tab[bl]; hi = tab[bl + 1];
+          hi2 = tab[br_ + 1];
+        }
         while (lo < hi) { const int m = (lo + hi) >> 1; if (sidx[m] < wv.x) lo = m + 1; else hi = m; }
-        int lo2 = lo, hi2 = ng;   // first good index > r
+        lo2 = staged ? max(lo, tab[(int)((wv.y - P.k_min) >> tb)]) : lo;
         while (lo2 < hi2) { const int m = (lo2 + hi2) >> 1; if (sidx[m] <= wv.y) lo2 = m + 1; else hi2 = m; }
         first = lo; K = lo2 - lo;
         if (K > 0) PL[lane] = polar_of<CPLX>(x, y);
@@ -336,7 +378,8 @@ static int grid_for(long long n, int block) {
 template <int PK>
 static void launch_classify_t(const void* pts, long long n, const PolyDev& P, int2* lr, fpe_diag* diag,
                               unsigned long long* hard, cudaStream_t s) {
-  size_t smem = P.nv <= kSmemHullMax ? P.nv * sizeof(int2) : 0;
+  const size_t smem = (P.nv <= kSmemHullMax ? P.nv * sizeof(int2) : 0) + (P.nv <= kSmemHullDbl ? P.nv * sizeof(double2) : 0);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_classify<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_classify<PK><<<grid_for(n, 256), 256, smem, s>>>(pts, n, P, lr, diag, hard);
 }
 
@@ -377,7 +420,8 @@ static void launch_eval_sparse_t(const void* pts, long long n, const PolyDev& P,
   constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
   constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
   const size_t smem = sizeof(SpTerm) * kSpWarps * kSpRound + sizeof(polar_t) * kSpWarps * 32 +
-                      sizeof(int) * kSpWarps * 65 + (P.n_good <= kSparseSmemIdx ? (size_t)P.n_good * sizeof(int32_t) : 0);
+                      sizeof(int) * (kSpWarps * 65 + kSpTab + 1) +
+                      (P.n_good <= kSparseSmemIdx ? (size_t)P.n_good * sizeof(int32_t) : 0);
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
