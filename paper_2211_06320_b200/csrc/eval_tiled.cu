@@ -195,6 +195,28 @@ __device__ __forceinline__ void horner_step2_c64(double& br0, double& bi0, doubl
   br0 = nr0; bi0 = ni0; br1 = nr1; bi1 = ni1;
 }
 
+// Packed single precision (sm_100a FFMA2: two fp32 FMAs per instruction, the scalar coefficient broadcast
+// to both halves): the fp32 Horner of two points per instruction, with the same roundings as the scalar
+// steps (Step<FPE_C32> / Step<FPE_R32>), so results are bitwise unchanged.
+__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 template <int CK> struct Ring {
   using CT = typename Step<CK>::CT;
   CT* buf;            // kStages * kChunk coefficients of this warp
@@ -313,6 +335,45 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
 #ifdef FPE_EXP_NO_HOT
     k = min(k, f0 - 1);
 #endif
+    if constexpr ((CK == FPE_C32 || CK == FPE_R32) && NP % 2 == 0) {
+      if (k - 7 >= f0) {   // points (j, j + 1) packed into one register pair each
+        unsigned long long pr[NP / 2], pi[NP / 2], qr[NP / 2], qi[NP / 2], qn[NP / 2];
+#pragma unroll
+        for (int q = 0; q < NP / 2; ++q) {
+          pr[q] = f2pack(br[2 * q], br[2 * q + 1]); pi[q] = f2pack(bi[2 * q], bi[2 * q + 1]);
+          qr[q] = f2pack(zr[2 * q], zr[2 * q + 1]); qi[q] = f2pack(zi[2 * q], zi[2 * q + 1]);
+          qn[q] = f2pack(-zi[2 * q], -zi[2 * q + 1]);
+        }
+        for (; k - 7 >= f0; k -= 8) {
+          CT a[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a[u] = cb[k - u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+#pragma unroll
+            for (int q = 0; q < NP / 2; ++q) {
+              if constexpr (CK == FPE_C32) {   // Step<FPE_C32>: t = fma(-bi, zi, ar), bi = fma(br, zi, fma(bi, zr, ai))
+                const unsigned long long t = ffma2(pi[q], qn[q], f2pack(a[u].x, a[u].x));
+                const unsigned long long v = ffma2(pi[q], qr[q], f2pack(a[u].y, a[u].y));
+                pi[q] = ffma2(pr[q], qi[q], v);
+                pr[q] = ffma2(pr[q], qr[q], t);
+              } else if constexpr (CPLX) {     // Step<FPE_R32> at complex points
+                const unsigned long long t = ffma2(pi[q], qn[q], f2pack(a[u], a[u]));
+                pi[q] = ffma2(pr[q], qi[q], fmul2(pi[q], qr[q]));
+                pr[q] = ffma2(pr[q], qr[q], t);
+              } else {                         // Step<FPE_R32> at real points
+                pr[q] = ffma2(pr[q], qr[q], f2pack(a[u], a[u]));
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NP / 2; ++q) {
+          f2unpack(pr[q], br[2 * q], br[2 * q + 1]);
+          f2unpack(pi[q], bi[2 * q], bi[2 * q + 1]);
+        }
+      }
+    } else {
     for (; k - 7 >= f0; k -= 8) {
       CT a[8];
 #pragma unroll
@@ -328,6 +389,7 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
           for (int j = 0; j < NP; ++j) horner_step<CK, CPLX>(br[j], bi[j], zr[j], zi[j], a[u]);
         }
       }
+    }
     }
     for (; k >= f0; --k) {
       const CT a = cb[k];
