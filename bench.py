@@ -134,14 +134,18 @@ def reduce_sum(pg, v: float, device) -> float:
     return float(t.item())
 
 
-def algorithmic_fma(diag_fields, cplx: bool) -> float:
+def algorithmic_fma(diag_fields, cplx: bool, parts: bool = False):
     """sum over points of c (K + 2 ceil(log2 l) [l > 0]): the paper's count (PAPER.md:1621-1627,
-    1321-1324), c = 4 fp64 FMAs per complex multiply-add, 1 for real."""
+    1321-1324), c = 4 fp64 FMAs per complex multiply-add, 1 for real.  parts=True returns the window
+    part c K (the Horner over the kept terms: the evaluator kernels) and the power part c 2 ceil(log2 l)
+    (z^l: applied by k_unsort's epilogue) separately."""
     import torch
     K = diag_fields["kept"].double()
     l = diag_fields["l"].double()
     pw = torch.where(l > 0, 2.0 * torch.ceil(torch.log2(torch.clamp(l, min=1.0))), torch.zeros_like(l))
     c = 4.0 if cplx else 1.0
+    if parts:
+        return float((c * K).sum()), float((c * pw).sum())
     return float((c * (K + pw)).sum())
 
 
@@ -232,14 +236,21 @@ def extra_context(device: int, steps: int = 3):
             del a
         except Exception as e:  # noqa: BLE001
             out[f"precondition_cfg{cfg}"] = {"error": repr(e)[:200]}
-    specs = [(1, None, False), (2, None, False), (4, None, False), (5, None, False), (5, None, True)]
-    for cfg, n, fp32 in specs:
-        name = f"cfg{cfg}" + ("_fp32" if fp32 else "")
+    # the BASELINE configs, then the second point sets of SURVEY 8(f) row 4 on the cfg5 / cfg2 polynomials
+    specs = [(1, None, False, None), (2, None, False, None), (4, None, False, None), (5, None, False, None),
+             (5, None, True, None), (5, 1 << 24, False, "disk"), (2, None, False, "rbar")]
+    for cfg, n, fp32, pset in specs:
+        name = f"cfg{cfg}" + ("_fp32" if fp32 else "") + (f"_{pset}" if pset else "")
         try:
             c = workloads.CONFIGS[cfg]
             n = n or c["n_points"]
             a = workloads.coefficients(cfg)
-            p = workloads.points(cfg, n)
+            if pset == "disk":
+                p = workloads.disk_points(cfg, n)
+            elif pset == "rbar":
+                p = workloads.rbar_points(cfg, n)
+            else:
+                p = workloads.points(cfg, n)
             if fp32:
                 a, p = workloads.to_fp32(a), workloads.to_fp32(p)
             poly = fpe.precondition(a, device=device)
@@ -249,7 +260,10 @@ def extra_context(device: int, steps: int = 3):
             _, _, dg = poly.evaluate(sub, exps=True, diag=True)
             D = fpe.diag_fields(dg)
             cplx = np.iscomplexobj(a)
-            work_pt = algorithmic_fma(D, cplx) / sub.numel()
+            wwin, wpow = algorithmic_fma(D, cplx, parts=True)
+            # dense: the evaluator kernels do the window sums (z^l in k_unsort); sparse: k_eval_sparse_coop
+            # forms every term's power itself
+            work_pt = (wwin + (wpow if poly.info["sparse"] else 0.0)) / sub.numel()
             meanK = float(D["kept"].double().mean())
             del dg, D
             vals = torch.empty(n, dtype=(torch.complex64 if cplx else torch.float32) if fp32 else
@@ -260,8 +274,10 @@ def extra_context(device: int, steps: int = 3):
             stages = dict(poly.last_stage_ms())
             poly.set_profiling(False)
             peak = FP64_FMA_PEAK * (2 if fp32 else 1)
-            ev_ms = sum(v for k, v in stages.items() if k in ("eval_mma", "eval_tiled")) or max(stages.values())
-            out[name] = {"workload": c["name"], "points": n, "evals_per_s": n / (ms * 1e-3), "ms_per_step": ms,
+            ev_ms = sum(v for k, v in stages.items() if k in ("eval_mma", "eval_tiled", "eval_overflow")) or \
+                max(stages.values())
+            out[name] = {"workload": c["name"] + (f" at {pset} points" if pset else ""), "points": n,
+                         "evals_per_s": n / (ms * 1e-3), "ms_per_step": ms,
                          "mean_kept_terms": meanK, "stages_ms": stages,
                          "eval_kernel_fma_frac": work_pt * n / (ev_ms * 1e-3) / peak,
                          "sparse": bool(poly.info["sparse"]), "dtype": "f32" if fp32 else "f64"}
@@ -371,7 +387,8 @@ def run_fpe(args):
     # algorithmic work from one untimed diagnostic pass
     _, _, dg = poly.evaluate(pts, exps=True, diag=True)
     D = fpe.diag_fields(dg)
-    fma_total = algorithmic_fma(D, cplx)
+    fma_window, fma_power = algorithmic_fma(D, cplx, parts=True)
+    fma_total = fma_window + fma_power
     meanK = float(D["kept"].double().mean())
     kq = torch.quantile(D["kept"].double()[:: max(1, D["kept"].numel() // (1 << 22))], torch.tensor([0.5, 0.99], dtype=torch.float64, device=D["kept"].device))
     kept_stats = {"median": float(kq[0]), "p99": float(kq[1]), "max": int(D["kept"].max())}
@@ -418,7 +435,9 @@ def run_fpe(args):
     ev_keys = [k for k in ("eval_mma", "eval_tiled", "eval_overflow") if k in stages]
     dom = "+".join(ev_keys) if ev_keys else max(stages, key=stages.get)
     dom_ms = sum(stages[k] for k in ev_keys) if ev_keys else stages[dom]
-    achieved = 2.0 * fma_total / (dom_ms * 1e-3) / 1e12        # TFLOP/s (2 flops per FMA)
+    # the evaluator kernels do the window sums (c K per point); z^l is applied by k_unsort's epilogue, so
+    # its 2 ceil(log2 l) multiplications are not credited to them
+    achieved = 2.0 * fma_window / (dom_ms * 1e-3) / 1e12        # TFLOP/s (2 flops per FMA)
     peak = 2.0 * FP64_FMA_PEAK * (2 if fp32 else 1) / 1e12   # fp32: 128 FMA lanes / SM / clk
 
     # -- end to end through the public API with host buffers (pinned) ---------------------------
@@ -472,7 +491,10 @@ def run_fpe(args):
                                   "fp64 FMA: 148 SM x 64 lanes x 1.965 GHz x 2 (guide unit counts/clock); the FP64 "
                                   "tensor cores (DMMA, k_eval_mma) run on the same datapath: 18.5T FMA/s measured "
                                   "(profiles/r01_dmma_vs_dfma.json)",
-                     "algorithmic_fma_per_launch": fma_total, "kernel_ms": dom_ms, "stages_ms": stages},
+                     "algorithmic_fma_per_launch": fma_window, "algorithmic_fma_step": fma_total,
+                     "algorithmic_note": "window sums c*K over the kept terms (the evaluator kernels); the step also "
+                                         "applies z^l (c*2*ceil(log2 l) per point) in k_unsort",
+                     "kernel_ms": dom_ms, "stages_ms": stages},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches * args.steps),

@@ -608,7 +608,7 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   // slot's own kernel stream -> D2H (one copy stream).  Consecutive chunks' kernels overlap, so one
   // chunk's evaluator tail (its last long-window groups) runs beside the next chunk's work; the chunks
   // stay large enough for the evaluator's window sharing (points of similar |z| per group), and the
-  // first one is smaller so that the D2H stream -- the steady-state bound -- starts early.
+  // first ones are smaller (a geometric ramp) so that the D2H stream -- the steady-state bound -- starts early.
   static const int kSlots = [] {
     const char* e = std::getenv("FPE_HOST_SLOTS");   // tuning experiments only
     return e ? std::max(2, std::min(fpe_poly_s::kHostSlots, std::atoi(e))) : 6;
@@ -619,7 +619,7 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   }();
   static const int lg_first = [] {
     const char* e = std::getenv("FPE_HOST_FIRST_LOG2");   // tuning experiments only
-    return e ? std::max(16, std::min(26, std::atoi(e))) : 21;
+    return e ? std::max(16, std::min(26, std::atoi(e))) : 20;
   }();
   const long long chunk = std::min<long long>(n_points, 1ll << lg_chunk);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -645,7 +645,14 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   cudaStream_t s_out = static_cast<cudaStream_t>(h->st_streams[1]);
   auto slot_base = [&](int b) { return static_cast<char*>(h->st_dev) + b * per; };
   auto slot_ws = [&](int b) { return slot_base(b) + al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8); };
-  const int used = (int)std::min<long long>(kSlots, (n_points - std::min<long long>(chunk, 1ll << lg_first) + chunk - 1) / chunk + 1);
+  // chunk sizes ramp up geometrically from 2^lg_first to `chunk`, so that the first results start their way
+  // back to the host early (the D2H stream is the steady-state bound)
+  auto next_size = [&](long long cur) { return std::min(chunk, cur * 2); };
+  int used = 0;
+  {
+    long long cur = std::min<long long>(chunk, 1ll << lg_first);
+    for (long long off = 0; off < n_points && used < kSlots; off += cur, cur = next_size(cur)) ++used;
+  }
   for (int b = 0; b < used; ++b) FPE_CUDA(cudaMemsetAsync(slot_ws(b), 0, kWsHeader, s_in));   // counters, before every chunk
   auto ev = [&](int slot, int kind) { return static_cast<cudaEvent_t>(h->st_events[slot * 3 + kind]); };
   long long launches = 0;
@@ -680,7 +687,7 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
   long long next = std::min<long long>(chunk, 1ll << lg_first);
   for (long long off = 0, c = 0, m = 0; off < n_points; off += m, ++c) {
     m = std::min(next, n_points - off);
-    next = chunk;
+    next = next_size(next);
     const int b = (int)(c % kSlots);
     cudaStream_t s_ev = static_cast<cudaStream_t>(h->st_streams[2 + b]);
     char* base = slot_base(b);

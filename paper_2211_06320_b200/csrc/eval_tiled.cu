@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
     }
     hull = sh;
   }
-  for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) hist[b] = 0;
+  const int cb = coarse_bits(n), nbk = 1 << cb;
+  for (int b = threadIdx.x; b < nbk; b += blockDim.x) hist[b] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long beg = (long long)blockIdx.x * ppc, end = min(n, beg + ppc);
@@ -124,13 +125,13 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
     // every point keeps its rank inside its (CTA, bucket) slice, so the scatter needs no atomics (one
     // shared-memory atomic per point: buckets rarely repeat within a warp, and warp-aggregating them
     // with __match_any_sync cost more than it saved -- 1.70 vs 1.59 ms)
-    if (ok) keys[2 * i + 1] = atomicAdd(&hist[key >> (24 - kCoarseBits)], 1u);
+    if (ok) keys[2 * i + 1] = atomicAdd(&hist[key >> (24 - cb)], 1u);
   }
   __syncthreads();
   // claim this CTA's slice of every bucket
-  for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) {
+  for (int b = threadIdx.x; b < nbk; b += blockDim.x) {
     const uint32_t c = hist[b];
-    cta_base[(size_t)blockIdx.x * kBuckets + b] = c ? atomicAdd(gcount + b, c) : 0u;
+    cta_base[((size_t)blockIdx.x << cb) + b] = c ? atomicAdd(gcount + b, c) : 0u;
   }
 }
 
@@ -452,13 +453,20 @@ __device__ __noinline__ void acc_fold(Acc& A, double hr, double hi, int pbase, d
   A.base = pbase;
 }
 
-__device__ __forceinline__ void stage_value(PtOut* out, long long pos, double re, double im, long long E) {
-  const unsigned long long a = __double_as_longlong(re), b = __double_as_longlong(im), e = (unsigned long long)E;
+// The evaluators stage a point's accumulator -- acc (re, im) 2^E, relative to z^n with n = base + k_min (n = -1:
+// nothing accumulated) -- and k_unsort applies the epilogue Q = acc z^n (finalize) on the way to the caller's
+// order: the polar-route power is fp64 work that would compete with the Horner DFMAs for the fp64 pipe here,
+// while k_unsort is bound by its random gathers and has the issue slots to spare.
+__device__ __forceinline__ void stage_acc(PtOut* out, long long pos, const Acc& A, long long extraE, int kmin) {
+  const unsigned long long a = __double_as_longlong(A.started ? A.r : 0.0), b = __double_as_longlong(A.started ? A.i : 0.0);
+  const unsigned long long e = (unsigned long long)extraE;
+  const unsigned long long nn = (unsigned long long)(A.started ? (long long)A.base + kmin : -1ll);
   asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(out + pos), "r"((uint32_t)a),
                "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)), "r"((uint32_t)e),
-               "r"((uint32_t)(e >> 32)), "r"(0u), "r"(0u)
+               "r"((uint32_t)(e >> 32)), "r"((uint32_t)nn), "r"((uint32_t)(nn >> 32))
                : "memory");
 }
+
 
 // Q = acc z^l as (re + i im) 2^E; the caller stages it (evaluator: over the point's record, in bucket
 // order -- every warp that reads the record has done so before the last piece is folded) or stores it
@@ -687,10 +695,7 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c,
   prefetch();
 #pragma unroll
   for (int j = 0; j < NP; ++j)
-    if (S.valid[j]) {
-      const Fin f = finalize<CPLX, PtTraits<OK>::f32>(S.x[j], S.y[j], A[j], P);
-      stage_value(out, S.idx[j], f.re, f.im, f.E);
-    }
+    if (S.valid[j]) stage_acc(out, S.idx[j], A[j], 0, (int)P.k_min);
 }
 
 // One warp evaluates piece p of a multi-piece group into its scratch slot; the warp that completes
@@ -736,8 +741,7 @@ __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long
         }
       }
     }
-    const Fin f = finalize<CPLX, PtTraits<OK>::f32>(S.x[j], S.y[j], A, P);
-    stage_value(out, S.idx[j], f.re, f.im, f.E);
+    stage_acc(out, S.idx[j], A, 0, (int)P.k_min);
   }
 }
 
@@ -927,22 +931,13 @@ __global__ void __launch_bounds__(256) k_eval_wide(long long n, PolyDev P, PtRec
         xacc_fold<CPLX>(A, br, bi, E, lo, x, y);
       }
     }
-    // Q = A z^(base + k_min) (finalize's polar power; z = 0 and non-finite z as finalize)
-    Fin f;
-    if (!A.started) {
-      Acc a0{0.0, 0.0, 0, false};
-      f = finalize<CPLX>(x, y, a0, P);
-      if (x == 0.0 && y == 0.0 && h.w >= h.z) {   // z = 0: a_0 (window {k_min})
-        double cr = 0.0, ci = 0.0;
-        a0_value<CK>(P, cr, ci);
-        f = Fin{cr, ci, (cr == 0.0 && ci == 0.0) ? 0 : (long long)P.shift};
-      }
-    } else {
-      Acc a{A.r, A.i, A.base, true};
-      f = finalize<CPLX>(x, y, a, P);
-      f.E += A.E;
+    if (!A.started && x == 0.0 && y == 0.0 && h.w >= h.z) {   // z = 0: the window {k_min}, value a_0 (finalize)
+      double cr = 0.0, ci = 0.0;
+      a0_value<CK>(P, cr, ci);
+      A = XAcc{cr, ci, 0, 0, true};
     }
-    stage_value(out, pos, f.re, f.im, f.E);
+    const Acc a{A.r, A.i, A.base, A.started};
+    stage_acc(out, pos, a, A.started ? A.E : 0, kmin);
   }
 }
 
@@ -1099,14 +1094,16 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
 // Results from bucket order to the caller's order: a coalesced pass over the caller's indices gathering one
 // 32-byte staged result each (a random sector read instead of the evaluator's random partial-sector
 // writes, which the DRAM turns into read-modify-writes).
-template <int OK>
+template <int PK, int OK>
 __global__ void __launch_bounds__(256) k_unsort(const PtOut* __restrict__ staged, const uint32_t* __restrict__ spos,
-                                                long long n, void* __restrict__ vals, long long* __restrict__ exps) {
+                                                long long n, const void* __restrict__ pts, PolyDev P,
+                                                void* __restrict__ vals, long long* __restrict__ exps) {
+  constexpr bool CPLX = PtTraits<OK>::cplx;
   constexpr int U = 4;   // independent gathers in flight per thread
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
-    double re[U], im[U];
-    long long E[U];
+    double re[U], im[U], x[U], y[U];
+    long long E[U], nn[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const long long i = i0 + u * stride;
@@ -1118,12 +1115,18 @@ __global__ void __launch_bounds__(256) k_unsort(const PtOut* __restrict__ staged
         re[u] = __hiloint2double((int)w[1], (int)w[0]);
         im[u] = __hiloint2double((int)w[3], (int)w[2]);
         E[u] = (long long)(((unsigned long long)w[5] << 32) | w[4]);
+        nn[u] = (long long)(((unsigned long long)w[7] << 32) | w[6]);
+        load_point<PK>(pts, i, x[u], y[u]);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const long long i = i0 + u * stride;
-      if (i < n) store_value<OK>(vals, exps, i, re[u], im[u], E[u]);
+      if (i < n) {
+        const Acc A{re[u], im[u], (int)(nn[u] >= 0 ? nn[u] - P.k_min : 0), nn[u] >= 0};
+        const Fin f = finalize<CPLX, PtTraits<OK>::f32>(x[u], y[u], A, P);
+        store_value<OK>(vals, exps, i, f.re, f.im, f.E + E[u]);
+      }
     }
   }
 }
@@ -1302,13 +1305,18 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   }
   const long long blocks = std::min<long long>((n + 4 * 256 - 1) / (4 * 256), 148ll * 16);
   const PtOut* staged = reinterpret_cast<const PtOut*>(rec);
+#define FPE_UN(PKV, OKV) k_unsort<PKV, OKV><<<(int)blocks, 256, 0, s>>>(staged, spos, n, pts, P, vals, exps)
   switch (pk * 4 + P.cdt) {   // the output kind follows NPFor<PK, CK>::OK
-    case FPE_R64 * 4 + FPE_R64: k_unsort<FPE_R64><<<(int)blocks, 256, 0, s>>>(staged, spos, n, vals, exps); break;
-    case FPE_R32 * 4 + FPE_R32: k_unsort<FPE_R32><<<(int)blocks, 256, 0, s>>>(staged, spos, n, vals, exps); break;
-    case FPE_R32 * 4 + FPE_C32: case FPE_C32 * 4 + FPE_R32: case FPE_C32 * 4 + FPE_C32:
-      k_unsort<FPE_C32><<<(int)blocks, 256, 0, s>>>(staged, spos, n, vals, exps); break;
-    default: k_unsort<FPE_C64><<<(int)blocks, 256, 0, s>>>(staged, spos, n, vals, exps); break;
+    case FPE_R64 * 4 + FPE_R64: FPE_UN(FPE_R64, FPE_R64); break;
+    case FPE_R64 * 4 + FPE_C64: FPE_UN(FPE_R64, FPE_C64); break;
+    case FPE_C64 * 4 + FPE_R64: FPE_UN(FPE_C64, FPE_C64); break;
+    case FPE_C64 * 4 + FPE_C64: FPE_UN(FPE_C64, FPE_C64); break;
+    case FPE_R32 * 4 + FPE_R32: FPE_UN(FPE_R32, FPE_R32); break;
+    case FPE_R32 * 4 + FPE_C32: FPE_UN(FPE_R32, FPE_C32); break;
+    case FPE_C32 * 4 + FPE_R32: FPE_UN(FPE_C32, FPE_C32); break;
+    default: FPE_UN(FPE_C32, FPE_C32); break;
   }
+#undef FPE_UN
   st.mark("unsort");
   return 5 + le + lm;
 }

@@ -73,7 +73,7 @@ FPE_HD dd_t dd_times_inv_ln2(dd_t a) {
 // log2 of a double-double v = vh + vl > 0 (vh normal): j + log2(v 2^-j).
 FPE_HD dd_t log2_dd(double vh, double vl) {
   int j = frexp_exp(vh);
-  double f = ldexp(vh, -j), fl = ldexp(vl, -j);
+  double f = ldexp_fast(vh, -j), fl = ldexp_fast(vl, -j);
   if (f < FPE_LOGTAB_F0) { f *= 2.0; fl *= 2.0; j -= 1; }
   dd_t L = dd_times_inv_ln2(ln_table(f, fl));
   dd_t s = two_sum((double)j, L.hi);
@@ -102,7 +102,7 @@ FPE_HD dd_t log2abs_quick(double x, double y, bool cplx) {
     }
   }
   const int e = frexp_exp(ax);
-  const double xs = ldexp(ax, -e), ys = ldexp(ay, -e);   // xs in [1/2, 1)
+  const double xs = ldexp_fast(ax, -e), ys = ldexp_fast(ay, -e);   // xs in [1/2, 1)
   dd_t p = two_prod(xs, xs), q = two_prod(ys, ys);
   dd_t s = two_sum(p.hi, q.hi);
   dd_t v = fast_two_sum(s.hi, fpe_add(s.lo, fpe_add(p.lo, q.lo)));   // |z|^2 4^-e in [1/4, 2)
@@ -132,10 +132,16 @@ FPE_HD dd_t atan2_turns(double x, double y) {
   if (sw) { double t = ax; ax = ay; ay = t; }
   {  // scale to ax in [1/2, 1) so that TwoProd stays exact for subnormal / huge inputs
     const int e = frexp_exp(ax);
-    ax = ldexp(ax, -e);
-    ay = ldexp(ay, -e);
+    ax = ldexp_fast(ax, -e);
+    ay = ldexp_fast(ay, -e);
   }
+  // table index round(128 ay/ax): only needs to be nearly right (|u| stays ~2^-8, far inside the series'
+  // range), so one fp32 division on the device instead of an fp64 one
+#ifdef __CUDA_ARCH__
+  const int j = min(128, __float2int_rn(__fdividef((float)ay, (float)ax) * 128.0f));
+#else
   const int j = fpe_d2i_rn(fpe_div(ay, ax) * 128.0);        // 0..128
+#endif
   const double c = (double)j * 0.0078125;
   // u = (ay - c ax) / (ax + c ay), atan(ay/ax) = atan(c) + atan(u), |u| <= 2^-8
   dd_t pc = two_prod(c, ax);
@@ -143,10 +149,19 @@ FPE_HD dd_t atan2_turns(double x, double y) {
   dd_t qc = two_prod(c, ay);
   dd_t den = two_sum(ax, qc.hi);
   den = fast_two_sum(den.hi, fpe_add(den.lo, qc.lo));
+  // u = num / den as uh + ul: uh from a reciprocal good to ~2^-46 (device: fp32 rcp + one Newton step),
+  // the exact remainder, and ul = remainder / den at the same accuracy -- |uh + ul - u| ~ 2^-92 |u|
+#ifdef __CUDA_ARCH__
+  const double rd0 = (double)__frcp_rn((float)den.hi);
+  const double rd = fpe_fma(rd0, fpe_fma(-den.hi, rd0, 1.0), rd0);
+  const double uh = fpe_mul(num.hi, rd);
+#else
+  const double rd = fpe_div(1.0, den.hi);
   const double uh = fpe_div(num.hi, den.hi);
+#endif
   double rr = fpe_fma(-uh, den.hi, num.hi);                 // exact remainder
   rr = fpe_add(rr, fpe_fma(-uh, den.lo, num.lo));
-  const double ul = fpe_div(rr, den.hi);
+  const double ul = fpe_mul(rr, rd);
   const double s = fpe_mul(uh, uh);
   double R = -1.0 / 11.0;
   R = fpe_fma(R, s, 1.0 / 9.0);

@@ -2,7 +2,7 @@
 //
 // Points carry a 24-bit key that is monotone in lambda (bits 0..22) with bit 23 = "long window";
 // l and r are both non-decreasing in lambda, so points with close keys have nested, nearly equal windows.
-// One counting-sort pass by the top kCoarseBits of the key (32768 buckets): k_classify_bucket
+// One counting-sort pass by the top coarse_bits(n) of the key (32768 buckets from 2^20 points up): k_classify_bucket
 // (eval_tiled.cu) builds a per-CTA histogram in shared memory, claims each CTA's slice of every bucket with
 // one global atomicAdd per nonzero bin and keeps every point's rank in its slice; k_bucket_scan turns
 // bucket totals into starts; k_bucket_scatter moves the records {index, key, l, r} and the points to
@@ -21,14 +21,15 @@ namespace fpe {
 // Exclusive scan of the kBuckets bucket totals into bucket starts (one CTA; buckets are laid out in
 // key order, so the record array ends up sorted by the top kCoarseBits of the key).
 __global__ void __launch_bounds__(1024) k_bucket_scan(const uint32_t* __restrict__ gcount,
-                                                      uint32_t* __restrict__ bstart) {
+                                                      uint32_t* __restrict__ bstart, int cb) {
   constexpr int kPer = kBuckets / 1024;
+  const int per = (1 << cb) / 1024;   // buckets per thread (cb >= 10)
   __shared__ uint32_t ws[32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   uint32_t c[kPer];
   uint32_t s = 0;
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) { c[j] = gcount[t * kPer + j]; s += c[j]; }
+  for (int j = 0; j < kPer; ++j) { c[j] = j < per ? gcount[t * per + j] : 0u; s += c[j]; }
   uint32_t x = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(const uint32_t* __restrict
   __syncthreads();
   uint32_t run = (wid ? ws[wid - 1] : 0) + x - s;
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) { bstart[t * kPer + j] = run; run += c[j]; }
+  for (int j = 0; j < kPer; ++j) if (j < per) { bstart[t * per + j] = run; run += c[j]; }
 }
 
 __device__ __forceinline__ double2 load_point_any(int pk, const void* __restrict__ p, long long i) {
@@ -61,7 +62,7 @@ __device__ __forceinline__ double2 load_point_any(int pk, const void* __restrict
 __global__ void __launch_bounds__(256) k_bucket_scatter(const uint2* __restrict__ keys, const int2* __restrict__ lr,
                                                         int pk, const void* __restrict__ pts, long long n,
                                                         long long ppc, const uint32_t* __restrict__ bstart,
-                                                        const uint32_t* __restrict__ cta_base,
+                                                        const uint32_t* __restrict__ cta_base, int cb,
                                                         PtRec* __restrict__ rec, uint32_t* __restrict__ spos) {
   constexpr int U = 4;   // independent loads in flight per thread
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -78,8 +79,8 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint2* __restrict_
     for (int u = 0; u < U; ++u) {
       const long long i = i0 + u * stride;
       if (i < n) {
-        const uint32_t c = kr[u].x >> (24 - kCoarseBits);
-        const uint32_t pos = __ldg(bstart + c) + __ldg(cta_base + (size_t)(i / ppc) * kBuckets + c) + kr[u].y;
+        const uint32_t c = kr[u].x >> (24 - cb);
+        const uint32_t pos = __ldg(bstart + c) + __ldg(cta_base + ((size_t)(i / ppc) << cb) + c) + kr[u].y;
         spos[i] = pos;
         // one 256-bit store (STG.E.ENL2.256): the whole 32-byte sector in one request
         const unsigned long long zx = __double_as_longlong(z[u].x), zy = __double_as_longlong(z[u].y);
@@ -162,9 +163,10 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const PtRec* __restri
 void bucket_finish(const uint2* keys, const int2* lr, long long n, long long ppc, const uint32_t* gcount,
                    const uint32_t* cta_base, uint32_t* bstart, PtRec* rec, uint32_t* spos, int pk,
                    const void* pts, long long k_min, const Plan& plan, cudaStream_t s) {
-  k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart);
+  const int cb = coarse_bits(n);
+  k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, cb);
   const long long blocks = std::min<long long>((n + 4 * 256 - 1) / (4 * 256), 148ll * 32);
-  k_bucket_scatter<<<(int)blocks, 256, 0, s>>>(keys, lr, pk, pts, n, ppc, bstart, cta_base, rec, spos);
+  k_bucket_scatter<<<(int)blocks, 256, 0, s>>>(keys, lr, pk, pts, n, ppc, bstart, cta_base, cb, rec, spos);
   const long long groups = (n + plan.gsize - 1) / plan.gsize;
   k_plan<<<(int)((groups + 7) / 8), 256, 0, s>>>(n, rec, k_min, plan);
 }

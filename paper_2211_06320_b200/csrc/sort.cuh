@@ -8,6 +8,13 @@ namespace fpe {
 constexpr int kCoarseBits = 15;                 // buckets: the top 15 of the 24 key bits (sign, exponent and
 constexpr int kBuckets = 1 << kCoarseBits;      // 7 mantissa bits of lambda + the long-window bit); groups of
                                                 // consecutive points of a bucket share 99% of their windows
+// Bucket bits for a batch of n points: 15 from 2^20 points up, fewer for small batches (~32 points per
+// bucket), so that the per-CTA histograms, slice claims and the bucket scan do not dominate them.
+__host__ __device__ __forceinline__ int coarse_bits(long long n) {
+  int b = 10;
+  while (b < kCoarseBits && (1ll << (b + 5)) < n) ++b;
+  return b;
+}
 constexpr int kScatterThreads = 1024;           // classify CTA size: one CTA per SM
 // points per classify CTA for a batch of n: one 1024-thread CTA per SM
 inline long long pts_per_cta(long long n) {
@@ -30,12 +37,12 @@ struct __align__(32) PtRec {
   int32_t l, r;
   double x, y;
 };
-// The evaluator overwrites a group's records with its results, in bucket order (coalesced; every read of
-// a record precedes its overwrite); k_unsort moves them to the caller's order.
+// The evaluator overwrites a group's records with its accumulators, in bucket order (coalesced; every read
+// of a record precedes its overwrite); k_unsort applies the epilogue and moves them to the caller's order.
 struct __align__(32) PtOut {
-  double re, im;
-  long long E;   // value = (re + i im) 2^E, before store_value's normalisation
-  long long pad;
+  double re, im;   // the point's accumulator acc (eval_tiled.cu stage_acc)
+  long long E;     // an extra binary exponent of acc (wide handles), else 0
+  long long n;     // value = acc 2^E z^n (k_unsort applies the power: finalize); -1: nothing accumulated
 };
 
 // A group: 32*NP consecutive points of the sorted permutation, evaluated by one warp (NP points per

@@ -56,6 +56,8 @@ def test_full_size(fpe, cfg, fp32, n_val):
     # -- indexing on every point ------------------------------------------------------------------------
     nbad = 0
     hard = 0
+    mean_width = float((D["r"] - D["l"] + 1).double().mean())
+    max_K = int(D["kept"].max())
     for lo in range(0, n, CHUNK):
         hi = min(n, lo + CHUNK)
         g = {k: x[lo:hi].cpu().numpy() for k, x in D.items() if k in ("lambda", "region", "l", "r", "kept", "hard")}
@@ -89,6 +91,11 @@ def test_full_size(fpe, cfg, fp32, n_val):
           f"counters {st}")
     assert np.all(err[fin] <= tol), (err[fin].max(), idx[np.argmax(np.where(fin, err, 0))])
     assert st["hard_lambdas"] == 0
+    # Theorem thm:equivAlgo: the mean band over the sphere is below 1 + 1.9046 sqrt(d D) (cfg3, cfg5); the
+    # worst case K <= d_eff + 1 (and cfg4's 4096 nonzeros)
+    if cfg in (3, 5):
+        assert mean_width < 1 + 1.9046 * np.sqrt(P.d_eff * P.drop)
+    assert max_K <= (4096 if cfg == 4 else P.d_eff + 1)
 
 
 @pytest.mark.parametrize("fp32", [False, True])

@@ -121,54 +121,7 @@ def test_empty_and_ragged(fpe):
 
 
 # ------------------------------------------------------- full-size configs ----
-def _sampled_config(fpe, cfg, n_idx, n_val, fp32=False, n_points=None):
-    a = workloads.coefficients(cfg)
-    pts = workloads.points(cfg, n_points)
-    if fp32:
-        a, pts = workloads.to_fp32(a), workloads.to_fp32(pts)
-    poly = fpe.precondition(a)
-    P = oracle.OraclePoly(a)
-    t = torch.from_numpy(pts).cuda()
-    v, e, dg = poly.evaluate(t, exps=True, diag=True)
-    idx = workloads.sample_indices(len(pts), n_idx, salt=cfg)
-    it = torch.from_numpy(idx).cuda()
-    import paper_2211_06320_b200 as m
-    D = {k: x[it].cpu().numpy() for k, x in m.diag_fields(dg).items()}
-    kept_all = m.diag_fields(dg)["kept"].double()
-    stats = {"mean_K": float(kept_all.mean()), "max_K": int(kept_all.max()),
-             "hard": int(m.diag_fields(dg)["hard"].sum())}
-    out = {"v": v[it].cpu().numpy(), "e": e[it].cpu().numpy()}
-    del v, e, dg, t
-    torch.cuda.empty_cache()
-    sub = pts[idx]
-    cls = check_indexing(P, sub, D)
-    vi = np.arange(min(n_val, len(idx)))
-    _values_ok(P, a, sub, out, vi, TOL32 if fp32 else TOL64, cls)
-    assert stats["hard"] == 0
-    return P, stats
-
-
-def test_cfg2_real_full(fpe):
-    P, st = _sampled_config(fpe, 2, 1 << 14, 256)
-    assert st["mean_K"] < 1 + 1.7673 * math.sqrt(P.d_eff * (P.drop + 1)) * 2   # real-line constant, loose
-
-
-def test_cfg3_bigrange_full(fpe):
-    P, st = _sampled_config(fpe, 3, 1 << 14, 128)
-    assert st["mean_K"] < 1 + 1.9046 * math.sqrt(P.d_eff * P.drop)
-
-
-def test_cfg4_sparse_full(fpe):
-    P, st = _sampled_config(fpe, 4, 1 << 14, 512)
-    assert st["max_K"] <= 4096
-
-
-@pytest.mark.parametrize("fp32", [False, True])
-def test_cfg5_full(fpe, fp32):
-    P, st = _sampled_config(fpe, 5, 1 << 13, 64, fp32=fp32)
-    assert st["mean_K"] < 1 + 1.9046 * math.sqrt(P.d_eff * P.drop)
-
-
+# (every point of cfg2-5 and cfg5-fp32 against the oracle: tests/test_gpu_fullsize.py)
 # --------------------------------------------------------- other entry points --
 def test_horner_context(fpe):
     a = workloads.coefficients(1)

@@ -25,16 +25,23 @@ def main(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[0]
+    units = dict(zip(hdr, rows[1]))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+             "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
     out = []
     for r in rows[2:]:
         if len(r) != len(hdr):
             continue
         d = dict(zip(hdr, r))
-        k = {"kernel": d.get("Kernel Name", "")[:120]}
+        k = {"kernel": d.get("Kernel Name", "")[:120], "units": "bytes for dram__*, ms for gpu__time_duration"}
         for key in RAW_KEYS:
             if key in d:
                 try:
-                    k[key] = float(d[key].replace(",", ""))
+                    v = float(d[key].replace(",", ""))
+                    u = units.get(key, "")
+                    if key.startswith("dram__bytes") or key == "gpu__time_duration.sum":
+                        v *= scale.get(u, 1.0)
+                    k[key] = v
                 except ValueError:
                     k[key] = d[key]
         stalls = {c.split("smsp__pcsamp_warps_issue_stalled_")[1]: float(d[c] or 0)
