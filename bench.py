@@ -203,10 +203,10 @@ def extra_context(device: int, steps: int = 3):
     import workloads
     dev = torch.device("cuda", device)
     out = {}
-    try:   # full Horner, cfg3 polynomial (d = 2^20 - 1), 2^17 sphere points
+    try:   # full Horner, cfg3 polynomial (d = 2^20 - 1), 2^20 sphere points (3.5 waves of the persistent warps)
         poly = fpe.precondition(workloads.coefficients(3), device=device)
-        pts = torch.from_numpy(workloads.points(3, 1 << 17, shard=5)).to(dev)
-        ms = _time_ms(lambda: poly.horner(pts), steps, 1)
+        pts = torch.from_numpy(workloads.points(3, 1 << 20, shard=5)).to(dev)
+        ms = _time_ms(lambda: poly.horner(pts), 2, 1)
         fma = 4.0 * (poly.info["k_max"] - poly.info["k_min"] + 1) * pts.numel()
         out["full_horner_cfg3"] = {"evals_per_s": pts.numel() / (ms * 1e-3), "ms": ms, "points": pts.numel(),
                                    "fma_per_s": fma / (ms * 1e-3)}

@@ -643,6 +643,9 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
     }
   cudaStream_t s_in = static_cast<cudaStream_t>(h->st_streams[0]);
   cudaStream_t s_out = static_cast<cudaStream_t>(h->st_streams[1]);
+  // the exponents' device->host copies on a second stream (a second copy engine), when FPE_HOST_SPLIT_D2H=1
+  static const bool split_d2h = [] { const char* e = std::getenv("FPE_HOST_SPLIT_D2H"); return e && e[0] == '1'; }();
+  cudaStream_t s_out2 = split_d2h ? static_cast<cudaStream_t>(h->st_streams[2 + fpe_poly_s::kHostSlots]) : s_out;
   auto slot_base = [&](int b) { return static_cast<char*>(h->st_dev) + b * per; };
   auto slot_ws = [&](int b) { return slot_base(b) + al(chunk * in_sz) + al(chunk * out_sz) + al(chunk * 8); };
   // chunk sizes ramp up geometrically from 2^lg_first to `chunk`, so that the first results start their way
@@ -654,7 +657,7 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
     for (long long off = 0; off < n_points && used < kSlots; off += cur, cur = next_size(cur)) ++used;
   }
   for (int b = 0; b < used; ++b) FPE_CUDA(cudaMemsetAsync(slot_ws(b), 0, kWsHeader, s_in));   // counters, before every chunk
-  auto ev = [&](int slot, int kind) { return static_cast<cudaEvent_t>(h->st_events[slot * 3 + kind]); };
+  auto ev = [&](int slot, int kind) { return static_cast<cudaEvent_t>(h->st_events[slot * 4 + kind]); };
   long long launches = 0;
   static const bool trace = std::getenv("FPE_HOST_TRACE") != nullptr;   // debugging: per-chunk timeline
   std::vector<cudaEvent_t> tev;
@@ -695,7 +698,10 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
     void* dv = base + al(chunk * in_sz);
     long long* de = reinterpret_cast<long long*>(base + al(chunk * in_sz) + al(chunk * out_sz));
     void* wsp = slot_ws(b);
-    if (c >= kSlots) FPE_CUDA_P(cudaStreamWaitEvent(s_in, ev(b, 2), 0));   // slot's previous results copied out
+    if (c >= kSlots) {   // the slot's previous results copied out
+      FPE_CUDA_P(cudaStreamWaitEvent(s_in, ev(b, 2), 0));
+      if (split_d2h) FPE_CUDA_P(cudaStreamWaitEvent(s_in, ev(b, 3), 0));
+    }
     mark(s_in);
     FPE_CUDA_P(cudaMemcpyAsync(dp, static_cast<const char*>(points_host) + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
     mark(s_in);
@@ -712,12 +718,15 @@ fpe_status fpe_evaluate_host(fpe_poly h, const void* points_host, fpe_dtype pt_d
     FPE_CUDA_P(cudaStreamWaitEvent(s_out, ev(b, 1), 0));
     mark(s_out);
     FPE_CUDA_P(cudaMemcpyAsync(static_cast<char*>(values_host) + off * out_sz, dv, m * out_sz, cudaMemcpyDeviceToHost, s_out));
-    if (exps_host) FPE_CUDA_P(cudaMemcpyAsync(exps_host + off, de, m * 8, cudaMemcpyDeviceToHost, s_out));
+    if (split_d2h) FPE_CUDA_P(cudaStreamWaitEvent(s_out2, ev(b, 1), 0));
+    if (exps_host) FPE_CUDA_P(cudaMemcpyAsync(exps_host + off, de, m * 8, cudaMemcpyDeviceToHost, s_out2));
     mark(s_out);
     FPE_CUDA_P(cudaEventRecord(ev(b, 2), s_out));
+    if (split_d2h) FPE_CUDA_P(cudaEventRecord(ev(b, 3), s_out2));
   }
 #undef FPE_CUDA_P
-  const cudaError_t se = cudaStreamSynchronize(s_out);
+  cudaError_t se = cudaStreamSynchronize(s_out);
+  if (se == cudaSuccess && split_d2h) se = cudaStreamSynchronize(s_out2);
   if (se != cudaSuccess) {
     set_error("fpe_evaluate_host: %s", cudaGetErrorString(se));
     return fail(FPE_ERR_CUDA);

@@ -959,15 +959,19 @@ __device__ __forceinline__ void stream_full(Ring<CK>& R, int lo, int hi, const t
   constexpr int kDrop = F32 ? 150 : 1100;    // 2^-E underflows the working type
   constexpr int kBlk = F32 ? 1 : 8;          // steps between checks: |z|^kBlk 2^kHalf stays finite for
                                              // |z| < 2^65 (fp64); fp32 checks every step
+  W s[NP];                                   // 2^-E: the scale of the coefficients still to come
+#pragma unroll
+  for (int j = 0; j < NP; ++j) s[j] = (W)1;
   auto rescale = [&]() {
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
       const double m = fmax(fabs((double)br[j]), fabs((double)bi[j]));
       if (m > ldexp(1.0, kHalf) && isfinite(m)) {
         const int e = frexp_exp(m);
-        br[j] = (W)ldexp((double)br[j], -e);
-        bi[j] = (W)ldexp((double)bi[j], -e);
+        br[j] = (W)ldexp_fast((double)br[j], -e);
+        bi[j] = (W)ldexp_fast((double)bi[j], -e);
         E[j] += e;
+        s[j] = E[j] > kDrop ? (W)0 : (W)ldexp(1.0, -E[j]);
       }
     }
   };
@@ -1003,9 +1007,6 @@ __device__ __forceinline__ void stream_full(Ring<CK>& R, int lo, int hi, const t
           }
         }
       } else {
-        W s[NP];
-#pragma unroll
-        for (int j = 0; j < NP; ++j) s[j] = E[j] > kDrop ? (W)0 : (W)ldexp(1.0, -E[j]);
         auto scaled_step = [&](const CT& a) {
 #pragma unroll
           for (int j = 0; j < NP; ++j) {

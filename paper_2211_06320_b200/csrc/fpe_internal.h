@@ -72,8 +72,8 @@ struct fpe_poly_s {
   // staging for fpe_evaluate_host (grown on demand, owned)
   void* st_dev = nullptr; size_t st_bytes = 0;
   static constexpr int kHostSlots = 8;   // staging slots available to fpe_evaluate_host
-  void* st_streams[2 + kHostSlots] = {};   // H2D copies, D2H copies, one kernel stream per staging slot
-  void* st_events[3 * kHostSlots] = {};    // per staging slot: h2d done, eval done, d2h done
+  void* st_streams[3 + kHostSlots] = {};   // H2D copies, D2H copies, one kernel stream per staging slot, D2H #2
+  void* st_events[4 * kHostSlots] = {};    // per staging slot: h2d done, eval done, d2h done, d2h #2 done
   fpe::PolyDev view() const;
 };
 

@@ -85,7 +85,6 @@ __device__ __forceinline__ void xadd(double& sr, double& si, long long& se, doub
   if (m != 0.0) { const int e = frexp_exp(m); sr = ldexp_fast(sr, -e); si = ldexp_fast(si, -e); se += e; }
 }
 
-constexpr int kSparseSmemIdx = 8192;   // good indices staged in shared memory (32 KiB)
 
 // Points have very uneven kept counts (cfg4: mean 1.15, max ~1800 near |z| = 1), so a lane-per-point loop
 // would run each warp for its longest point (round 1: 62% of the instructions at 1-7 active lanes).  A warp
@@ -95,7 +94,7 @@ constexpr int kSparseSmemIdx = 8192;   // good indices staged in shared memory (
 // lane sums its own point's terms in increasing k in extended range.  A point's result is therefore the
 // same whatever points share its warp.
 constexpr int kSpWarps = 8;
-constexpr int kSpRound = 128;   // terms per warp and round in shared memory
+constexpr int kSpRound = 64;    // terms per warp and round in shared memory
 constexpr int kSpTab = 4096;    // buckets of the good-index table
 struct SpTerm { double r, i; long long e; };
 
@@ -129,25 +128,19 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
   int* offs = reinterpret_cast<int*>(pol + kSpWarps * 32);                                         // [warps][33]
   int* firsts = offs + kSpWarps * 33;                                                              // [warps][32]
   int* tab = firsts + kSpWarps * 32;               // [kSpTab + 1] bucket -> first good index position
-  int* sidx_s = tab + kSpTab + 1;
-  const int32_t* sidx = P.sidx;
+  const int32_t* __restrict__ sidx = P.sidx;       // read through L1 (16 KiB at cfg4)
   const int ng = (int)P.n_good;
-  const bool staged = ng <= kSparseSmemIdx;
-  // the good indices in shared memory, and a bucket table over [k_min, k_max] (buckets of 2^tb indices):
-  // the first good index >= k lies in [tab[b], tab[b + 1]] for b = (k - k_min) >> tb, so each window
-  // bound costs a search over ~ng / kSpTab entries instead of log2(ng) steps
+  // a bucket table over [k_min, k_max] (buckets of 2^tb indices): the first good index >= k lies in
+  // [tab[b], tab[b + 1]] for b = (k - k_min) >> tb, so each window bound costs a search over ~ng / kSpTab
+  // entries instead of log2(ng) steps
   int tb = 0;
   while (((P.k_max - P.k_min) >> tb) >= kSpTab) ++tb;
   const int nb = (int)((P.k_max - P.k_min) >> tb) + 1;
-  if (staged) {
-    for (int i = threadIdx.x; i < ng; i += blockDim.x) sidx_s[i] = P.sidx[i];
-    for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
-      const long long key = P.k_min + ((long long)b << tb);
-      int lo = 0, hi = ng;
-      while (lo < hi) { const int m = (lo + hi) >> 1; if ((long long)__ldg(P.sidx + m) < key) lo = m + 1; else hi = m; }
-      tab[b] = lo;
-    }
-    sidx = sidx_s;
+  for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+    const long long key = P.k_min + ((long long)b << tb);
+    int lo = 0, hi = ng;
+    while (lo < hi) { const int m = (lo + hi) >> 1; if ((long long)__ldg(sidx + m) < key) lo = m + 1; else hi = m; }
+    tab[b] = lo;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -166,15 +159,11 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
       if (wv.y < wv.x) state = 1;
       else if (x == 0.0 && y == 0.0) state = 2;
       else {
-        int lo = 0, hi = ng, lo2, hi2 = ng;   // first good index >= l, first good index > r
-        if (staged) {
-          const int bl = (int)((wv.x - P.k_min) >> tb), br_ = (int)((wv.y - P.k_min) >> tb);
-          lo = tab[bl]; hi = tab[bl + 1];
-          hi2 = tab[br_ + 1];
-        }
-        while (lo < hi) { const int m = (lo + hi) >> 1; if (sidx[m] < wv.x) lo = m + 1; else hi = m; }
-        lo2 = staged ? max(lo, tab[(int)((wv.y - P.k_min) >> tb)]) : lo;
-        while (lo2 < hi2) { const int m = (lo2 + hi2) >> 1; if (sidx[m] <= wv.y) lo2 = m + 1; else hi2 = m; }
+        const int bl = (int)((wv.x - P.k_min) >> tb), br_ = (int)((wv.y - P.k_min) >> tb);
+        int lo = tab[bl], hi = tab[bl + 1];           // first good index >= l
+        while (lo < hi) { const int m = (lo + hi) >> 1; if (__ldg(sidx + m) < wv.x) lo = m + 1; else hi = m; }
+        int lo2 = max(lo, tab[br_]), hi2 = tab[br_ + 1];   // first good index > r
+        while (lo2 < hi2) { const int m = (lo2 + hi2) >> 1; if (__ldg(sidx + m) <= wv.y) lo2 = m + 1; else hi2 = m; }
         first = lo; K = lo2 - lo;
         if (K > 0) PL[lane] = polar_of<CPLX>(x, y);
       }
@@ -197,7 +186,7 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
         int a = 0, b = 31;
         while (a < b) { const int m = (a + b + 1) >> 1; if (OF[m] <= g) a = m; else b = m - 1; }
         const int j = FI[a] + (g - OF[a]);
-        T[f] = sparse_term<CK, CPLX>(P, PL[a], j, sidx[j]);
+        T[f] = sparse_term<CK, CPLX>(P, PL[a], j, __ldg(sidx + j));
       }
       __syncwarp();
       // this lane's terms inside the round, in increasing k (the flat order)
@@ -420,8 +409,7 @@ static void launch_eval_sparse_t(const void* pts, long long n, const PolyDev& P,
   constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
   constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
   const size_t smem = sizeof(SpTerm) * kSpWarps * kSpRound + sizeof(polar_t) * kSpWarps * 32 +
-                      sizeof(int) * (kSpWarps * 65 + kSpTab + 1) +
-                      (P.n_good <= kSparseSmemIdx ? (size_t)P.n_good * sizeof(int32_t) : 0);
+                      sizeof(int) * (kSpWarps * 65 + kSpTab + 1);
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -430,7 +418,7 @@ static void launch_eval_sparse_t(const void* pts, long long n, const PolyDev& P,
     attr_set[dev] = true;
   }
   const long long warps = (n + 31) / 32;
-  const long long blocks = std::min<long long>((warps + kSpWarps - 1) / kSpWarps, 148ll * 8);
+  const long long blocks = std::min<long long>((warps + kSpWarps - 1) / kSpWarps, 148ll * 16);
   k_eval_sparse_coop<PK, CK, OK><<<(int)std::max(1ll, blocks), kSpWarps * 32, smem, s>>>(pts, n, P, lr, vals, exps);
 }
 

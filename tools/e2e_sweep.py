@@ -1,5 +1,6 @@
 """e2e (fpe_evaluate_host, pinned host buffers) time of cfg3 for several pipeline settings, each in its own
-process (the library reads FPE_HOST_* once):  python tools/e2e_sweep.py 22:18:6 22:21:6 ..."""
+process (the library reads FPE_HOST_* once):  python tools/e2e_sweep.py 22:18:6 22:21:6:1 ...
+(chunk log2 : first-chunk log2 : slots [: split D2H])"""
 import os
 import subprocess
 import sys
@@ -22,7 +23,7 @@ print(" ".join(f"{t:.2f}" for t in ts))
 '''
 
 for s in sys.argv[1:]:
-    c, f, k = s.split(":")
-    env = dict(os.environ, FPE_HOST_CHUNK_LOG2=c, FPE_HOST_FIRST_LOG2=f, FPE_HOST_SLOTS=k)
+    c, f, k, sp = (s.split(":") + ["0"])[:4]
+    env = dict(os.environ, FPE_HOST_CHUNK_LOG2=c, FPE_HOST_FIRST_LOG2=f, FPE_HOST_SLOTS=k, FPE_HOST_SPLIT_D2H=sp)
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
     print(s, r.stdout.strip() or r.stderr[-500:], flush=True)
