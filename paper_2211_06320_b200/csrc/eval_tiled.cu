@@ -323,14 +323,26 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
 #ifdef FPE_EXP_NO_MASK
     k = min(k, F_hi);
 #endif
-    for (const int m1 = max(k0, F_hi + 1); k >= m1; --k) {
-      const CT a = cb[k];
+    // masked steps (ragged window ends): 8 coefficients loaded ahead as in the unmasked loop, so that a
+    // warp running alone (the tail of a batch) is not bound by one shared-memory latency per coefficient
+    auto masked_step = [&](const CT a, int kk) {
 #pragma unroll
       for (int j = 0; j < NP; ++j) {
         W nr = br[j], ni = bi[j];
         horner_step<CK, CPLX>(nr, ni, zr[j], zi[j], a);
-        if (k >= wl[j] && k <= wr[j]) { br[j] = nr; bi[j] = ni; }
+        if (kk >= wl[j] && kk <= wr[j]) { br[j] = nr; bi[j] = ni; }
       }
+    };
+    {
+      const int m1 = max(k0, F_hi + 1);
+      for (; k - 7 >= m1; k -= 8) {
+        CT a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = cb[k - u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) masked_step(a[u], k - u);
+      }
+      for (; k >= m1; --k) masked_step(cb[k], k);
     }
     const int f0 = max(k0, F_lo);
 #ifdef FPE_EXP_NO_HOT
@@ -400,15 +412,14 @@ __device__ __forceinline__ void stream_range(Ring<CK>& R, int lo, int hi, const 
 #ifdef FPE_EXP_NO_MASK
     k = k0 - 1;
 #endif
-    for (; k >= k0; --k) {
-      const CT a = cb[k];
+    for (; k - 7 >= k0; k -= 8) {
+      CT a[8];
 #pragma unroll
-      for (int j = 0; j < NP; ++j) {
-        W nr = br[j], ni = bi[j];
-        horner_step<CK, CPLX>(nr, ni, zr[j], zi[j], a);
-        if (k >= wl[j] && k <= wr[j]) { br[j] = nr; bi[j] = ni; }
-      }
+      for (int u = 0; u < 8; ++u) a[u] = cb[k - u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) masked_step(a[u], k - u);
     }
+    for (; k >= k0; --k) masked_step(cb[k], k);
     ring_release(R);
   }
 }
@@ -421,6 +432,8 @@ struct Acc {
   double r, i;
   int base;        // relative index of the lowest coefficient folded in so far
   bool started;
+  bool have_zk;    // zk = z^kPiece computed (once per point: a long window folds up to ~256 pieces)
+  xc_t zk;
 };
 
 // (re, im) * (h + e) 2^E, scaled into range (the product is bounded by the cover argument).
@@ -447,8 +460,12 @@ template <bool CPLX>
 __device__ __noinline__ void acc_fold(Acc& A, double hr, double hi, int pbase, double x, double y) {
   if (!A.started) { A.r = hr; A.i = hi; A.base = pbase; A.started = true; return; }
   const int gap = A.base - pbase;
-  const xc_t m = (gap == kPiece) ? power_piece<CPLX>(x, y) : power_polar<CPLX>(x, y, gap);
-  mul_ext(A.r, A.i, m);
+  if (gap == kPiece) {
+    if (!A.have_zk) { A.zk = power_piece<CPLX>(x, y); A.have_zk = true; }
+    mul_ext(A.r, A.i, A.zk);
+  } else {
+    mul_ext(A.r, A.i, power_polar<CPLX>(x, y, gap));
+  }
   A.r += hr; A.i += hi;
   A.base = pbase;
 }
@@ -701,7 +718,7 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c,
 // One warp evaluates piece p of a multi-piece group into its scratch slot; the warp that completes
 // the group's last piece folds all partials in order and finalises.
 template <int PK, int CK, int OK, int NP>
-__device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long long n, const Plan& plan,
+__device__ __forceinline__ bool multi_piece(Ring<CK>& R, uint32_t g, int p, long long n, const Plan& plan,
                                             const PtRec* rec, const PolyDev& P, PtOut* out) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   using W = typename Step<CK>::W;
@@ -727,7 +744,7 @@ __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long
   uint32_t done = 0;
   if (lane == 0) done = atomicAdd(plan.gcnt + g, 1u);
   done = __shfl_sync(0xffffffffu, done, 0);
-  if (done != (uint32_t)d.npieces - 1) return;
+  if (done != (uint32_t)d.npieces - 1) return false;
   __threadfence();
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
@@ -743,6 +760,7 @@ __device__ __forceinline__ void multi_piece(Ring<CK>& R, uint32_t g, int p, long
     }
     stage_acc(out, S.idx[j], A, 0, (int)P.k_min);
   }
+  return true;
 }
 
 template <int CK>
@@ -752,6 +770,29 @@ constexpr size_t ring_bytes() {
 
 // Persistent evaluator: every warp first takes parallel pieces of long windows, then whole groups,
 // both from global atomic counters (largest work first; the tail is at most one group).
+#ifdef FPE_ITEM_TRACE
+// Debugging (build with -DFPE_ITEM_TRACE): per work item of k_eval_tiled, {start ns, end ns, info} with
+// info = kind (1 multi piece, 2 group) << 60 | group << 20 | union length / 16 (or the piece index).
+__device__ unsigned long long fpe_item_trace[1 << 20][3];
+__device__ unsigned int fpe_item_trace_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_item(unsigned long long t0, unsigned long long info) {
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned int i = atomicAdd(&fpe_item_trace_n, 1u);
+    if (i < (1u << 20)) { fpe_item_trace[i][0] = t0; fpe_item_trace[i][1] = gtimer(); fpe_item_trace[i][2] = info; }
+  }
+}
+#define FPE_TRACE_T0 const unsigned long long trace_t0 = gtimer()
+#define FPE_TRACE(info) trace_item(trace_t0, (info))
+#else
+#define FPE_TRACE_T0
+#define FPE_TRACE(info)
+#endif
+
 template <int PK, int CK, int OK, int NP>
 #ifndef FPE_EVAL_MIN_CTAS
 #define FPE_EVAL_MIN_CTAS 3   // CTAs per SM the register budget is sized for (12 warps)
@@ -780,7 +821,10 @@ __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(l
     if (lane == 0) nxt = atomicAdd(plan.ctrs + 0, 1u);
     const uint2 item = plan.items[it];
     if (item.x == ~0u) continue;
-    multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, rec, P, out);
+    FPE_TRACE_T0;
+    const bool folded = multi_piece<PK, CK, OK, NP>(R, item.x, (int)item.y, n, plan, rec, P, out);
+    FPE_TRACE((1ull << 60) | ((unsigned long long)folded << 59) | ((unsigned long long)item.x << 20) | item.y);
+    (void)folded;
   }
   // groups: software-pipelined one group ahead (the next group's records load during this epilogue)
   const int kmin = (int)P.k_min;
@@ -799,7 +843,12 @@ __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(l
     };
     if (cur.d.npieces > 1 || (cur.d.mma_np > 0 && cur.d.mma_slot == kMmaInWarp))
       fetch_next();   // evaluated as parallel pieces (multi_piece), or by k_eval_overflow
-    else single_group<PK, CK, OK, NP>(R, cur, n, P, plan, out, fetch_next);
+    else {
+      FPE_TRACE_T0;
+      single_group<PK, CK, OK, NP>(R, cur, n, P, plan, out, fetch_next);
+      FPE_TRACE((2ull << 60) | ((unsigned long long)cur.g << 20) |
+                (unsigned long long)(cur.d.hi >= cur.d.lo ? (cur.d.hi - cur.d.lo + 1) / 16 : 0));
+    }
     cur = nx;
   }
 }
@@ -847,7 +896,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_eval_overflow(long long n, Poly
 // [1/2, 1), so m w never overflows; a coefficient larger than b by more than 2^60 moves b to the
 // coefficient's scale first (b may then underflow: it is below the coefficient's rounding).  All in fp64
 // (fp32 handles too: more accurate than their 2^-16 tolerance needs).
-struct XAcc { double r, i; long long E; int base; bool started; };
+struct XAcc { double r, i; long long E; int base; bool started; bool have_zk; xc_t zk; };
 
 __device__ __forceinline__ void xnorm(double& r, double& i, long long& E) {
   const double m = fmax(fabs(r), fabs(i));
@@ -895,7 +944,8 @@ template <bool CPLX>
 __device__ __noinline__ void xacc_fold(XAcc& A, double hr, double hi, long long hE, int pbase, double x, double y) {
   if (!A.started) { A.r = hr; A.i = hi; A.E = hE; A.base = pbase; A.started = true; return; }
   const int gap = A.base - pbase;
-  const xc_t m = (gap == kPiece) ? power_piece<CPLX>(x, y) : power_polar<CPLX>(x, y, gap);
+  if (gap == kPiece && !A.have_zk) { A.zk = power_piece<CPLX>(x, y); A.have_zk = true; }
+  const xc_t m = (gap == kPiece) ? A.zk : power_polar<CPLX>(x, y, gap);
   double r = __fma_rn(A.r, m.hr, __fma_rn(-A.i, m.hi, __fma_rn(A.r, m.er, -A.i * m.ei)));
   double i = __fma_rn(A.r, m.hi, __fma_rn(A.i, m.hr, __fma_rn(A.r, m.ei, A.i * m.er)));
   long long E = A.E + m.E;
@@ -1323,3 +1373,16 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
 }
 
 }  // namespace fpe
+
+#ifdef FPE_ITEM_TRACE
+extern "C" int fpe_debug_item_trace(unsigned long long* host, int cap, int reset) {
+  unsigned int n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, fpe::fpe_item_trace_n, sizeof(n));
+  n = n < (1u << 20) ? n : (1u << 20);
+  const int m = (int)(n < (unsigned)cap ? n : (unsigned)cap);
+  if (host && m) cudaMemcpyFromSymbol(host, fpe::fpe_item_trace, (size_t)m * 24);
+  if (reset) { unsigned int z = 0; cudaMemcpyToSymbol(fpe::fpe_item_trace_n, &z, sizeof(z)); }
+  return m;
+}
+#endif
