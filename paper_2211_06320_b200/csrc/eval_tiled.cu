@@ -1145,12 +1145,18 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
 // Results from bucket order to the caller's order: a coalesced pass over the caller's indices gathering one
 // 32-byte staged result each (a random sector read instead of the evaluator's random partial-sector
 // writes, which the DRAM turns into read-modify-writes).
+#ifndef FPE_UNSORT_U
+#define FPE_UNSORT_U 4      // independent gathers in flight per thread
+#endif
+#ifndef FPE_UNSORT_MINB
+#define FPE_UNSORT_MINB 1   // CTAs per SM the register budget is sized for
+#endif
 template <int PK, int OK>
-__global__ void __launch_bounds__(256) k_unsort(const PtOut* __restrict__ staged, const uint32_t* __restrict__ spos,
+__global__ void __launch_bounds__(256, FPE_UNSORT_MINB) k_unsort(const PtOut* __restrict__ staged, const uint32_t* __restrict__ spos,
                                                 long long n, const void* __restrict__ pts, PolyDev P,
                                                 void* __restrict__ vals, long long* __restrict__ exps) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
-  constexpr int U = 4;   // independent gathers in flight per thread
+  constexpr int U = FPE_UNSORT_U;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
     double re[U], im[U], x[U], y[U];
