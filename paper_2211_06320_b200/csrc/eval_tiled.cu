@@ -1146,10 +1146,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
 // 32-byte staged result each (a random sector read instead of the evaluator's random partial-sector
 // writes, which the DRAM turns into read-modify-writes).
 #ifndef FPE_UNSORT_U
-#define FPE_UNSORT_U 4      // independent gathers in flight per thread
+#define FPE_UNSORT_U 2      // independent gathers in flight per thread
 #endif
 #ifndef FPE_UNSORT_MINB
-#define FPE_UNSORT_MINB 1   // CTAs per SM the register budget is sized for
+#define FPE_UNSORT_MINB 3   // CTAs per SM the register budget is sized for (2 x 3: 2.27 -> 2.02 ms at cfg3)
 #endif
 template <int PK, int OK>
 __global__ void __launch_bounds__(256, FPE_UNSORT_MINB) k_unsort(const PtOut* __restrict__ staged, const uint32_t* __restrict__ spos,
