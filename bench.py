@@ -324,22 +324,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def profiled_traffic(prefixes=("void k_eval_tiled", "k_eval_mma", "void k_eval_mma")):
-    """DRAM bytes (read + write) per step of the window evaluator (k_eval_mma + k_eval_tiled), from the
-    committed ncu --set full summary (profiles/r01_ncu_eval_tiled_cfg3.json, captured on the same
-    workload); None if absent."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_eval_tiled_cfg3.json")
-    try:
-        with open(path) as f:
-            tot, seen = 0.0, False
-            for k in json.load(f):
-                if k.get("kernel", "").startswith(prefixes):
-                    tot += 1e9 * (k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"])
-                    seen = True
-            if seen:
-                return {"bytes": tot, "source": os.path.relpath(path, ROOT)}
-    except (OSError, ValueError, KeyError):
-        pass
+def profiled_traffic(prefixes=("void k_eval_tiled", "k_eval_mma", "void k_eval_mma", "void k_eval_overflow")):
+    """DRAM bytes (read + write) per step of the window evaluator (k_eval_mma + k_eval_tiled [+ the overflow
+    kernel]) from the committed ncu --set full summary of the same cfg3 workload (round 2:
+    profiles/r02_ncu_cfg3_all_kernels.json, in bytes; round 1's file was in GB); None if absent."""
+    for name, scale in (("r02_ncu_cfg3_all_kernels.json", 1.0), ("r01_ncu_eval_tiled_cfg3.json", 1e9)):
+        path = os.path.join(ROOT, "profiles", name)
+        try:
+            with open(path) as f:
+                tot, seen = 0.0, False
+                for k in json.load(f):
+                    if k.get("kernel", "").startswith(prefixes):
+                        tot += scale * (k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"])
+                        seen = True
+                if seen:
+                    return {"bytes": tot, "source": os.path.relpath(path, ROOT)}
+        except (OSError, ValueError, KeyError):
+            continue
     return None
 
 
@@ -482,11 +483,11 @@ def run_fpe(args):
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak,
                      "traffic": (profiled_traffic() or {}).get("bytes") if (cfg == 3 and not fp32) else None,
-                     "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of k_eval_mma + k_eval_tiled "
-                                     "(profiles/r01_ncu_eval_tiled_cfg3.json): it reads the 32-B bucket-order records "
-                                     f"and writes its 32-B results over them ({64 * n / 1e9:.2f} GB); the path's "
-                                     f"algorithmic bytes are 40 B/pt = {40 * n / 1e9:.2f} GB (points in, values and "
-                                     "exponents out, the latter written by k_unsort)",
+                     "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of the evaluator kernels "
+                                     f"({(profiled_traffic() or {}).get('source')}): they read the 32-B bucket-order "
+                                     f"records and write 32-B accumulators over them ({64 * n / 1e9:.2f} GB); the "
+                                     f"path's algorithmic bytes are 40 B/pt = {40 * n / 1e9:.2f} GB (points in, values "
+                                     "and exponents out, the latter written by k_unsort)",
                      "peak_note": ("fp32 FMA: 148 SM x 128 lanes x 1.965 GHz x 2; " if fp32 else "") +
                                   "fp64 FMA: 148 SM x 64 lanes x 1.965 GHz x 2 (guide unit counts/clock); the FP64 "
                                   "tensor cores (DMMA, k_eval_mma) run on the same datapath: 18.5T FMA/s measured "
