@@ -18,10 +18,10 @@ namespace fpe {
 // out near 72% of the pipe.  mma.sync DMMA runs the same datapath from its fragments at 99.7%
 // (profiles/r01_dmma_vs_dfma.json).  Over whole 256-coefficient chunks the Horner sum is a dense
 // contraction once split by phase k mod 16:
-//   sum_{k in piece} a_k z^{k-k0} = sum_{m<16} z^m R_m,  R_m = sum_t a_{k0+16t+m} u^t,  u = z^16,
-// and each chunk q is C <- C (.) w + A V with A[m][i] = a_{256q+16i+m} (16 x 16, straight from the staged
-// chunk), V[i][p] = u_p^i, w_p = u_p^16 = z_p^256 and C[m][p] = R_m at point p: 4 real m16n8k4 DMMAs per
-// 4 powers and 8 points for the complex product.  One CTA (8 warps x 16 points = a group) per item
+//   sum_{k in piece} a_k z^{k-k0} = sum_{m<16} z^m R_m,  R_m = sum_{q,i} a_{k0+256q+16i+m} u^i w^q,
+// u = z^16, w = z^256, and each chunk q (in increasing order) is C += A_q V_q with A_q[m][i] = a_{256q+16i+m}
+// (16 x 16, straight from the staged chunk), V_q[i][p] = u_p^i w_p^q and C[m][p] = R_m at point p
+// (mma_piece.cuh): 4 real m16n8k4 DMMAs per 4 powers and 8 points for the complex product.  One CTA (8 warps x 16 points = a group) per item
 // (group, piece), the piece's 64 chunks staged once per CTA by TMA into a 4-stage ring shared by the
 // warps.  A point's column is active iff mma_covers (its window covers the whole piece), so every value
 // is relative to the piece start, which lies in the point's window; u, u^4, w are
@@ -70,9 +70,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, FPE_MMA_MINB) k_eval_mma(long 
     if (item.x == ~0u) continue;
     const uint32_t grp = item.x;
     const int p = (int)item.y;
-    const int q0 = p * kPieceChunks + kPieceChunks - 1;   // chunks descend from q0
+    const int q0 = p * kPieceChunks;   // chunks ascend from q0 (mma_piece.cuh)
     if (tid == 0)
-      for (int i = 0; i < kMmaStages; ++i) issue(q0 - i);
+      for (int i = 0; i < kMmaStages; ++i) issue(q0 + i);
     __syncwarp();
     // this warp's 16 points: lanes [0, 16) own point 16 w + lane (lanes 16..31 mirror them)
     const int q = 16 * w + (lane & 15);
@@ -92,11 +92,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, FPE_MMA_MINB) k_eval_mma(long 
     for (int k = 0; k < kPieceChunks; ++k) {
       const int s = (int)(t_seq % kMmaStages);
       mbar_wait(full + s, (t_seq / kMmaStages) & 1u);
-      if (busy) mma_chunk(F, ring[s], k == 0);
+      if (busy) mma_chunk(F, ring[s]);
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
       ++t_seq;
-      if (tid == 0 && k + kMmaStages < kPieceChunks) issue(q0 - k - kMmaStages);
+      if (tid == 0 && k + kMmaStages < kPieceChunks) issue(q0 + k + kMmaStages);
       __syncwarp();
     }
     double orr, oi;

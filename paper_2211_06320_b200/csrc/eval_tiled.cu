@@ -225,7 +225,8 @@ template <int CK> struct Ring {
   const CT* coef;     // padded dense coefficient array (relative to k_min)
   uint32_t g;         // chunks consumed (warp-uniform)
   uint32_t gi;        // chunks issued (warp-uniform)
-  int q_next, q_end;  // next chunk to issue (descending) and the last chunk of the current range
+  int q_next, q_end;  // next chunk to issue and the last chunk of the current range
+  int dir;            // -1: chunks in decreasing order (Horner), +1: increasing (mma_piece.cuh)
 };
 
 template <int CK>
@@ -236,11 +237,11 @@ __device__ __forceinline__ void ring_issue_n(Ring<CK>& R, int n) {
       const int s = (int)((R.gi + i) % kStages);
       fence_proxy_async();
       mbar_expect_tx(R.bar + s, kChunk * sizeof(CT));
-      tma_load_1d(R.buf + s * kChunk, R.coef + (size_t)(R.q_next - i) * kChunk, kChunk * sizeof(CT), R.bar + s);
+      tma_load_1d(R.buf + s * kChunk, R.coef + (size_t)(R.q_next + R.dir * i) * kChunk, kChunk * sizeof(CT), R.bar + s);
     }
   }
   R.gi += n;
-  R.q_next -= n;
+  R.q_next += R.dir * n;
 }
 // Start streaming the chunks that cover [lo, hi] (relative indices, lo <= hi), highest chunk first.
 template <int CK>
@@ -250,7 +251,16 @@ __device__ __forceinline__ void ring_begin(Ring<CK>& R, int lo, int hi) {
 #endif
   R.q_next = hi / kChunk;
   R.q_end = lo / kChunk;
+  R.dir = -1;
   ring_issue_n(R, min(kStages - (int)(R.gi - R.g), R.q_next - R.q_end + 1));
+}
+// The same in increasing chunk order (the tensor-core pieces).
+template <int CK>
+__device__ __forceinline__ void ring_begin_up(Ring<CK>& R, int lo, int hi) {
+  R.q_next = lo / kChunk;
+  R.q_end = hi / kChunk;
+  R.dir = 1;
+  ring_issue_n(R, min(kStages - (int)(R.gi - R.g), R.q_end - R.q_next + 1));
 }
 template <int CK>
 __device__ __forceinline__ const typename Step<CK>::CT* ring_wait(Ring<CK>& R) {
@@ -262,7 +272,7 @@ template <int CK>
 __device__ __forceinline__ void ring_release(Ring<CK>& R) {
   __syncwarp();
   ++R.g;
-  if (R.q_next >= R.q_end) ring_issue_n(R, 1);
+  if (R.dir < 0 ? R.q_next >= R.q_end : R.q_next <= R.q_end) ring_issue_n(R, 1);
 }
 
 // The in-warp tensor-core pass of piece p for 16 points (x, y, act: the point of lane & 15, as in
@@ -276,9 +286,9 @@ struct MmaPassOut {
 __device__ __noinline__ MmaPassOut mma_pass_inwarp(Ring<FPE_C64> R, double x, double y, int act, int p) {
   MmaFrag F;
   mma_setup(F, x, y, act);
-  ring_begin(R, p * kPiece, p * kPiece + kPiece - 1);
+  ring_begin_up(R, p * kPiece, p * kPiece + kPiece - 1);
   for (int k = 0; k < kMmaPieceChunks; ++k) {
-    mma_chunk(F, ring_wait(R), k == 0);
+    mma_chunk(F, ring_wait(R));
     ring_release(R);
   }
   MmaPassOut o;
@@ -809,7 +819,7 @@ __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(l
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0};
+  Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0, -1};
   PtOut* const out = reinterpret_cast<PtOut*>(rec);   // results overwrite the records (bucket order)
   const uint32_t n_multi = min(plan.ctrs[2], plan.cap);
   // the next item index is fetched one item ahead, so the atomic's latency hides behind the work
@@ -871,7 +881,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_eval_overflow(long long n, Poly
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0};
+  Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0, -1};
   PtOut* const out = reinterpret_cast<PtOut*>(rec);
   const int kmin = (int)P.k_min;
   for (;;) {
@@ -1098,7 +1108,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0};
+  Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0, -1};
   const int hi = (int)(P.k_max - P.k_min);
   const long long ngroups = (n + 32 * NP - 1) / (32 * NP);
   for (;;) {

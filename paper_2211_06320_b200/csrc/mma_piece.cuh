@@ -6,8 +6,12 @@
 // pure function of (z, handle), whatever the batch (fpe.h).
 //
 // Phase split: over whole 256-coefficient chunks the piece sum is
-//   sum_{k in piece} a_k z^{k-k0} = sum_{m<16} z^m R_m,  R_m = sum_t a_{k0+16t+m} u^t,  u = z^16,
-// and chunk q is C <- C (.) w + A V with A[m][i] = a_{256q+16i+m}, V[i][p] = u_p^i, w_p = z_p^256.
+//   sum_{k in piece} a_k z^{k-k0} = sum_{m<16} z^m R_m,  R_m = sum_q sum_i a_{k0+256q+16i+m} u^i w^q,
+// u = z^16, w = z^256.  The chunks are fed in increasing q and each is one accumulation C += A_q V_q with
+// A_q[m][i] = a_{k0+256q+16i+m} (straight from the staged chunk) and V_q[i][p] = u_p^i w_p^q, the B
+// fragment advanced by V_{q+1} = V_q (.) w after the chunk's DMMAs are issued -- so the per-chunk power
+// update does not wait on the accumulators (a Horner over chunks, C <- C (.) w + A V, would put a complex
+// multiply of every accumulator between consecutive chunks' DMMAs).
 // Lane layout (m16n8k4 fragments): lanes 0..15 own the warp's 16 points (lanes 16..31 mirror them);
 // thread (g = lane >> 2, c = lane & 3) holds B rows c of the two 8-point column tiles t and C columns 2c, 2c+1.
 #pragma once
@@ -41,8 +45,8 @@ __device__ __forceinline__ void mma_dd_sqr_c(xc_t& v) {
 
 // Fragments of one warp's 16 points for one piece.
 struct MmaFrag {
-  double vr[2][4], vi[2][4];     // B: u^(4 ks + c) of the column tiles (0 for inactive columns)
-  double cwr[2][2], cwi[2][2];   // w = z^256 of the C columns 2c, 2c + 1
+  double vr[2][4], vi[2][4];     // B: u^(4 ks + c) w^q of the column tiles (0 for inactive columns)
+  double cwr[2], cwi[2];         // w = z^256 of the B columns g, 8 + g
   double cr[2][4], ci[2][4];     // C: Re / Im of R_m (rows g, g + 8; columns 2c, 2c + 1)
 };
 
@@ -77,27 +81,17 @@ __device__ __forceinline__ void mma_setup(MmaFrag& F, double x, double y, int ac
       F.vr[t][ks] = on ? pr : 0.0;
       F.vi[t][ks] = on ? pi : 0.0;
     }
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {                // w of the C columns 2c, 2c + 1
-      const int s2 = 8 * t + 2 * c + e;
-      F.cwr[t][e] = __shfl_sync(0xffffffffu, wwr, s2);
-      F.cwi[t][e] = __shfl_sync(0xffffffffu, wwi, s2);
-    }
+    F.cwr[t] = __shfl_sync(0xffffffffu, wwr, src);   // w of the B column g of tile t
+    F.cwi[t] = __shfl_sync(0xffffffffu, wwi, src);
 #pragma unroll
     for (int e = 0; e < 4; ++e) { F.cr[t][e] = 0.0; F.ci[t][e] = 0.0; }
   }
 }
 
-// One 256-coefficient chunk (cb: its first coefficient; chunks are fed highest first, `first` for the
-// piece's top chunk): C <- C (.) w + A V.
-__device__ __forceinline__ void mma_chunk(MmaFrag& F, const double2* cb, bool first) {
+// One 256-coefficient chunk (cb: its first coefficient; chunks are fed in increasing q): C += A_q V_q, then
+// V <- V (.) w for the next chunk.
+__device__ __forceinline__ void mma_chunk(MmaFrag& F, const double2* cb) {
   const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
-  if (!first) {
-#pragma unroll
-    for (int t = 0; t < 2; ++t)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) mma_cmul(F.cr[t][e], F.ci[t][e], F.cr[t][e], F.ci[t][e], F.cwr[t][e & 1], F.cwi[t][e & 1]);
-  }
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
     const double2 a0 = cb[64 * ks + 16 * c + g], a1 = cb[64 * ks + 16 * c + g + 8];   // A[g|g+8][4ks + c]
@@ -109,6 +103,10 @@ __device__ __forceinline__ void mma_chunk(MmaFrag& F, const double2* cb, bool fi
       mma_dmma(F.ci[t], a0.y, a1.y, F.vr[t][ks]);
     }
   }
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) mma_cmul(F.vr[t][ks], F.vi[t][ks], F.vr[t][ks], F.vi[t][ks], F.cwr[t], F.cwi[t]);
 }
 
 // sum_m z^m R_m for the warp's 16 points: rows g and g + 8 in the thread, then a tree over g (lane bits
