@@ -55,7 +55,7 @@ constexpr long long kMaxBatch = 1ll << 28;
 // workspace = kWsHeader bytes of counters (kStat*) + the path's scratch
 static size_t ws_bytes_for(long long n) {
   long long b = n < kMaxBatch ? n : kMaxBatch;
-  size_t naive = ((size_t)b * sizeof(int2) + 255) & ~size_t(255);
+  size_t naive = (((size_t)b * sizeof(int2) + 255) & ~size_t(255)) + (kSparseTab + 1) * sizeof(int);   // lr + table
   size_t tiled = tiled_ws_bytes(b);
   return kWsHeader + (naive > tiled ? naive : tiled);
 }
@@ -543,9 +543,10 @@ static fpe_status evaluate_impl(fpe_poly h, const void* points, fpe_dtype pt_dt,
       int2* lr = static_cast<int2*>(scratch);
       launch_classify(pt_dt, pp, m, P, lr, dd, stats + kStatHard, s);
       stg.mark("classify");
-      launch_eval_sparse(pt_dt, pp, m, P, lr, vv, ee, s);
+      int* tab = reinterpret_cast<int*>(static_cast<char*>(scratch) + (((size_t)m * sizeof(int2) + 255) & ~size_t(255)));
+      launch_eval_sparse(pt_dt, pp, m, P, lr, tab, vv, ee, s);
       stg.mark("eval_sparse");
-      launches += 2;
+      launches += 3;   // classify, good-index table, evaluation
       if (dd) { launch_confidence(out_kind, m, P, vv, ee, dd, s); launches += 1; }
     }
   }

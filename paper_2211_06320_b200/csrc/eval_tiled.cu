@@ -1248,19 +1248,21 @@ static int launch_eval_overflow_t(long long n, const PolyDev& P, PtRec* rec, con
   return 1;
 }
 
-// points per lane: complex steps (4 FMAs per coefficient) share a coefficient load between 2 points,
-// real steps (1 FMA) between 4 (shared-memory wavefronts per FMA); 4 complex points per
-// lane measured slower (register spills in the epilogue)
+// points per lane (groups of 32 NP points): 4 -- each coefficient load feeds 16 fp64 FMAs (complex) or 4
+// (real) per lane; the single-precision evaluator as a build knob (packed FFMA2 pairs)
+#ifndef FPE_NP_F32
+#define FPE_NP_F32 4
+#endif
 template <int PK, int CK>
 struct NPFor {
   static constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
-  static constexpr int value = 4;
+  static constexpr int value = PtTraits<CK>::f32 ? FPE_NP_F32 : 4;
   static constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
 };
 
 static int np_for(int pk, int cdt) {
-  const bool cplx = (pk == FPE_C64 || pk == FPE_C32 || cdt == FPE_C64 || cdt == FPE_C32);
-  return 4;
+  (void)pk;
+  return (cdt == FPE_R32 || cdt == FPE_C32) ? FPE_NP_F32 : 4;
 }
 
 template <int PK>

@@ -95,7 +95,7 @@ __device__ __forceinline__ void xadd(double& sr, double& si, long long& se, doub
 // same whatever points share its warp.
 constexpr int kSpWarps = 8;
 constexpr int kSpRound = 64;    // terms per warp and round in shared memory
-constexpr int kSpTab = 4096;    // buckets of the good-index table
+constexpr int kSpTab = kSparseTab;
 struct SpTerm { double r, i; long long e; };
 
 template <int CK, bool CPLX>
@@ -117,9 +117,27 @@ __device__ __forceinline__ SpTerm sparse_term(const PolyDev& P, const polar_t& p
   return t;
 }
 
+// A bucket table over [k_min, k_max] (buckets of 2^tb indices): the first good index >= k lies in
+// [tab[b], tab[b + 1]] for b = (k - k_min) >> tb, so each window bound costs a search over ~n_good / kSpTab
+// entries instead of log2(n_good) steps.  Built once per call (one CTA).
+__global__ void __launch_bounds__(1024) k_sparse_table(PolyDev P, int* __restrict__ tab) {
+  int tb = 0;
+  while (((P.k_max - P.k_min) >> tb) >= kSpTab) ++tb;
+  const int nb = (int)((P.k_max - P.k_min) >> tb) + 1;
+  const int ng = (int)P.n_good;
+  for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+    const long long key = P.k_min + ((long long)b << tb);
+    int lo = 0, hi = ng;
+    while (lo < hi) { const int m = (lo + hi) >> 1; if ((long long)__ldg(P.sidx + m) < key) lo = m + 1; else hi = m; }
+    tab[b] = lo;
+  }
+}
+
 template <int PK, int CK, int OK>
 __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* __restrict__ pts, long long n, PolyDev P,
-                                                                    const int2* __restrict__ lr, void* __restrict__ vals,
+                                                                    const int2* __restrict__ lr,
+                                                                    const int* __restrict__ tab,
+                                                                    void* __restrict__ vals,
                                                                     long long* __restrict__ exps) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   extern __shared__ __align__(16) unsigned char sp_smem[];
@@ -127,22 +145,9 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
   polar_t* pol = reinterpret_cast<polar_t*>(sp_smem + sizeof(SpTerm) * kSpWarps * kSpRound);      // [warps][32]
   int* offs = reinterpret_cast<int*>(pol + kSpWarps * 32);                                         // [warps][33]
   int* firsts = offs + kSpWarps * 33;                                                              // [warps][32]
-  int* tab = firsts + kSpWarps * 32;               // [kSpTab + 1] bucket -> first good index position
   const int32_t* __restrict__ sidx = P.sidx;       // read through L1 (16 KiB at cfg4)
-  const int ng = (int)P.n_good;
-  // a bucket table over [k_min, k_max] (buckets of 2^tb indices): the first good index >= k lies in
-  // [tab[b], tab[b + 1]] for b = (k - k_min) >> tb, so each window bound costs a search over ~ng / kSpTab
-  // entries instead of log2(ng) steps
-  int tb = 0;
+  int tb = 0;                                      // the bucket table's shift (k_sparse_table)
   while (((P.k_max - P.k_min) >> tb) >= kSpTab) ++tb;
-  const int nb = (int)((P.k_max - P.k_min) >> tb) + 1;
-  for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
-    const long long key = P.k_min + ((long long)b << tb);
-    int lo = 0, hi = ng;
-    while (lo < hi) { const int m = (lo + hi) >> 1; if ((long long)__ldg(sidx + m) < key) lo = m + 1; else hi = m; }
-    tab[b] = lo;
-  }
-  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   SpTerm* T = terms + w * kSpRound;
   polar_t* PL = pol + w * 32;
@@ -160,9 +165,9 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
       else if (x == 0.0 && y == 0.0) state = 2;
       else {
         const int bl = (int)((wv.x - P.k_min) >> tb), br_ = (int)((wv.y - P.k_min) >> tb);
-        int lo = tab[bl], hi = tab[bl + 1];           // first good index >= l
+        int lo = __ldg(tab + bl), hi = __ldg(tab + bl + 1);           // first good index >= l
         while (lo < hi) { const int m = (lo + hi) >> 1; if (__ldg(sidx + m) < wv.x) lo = m + 1; else hi = m; }
-        int lo2 = max(lo, tab[br_]), hi2 = tab[br_ + 1];   // first good index > r
+        int lo2 = max(lo, __ldg(tab + br_)), hi2 = __ldg(tab + br_ + 1);   // first good index > r
         while (lo2 < hi2) { const int m = (lo2 + hi2) >> 1; if (__ldg(sidx + m) <= wv.y) lo2 = m + 1; else hi2 = m; }
         first = lo; K = lo2 - lo;
         if (K > 0) PL[lane] = polar_of<CPLX>(x, y);
@@ -404,12 +409,13 @@ static void launch_horner_t(const void* pts, long long n, const PolyDev& P, void
   }
 
 template <int PK, int CK>
-static void launch_eval_sparse_t(const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
+static void launch_eval_sparse_t(const void* pts, long long n, const PolyDev& P, const int2* lr, int* tab, void* vals,
                                  long long* exps, cudaStream_t s) {
   constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
   constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
   const size_t smem = sizeof(SpTerm) * kSpWarps * kSpRound + sizeof(polar_t) * kSpWarps * 32 +
-                      sizeof(int) * (kSpWarps * 65 + kSpTab + 1);
+                      sizeof(int) * (kSpWarps * 65);
+  k_sparse_table<<<1, 1024, 0, s>>>(P, tab);
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -419,12 +425,12 @@ static void launch_eval_sparse_t(const void* pts, long long n, const PolyDev& P,
   }
   const long long warps = (n + 31) / 32;
   const long long blocks = std::min<long long>((warps + kSpWarps - 1) / kSpWarps, 148ll * 16);
-  k_eval_sparse_coop<PK, CK, OK><<<(int)std::max(1ll, blocks), kSpWarps * 32, smem, s>>>(pts, n, P, lr, vals, exps);
+  k_eval_sparse_coop<PK, CK, OK><<<(int)std::max(1ll, blocks), kSpWarps * 32, smem, s>>>(pts, n, P, lr, tab, vals, exps);
 }
 
-bool launch_eval_sparse(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, void* vals,
+bool launch_eval_sparse(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, int* tab, void* vals,
                         long long* exps, cudaStream_t s) {
-  FPE_DISPATCH_PC(launch_eval_sparse_t, pts, n, P, lr, vals, exps, s)
+  FPE_DISPATCH_PC(launch_eval_sparse_t, pts, n, P, lr, tab, vals, exps, s)
   return true;
 }
 
