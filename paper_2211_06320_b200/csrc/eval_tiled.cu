@@ -83,13 +83,15 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long beg = (long long)blockIdx.x * ppc, end = min(n, beg + ppc);
+  double xn = 0.0, yn = 0.0;   // the next iteration's point, loaded one iteration ahead
+  if (beg + threadIdx.x < end) load_point<PK>(pts, beg + threadIdx.x, xn, yn);
   for (long long i0 = beg + threadIdx.x; i0 - lane < end; i0 += blockDim.x) {
     const long long i = i0;
     const bool ok = i < end;
     uint32_t key = 0xffffffffu;
+    const double x = xn, y = yn;
+    if (i0 + blockDim.x < end) load_point<PK>(pts, i0 + blockDim.x, xn, yn);
     if (ok) {
-      double x, y;
-      load_point<PK>(pts, i, x, y);
       int hard = 0;
       double lam = 0.0;
       int istar, l, r;

@@ -39,9 +39,12 @@ __global__ void __launch_bounds__(256) k_classify(const void* __restrict__ pts, 
     __syncthreads();
     hull = sh;
   }
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    double x, y;
-    load_point<PK>(pts, i, x, y);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  double xn = 0.0, yn = 0.0;   // the next iteration's point, loaded one iteration ahead
+  if (blockIdx.x * (long long)blockDim.x + threadIdx.x < n) load_point<PK>(pts, blockIdx.x * (long long)blockDim.x + threadIdx.x, xn, yn);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double x = xn, y = yn;
+    if (i + stride < n) load_point<PK>(pts, i + stride, xn, yn);
     int hard = 0;
     double lam = 0.0;
     int istar, l, r;
