@@ -1253,18 +1253,21 @@ static int launch_eval_overflow_t(long long n, const PolyDev& P, PtRec* rec, con
 // points per lane (groups of 32 NP points): 4 -- each coefficient load feeds 16 fp64 FMAs (complex) or 4
 // (real) per lane; the single-precision evaluator as a build knob (packed FFMA2 pairs)
 #ifndef FPE_NP_F32
-#define FPE_NP_F32 4
+#define FPE_NP_F32 2   // 2 vs 4: 22.07 vs 22.33 ms at cfg5-fp32
+#endif
+#ifndef FPE_NP_REAL
+#define FPE_NP_REAL 2   // real coefficients at real points (fp64): 64-point groups, 0.72 vs 1.22 ms at cfg2
 #endif
 template <int PK, int CK>
 struct NPFor {
   static constexpr bool cplx = PtTraits<PK>::cplx || PtTraits<CK>::cplx;
-  static constexpr int value = PtTraits<CK>::f32 ? FPE_NP_F32 : 4;
+  static constexpr int value = PtTraits<CK>::f32 ? FPE_NP_F32 : (cplx ? 4 : FPE_NP_REAL);
   static constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
 };
 
 static int np_for(int pk, int cdt) {
-  (void)pk;
-  return (cdt == FPE_R32 || cdt == FPE_C32) ? FPE_NP_F32 : 4;
+  if (cdt == FPE_R32 || cdt == FPE_C32) return FPE_NP_F32;
+  return (pk == FPE_R64 && cdt == FPE_R64) ? FPE_NP_REAL : 4;
 }
 
 template <int PK>
