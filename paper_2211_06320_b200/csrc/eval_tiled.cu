@@ -1265,9 +1265,13 @@ struct NPFor {
   static constexpr int OK = PtTraits<CK>::f32 ? (cplx ? FPE_C32 : FPE_R32) : (cplx ? FPE_C64 : FPE_R64);
 };
 
-static int np_for(int pk, int cdt) {
+// Points per lane of the launch: 2 (groups of 64: tighter window unions) except for complex fp64
+// coefficients whose windows can cover a whole tensor-core piece (d_eff + 1 >= kPiece), where the DMMA items
+// need groups of 128 (k_eval_mma: 8 warps x 16 points).
+static int np_for(int pk, int cdt, long long d_eff) {
   if (cdt == FPE_R32 || cdt == FPE_C32) return FPE_NP_F32;
-  return (pk == FPE_R64 && cdt == FPE_R64) ? FPE_NP_REAL : 4;
+  if (cdt == FPE_C64) return d_eff + 1 >= kPiece ? 4 : 2;
+  return (pk == FPE_R64) ? FPE_NP_REAL : 2;
 }
 
 template <int PK>
@@ -1330,7 +1334,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   plan.stats = stats;
   plan.ctrs = reinterpret_cast<uint32_t*>(p);
   plan.mma_ctrs = plan.ctrs + 4;
-  const int np = np_for(pk, P.cdt);
+  const int np = np_for(pk, P.cdt, P.k_max - P.k_min);
   plan.gsize = 32 * np;
   plan.mma_on = (P.cdt == FPE_C64 && plan.gsize == 128 && !FPE_NO_MMA_ITEMS && !P.wide) ? 1 : 0;
   plan.ngroups = (uint32_t)((n + plan.gsize - 1) / plan.gsize);
@@ -1356,18 +1360,18 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     lm = 1;
   }
   int le = 0;
-#define FPE_EV(PKV, CKV)                                                                                  \
+#define FPE_EV(PKV, CKV, NPV)                                                                             \
   le = P.wide ? launch_eval_wide_t<PKV, CKV, NPFor<PKV, CKV>::OK>(n, P, rec, s)                              \
-              : launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPFor<PKV, CKV>::value>(n, P, rec, plan, s)
+              : launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPV>(n, P, rec, plan, s)
   switch (pk * 4 + P.cdt) {
-    case FPE_R64 * 4 + FPE_R64: FPE_EV(FPE_R64, FPE_R64); break;
-    case FPE_R64 * 4 + FPE_C64: FPE_EV(FPE_R64, FPE_C64); break;
-    case FPE_C64 * 4 + FPE_R64: FPE_EV(FPE_C64, FPE_R64); break;
-    case FPE_C64 * 4 + FPE_C64: FPE_EV(FPE_C64, FPE_C64); break;
-    case FPE_R32 * 4 + FPE_R32: FPE_EV(FPE_R32, FPE_R32); break;
-    case FPE_R32 * 4 + FPE_C32: FPE_EV(FPE_R32, FPE_C32); break;
-    case FPE_C32 * 4 + FPE_R32: FPE_EV(FPE_C32, FPE_R32); break;
-    case FPE_C32 * 4 + FPE_C32: FPE_EV(FPE_C32, FPE_C32); break;
+    case FPE_R64 * 4 + FPE_R64: FPE_EV(FPE_R64, FPE_R64, FPE_NP_REAL); break;
+    case FPE_R64 * 4 + FPE_C64: if (np == 4) FPE_EV(FPE_R64, FPE_C64, 4); else FPE_EV(FPE_R64, FPE_C64, 2); break;
+    case FPE_C64 * 4 + FPE_R64: FPE_EV(FPE_C64, FPE_R64, 2); break;
+    case FPE_C64 * 4 + FPE_C64: if (np == 4) FPE_EV(FPE_C64, FPE_C64, 4); else FPE_EV(FPE_C64, FPE_C64, 2); break;
+    case FPE_R32 * 4 + FPE_R32: FPE_EV(FPE_R32, FPE_R32, FPE_NP_F32); break;
+    case FPE_R32 * 4 + FPE_C32: FPE_EV(FPE_R32, FPE_C32, FPE_NP_F32); break;
+    case FPE_C32 * 4 + FPE_R32: FPE_EV(FPE_C32, FPE_R32, FPE_NP_F32); break;
+    case FPE_C32 * 4 + FPE_C32: FPE_EV(FPE_C32, FPE_C32, FPE_NP_F32); break;
     default: return -1;
   }
 #undef FPE_EV
