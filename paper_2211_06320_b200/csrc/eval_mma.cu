@@ -30,7 +30,7 @@ namespace fpe {
 #define FPE_MMA_MINB 2     // CTAs per SM the register budget is sized for (16 warps: 7.16 vs 7.35 ms with 1)
 #endif
 #ifndef FPE_MMA_STAGES
-#define FPE_MMA_STAGES 4
+#define FPE_MMA_STAGES 6   // 6 vs 4: 7.30 vs 7.36 ms at cfg3
 #endif
 constexpr int kMmaWarps = 8;
 constexpr int kMmaStages = FPE_MMA_STAGES;

@@ -1270,7 +1270,10 @@ struct NPFor {
 // need groups of 128 (k_eval_mma: 8 warps x 16 points).
 static int np_for(int pk, int cdt, long long d_eff) {
   if (cdt == FPE_R32 || cdt == FPE_C32) return FPE_NP_F32;
-  if (cdt == FPE_C64) return d_eff + 1 >= kPiece ? 4 : 2;
+#ifndef FPE_NP_C64_LONG
+#define FPE_NP_C64_LONG 4   // experiments: 2 gives 64-point groups (and no tensor-core items)
+#endif
+  if (cdt == FPE_C64) return d_eff + 1 >= kPiece ? FPE_NP_C64_LONG : 2;
   return (pk == FPE_R64) ? FPE_NP_REAL : 2;
 }
 
