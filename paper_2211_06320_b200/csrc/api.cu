@@ -586,7 +586,7 @@ fpe_status fpe_horner(fpe_poly h, const void* points, fpe_dtype pt_dt, int64_t n
     launch_horner(pt_dt, points, n_points, P, values_out, reinterpret_cast<long long*>(exps_out), s);
   } else {
     run_horner_tiled(pt_dt, points, n_points, P, static_cast<uint32_t*>(workspace), values_out,
-                     reinterpret_cast<long long*>(exps_out), s);
+                     reinterpret_cast<long long*>(exps_out), s, ws_bytes);
   }
   stg.mark("horner_full");
   g_last = LastCall{};

@@ -1097,7 +1097,9 @@ __device__ __forceinline__ void stream_full(Ring<CK>& R, int lo, int hi, const t
 template <int PK, int CK, int OK, int NP>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __restrict__ pts, long long n, PolyDev P,
                                                                  uint32_t* __restrict__ ctr, void* __restrict__ vals,
-                                                                 long long* __restrict__ exps) {
+                                                                 long long* __restrict__ exps,
+                                                                 const uint32_t* __restrict__ list,
+                                                                 const uint32_t* __restrict__ list_n) {
   using CT = typename Step<CK>::CT;
   using W = typename Step<CK>::W;
   constexpr bool CPLX = PtTraits<OK>::cplx;
@@ -1112,7 +1114,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
   __syncwarp();
   Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0, -1};
   const int hi = (int)(P.k_max - P.k_min);
-  const long long ngroups = (n + 32 * NP - 1) / (32 * NP);
+  // list mode (the points k_horner_mma leaves to this kernel): positions index list[0 .. *list_n)
+  const long long nn = list ? (long long)*list_n : n;
+  const long long ngroups = (nn + 32 * NP - 1) / (32 * NP);
   for (;;) {
     uint32_t g = 0;
     if (lane == 0) g = atomicAdd(ctr, 1u);
@@ -1120,20 +1124,21 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
     if ((long long)g >= ngroups) break;
     ring_begin(R, 0, hi);
     double x[NP], y[NP];
-    long long idx[NP];   // sorted position
+    long long idx[NP];   // the point's index in the caller's order (-1: none)
     W zr[NP], zi[NP], br[NP], bi[NP];
     int E[NP];
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
-      idx[j] = (long long)g * (32 * NP) + j * 32 + lane;
+      const long long q = (long long)g * (32 * NP) + j * 32 + lane;
+      idx[j] = q < nn ? (list ? (long long)__ldg(list + q) : q) : -1;
       x[j] = 0.0; y[j] = 0.0;
-      if (idx[j] < n) load_point<PK>(pts, idx[j], x[j], y[j]);
+      if (idx[j] >= 0) load_point<PK>(pts, idx[j], x[j], y[j]);
       zr[j] = (W)x[j]; zi[j] = (W)y[j]; br[j] = 0; bi[j] = 0; E[j] = 0;
     }
     stream_full<CK, NP, CPLX>(R, 0, hi, zr, zi, br, bi, E);
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
-      if (idx[j] >= n) continue;
+      if (idx[j] < 0) continue;
       Acc A{(double)br[j], (double)bi[j], 0, true};
       if (!isfinite(x[j]) || !isfinite(y[j]) || (x[j] == 0.0 && y[j] == 0.0)) {
         const Fin f = finalize<CPLX>(x[j], y[j], A, P);   // NaN / a_0 (the E = 0 paths)
@@ -1149,6 +1154,123 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
         qr = r; qi = i; Ez = p.E;
       }
       store_value<OK>(vals, exps, idx[j], qr, qi, Ez + E[j] + P.shift);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Full Horner on the FP64 tensor cores (the context baseline, fpe_horner, complex fp64 coefficients): the
+// same phase-split contraction as the tensor-core pieces (mma_piece.cuh), over EVERY piece of the
+// coefficient range for every point.  A CTA of 8 warps takes 128 consecutive points and walks the pieces
+// top-down, each piece's chunks in increasing order through a CTA-shared TMA ring; a piece's partial is
+// folded into the point's extended-range accumulator with z^16384 (as the evaluator's long windows).
+// Without the band there is no magnitude bound inside a piece: for |z| > 1 the accumulators and the B
+// fragment are rescaled by 2^-delta per chunk, delta = floor(256 log2|z|) (exact powers of two, so only
+// underflowing -- negligible -- early terms are lost); for |z| <= 1 the terms only shrink.  Points outside
+// 2^-3 <= max(|x|, |y|) < 2^3 (the range of the chunk powers u^i <= z^240), zero and non-finite points are
+// appended to a list that k_horner_tiled evaluates afterwards.
+constexpr int kHmWarps = 8;
+constexpr int kHmStages = 6;
+
+template <int PK>
+__global__ void __launch_bounds__(kHmWarps * 32, 2) k_horner_mma(const void* __restrict__ pts, long long n, PolyDev P,
+                                                                uint32_t* __restrict__ ctrs, uint32_t* __restrict__ rejects,
+                                                                void* __restrict__ vals, long long* __restrict__ exps) {
+  constexpr bool CPLX = true;
+  __shared__ __align__(128) double2 ring[kHmStages][kChunk];
+  __shared__ uint64_t full[kHmStages], empty[kHmStages];
+  __shared__ uint32_t grp_sh;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) {
+    for (int st = 0; st < kHmStages; ++st) { mbar_init(full + st, 1); mbar_init(empty + st, kHmWarps); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double2* coef = static_cast<const double2*>(P.coef);
+  const long long nchunks = (P.k_max - P.k_min) / kChunk + 1;      // chunks holding [0, d_eff]
+  const int ptop = (int)((nchunks - 1) / kMmaPieceChunks);
+  const int nq_top = (int)(nchunks - (long long)ptop * kMmaPieceChunks);
+  auto chunk_of = [&](long long t) -> long long {   // the t-th chunk of a group: pieces top-down, chunks up
+    if (t < nq_top) return (long long)ptop * kMmaPieceChunks + t;
+    const long long u = t - nq_top;
+    return (long long)(ptop - 1 - u / kMmaPieceChunks) * kMmaPieceChunks + (u % kMmaPieceChunks);
+  };
+  uint32_t t_seq = 0, t_issued = 0;
+  auto issue = [&](long long chunk) {   // thread 0
+    const int st = (int)(t_issued % kHmStages);
+    if (t_issued >= (uint32_t)kHmStages) mbar_wait(empty + st, ((t_issued / kHmStages) - 1) & 1u);
+    fence_proxy_async();
+    mbar_expect_tx(full + st, kChunk * sizeof(double2));
+    tma_load_1d(ring[st], coef + (size_t)chunk * kChunk, kChunk * sizeof(double2), full + st);
+    ++t_issued;
+  };
+  const long long ngroups = (n + 127) / 128;
+  for (;;) {
+    if (tid == 0) grp_sh = atomicAdd(ctrs, 1u);
+    __syncthreads();
+    const uint32_t grp = grp_sh;
+    __syncthreads();
+    if ((long long)grp >= ngroups) break;
+    if (tid == 0)
+      for (long long i = 0; i < kHmStages && i < nchunks; ++i) issue(chunk_of(i));
+    long long issued_local = min((long long)kHmStages, nchunks);
+    const long long pos = (long long)grp * 128 + 16 * w + (lane & 15);
+    double x = 0.0, y = 0.0;
+    if (pos < n) load_point<PK>(pts, pos, x, y);
+    const double mz = fmax(fabs(x), fabs(y));
+    const int ez = (mz != 0.0 && isfinite(mz)) ? frexp_exp(mz) : 10000;
+    const int act = (pos < n && isfinite(x) && isfinite(y) && ez >= -2 && ez <= 3) ? 1 : 0;   // 2^-3 <= m < 2^3
+    if (lane < 16 && pos < n && !act) rejects[atomicAdd(ctrs + 1, 1u)] = (uint32_t)pos;
+    // per-chunk rescaling for |z| > 1: delta = floor(256 log2|z|)
+    const int delta = act ? max(0, (int)floor(256.0 * log2(hypot(x, y)))) : 0;
+    const int g = lane >> 2, c = lane & 3;
+    double sb[2], sc[2][2];   // 2^-delta of the B columns g, 8 + g and of the C columns 2c, 2c + 1
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      sb[t] = pow2i(-__shfl_sync(0xffffffffu, delta, 8 * t + g));
+#pragma unroll
+      for (int e = 0; e < 2; ++e) sc[t][e] = pow2i(-__shfl_sync(0xffffffffu, delta, 8 * t + 2 * c + e));
+    }
+    XAcc A{0.0, 0.0, 0, 0, false, false, {}};
+    for (int p = ptop; p >= 0; --p) {
+      const int nq = (p == ptop) ? nq_top : kMmaPieceChunks;
+      MmaFrag F;
+      mma_setup(F, x, y, act);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) { F.cwr[t] *= sb[t]; F.cwi[t] *= sb[t]; }   // V advances by w 2^-delta
+      const bool busy = __any_sync(0xffffffffu, act);
+      for (int k = 0; k < nq; ++k) {
+        const int st = (int)(t_seq % kHmStages);
+        mbar_wait(full + st, (t_seq / kHmStages) & 1u);
+        if (busy) {
+          mma_chunk(F, ring[st]);
+          if (k + 1 < nq) {   // C 2^-delta before the next chunk's terms
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) { F.cr[t][e] *= sc[t][e & 1]; F.ci[t][e] *= sc[t][e & 1]; }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+        ++t_seq;
+        if (tid == 0 && issued_local < nchunks) issue(chunk_of(issued_local));
+        ++issued_local;
+        __syncwarp();
+      }
+      double pr, pi;
+      mma_finish(F, x, y, pr, pi);
+      if (act) {
+        long long pe = (long long)delta * (nq - 1);
+        double r = pr, i = pi;
+        xnorm(r, i, pe);
+        xacc_fold<CPLX>(A, r, i, pe, p * kPiece, x, y);
+      }
+    }
+    if (lane < 16 && act) {
+      const Acc a{A.r, A.i, A.base, A.started};
+      Fin f = finalize<CPLX>(x, y, a, P);
+      store_value<FPE_C64>(vals, exps, pos, f.re, f.im, f.E + A.E);
     }
   }
 }
@@ -1295,11 +1417,31 @@ static void launch_horner_tiled_t(const void* pts, long long n, const PolyDev& P
   const size_t smem = eval_smem<CK>();
   const int grid = persistent_grid(reinterpret_cast<const void*>(k_horner_tiled<PK, CK, OK, NP>), kWarps * 32, smem);
   cudaMemsetAsync(ctr, 0, sizeof(uint32_t), s);
-  k_horner_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(pts, n, P, ctr, vals, exps);
+  k_horner_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(pts, n, P, ctr, vals, exps, nullptr, nullptr);
+}
+
+template <int PK>
+static void launch_horner_mma_t(const void* pts, long long n, const PolyDev& P, uint32_t* ctrs, uint32_t* rejects,
+                                void* vals, long long* exps, cudaStream_t s) {
+  const int grid = persistent_grid(reinterpret_cast<const void*>(k_horner_mma<PK>), kHmWarps * 32, 0);
+  k_horner_mma<PK><<<grid, kHmWarps * 32, 0, s>>>(pts, n, P, ctrs, rejects, vals, exps);
+  // the rejected points: the vector full Horner over the list
+  constexpr int NP = NPFor<PK, FPE_C64>::value;
+  const size_t smem = eval_smem<FPE_C64>();
+  const int g2 = persistent_grid(reinterpret_cast<const void*>(k_horner_tiled<PK, FPE_C64, FPE_C64, NP>), kWarps * 32, smem);
+  k_horner_tiled<PK, FPE_C64, FPE_C64, NP><<<g2, kWarps * 32, smem, s>>>(pts, n, P, ctrs + 2, vals, exps, rejects, ctrs + 1);
 }
 
 bool run_horner_tiled(int pk, const void* pts, long long n, const PolyDev& P, uint32_t* ctr, void* vals,
-                      long long* exps, cudaStream_t s) {
+                      long long* exps, cudaStream_t s, size_t ws_bytes) {
+  // complex fp64 coefficients: the tensor-core full Horner (ctr: 3 counters + the reject list of n points)
+  if (P.cdt == FPE_C64 && !P.wide && (pk == FPE_C64 || pk == FPE_R64) && ws_bytes >= 256 + (size_t)n * 4) {
+    cudaMemsetAsync(ctr, 0, 4 * sizeof(uint32_t), s);
+    uint32_t* rejects = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ctr) + 256);
+    if (pk == FPE_C64) launch_horner_mma_t<FPE_C64>(pts, n, P, ctr, rejects, vals, exps, s);
+    else launch_horner_mma_t<FPE_R64>(pts, n, P, ctr, rejects, vals, exps, s);
+    return true;
+  }
   switch (pk * 4 + P.cdt) {
     case FPE_R64 * 4 + FPE_R64: launch_horner_tiled_t<FPE_R64, FPE_R64>(pts, n, P, ctr, vals, exps, s); break;
     case FPE_R64 * 4 + FPE_C64: launch_horner_tiled_t<FPE_R64, FPE_C64>(pts, n, P, ctr, vals, exps, s); break;
