@@ -1167,8 +1167,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
 // Without the band there is no magnitude bound inside a piece: for |z| > 1 the accumulators and the B
 // fragment are rescaled by 2^-delta per chunk, delta = floor(256 log2|z|) (exact powers of two, so only
 // underflowing -- negligible -- early terms are lost); for |z| <= 1 the terms only shrink.  Points outside
-// 2^-3 <= max(|x|, |y|) < 2^3 (the range of the chunk powers u^i <= z^240), zero and non-finite points are
-// appended to a list that k_horner_tiled evaluates afterwards.
+// 2^-4 <= |z| < 2^3.99 (the range of w = z^256 and of the chunk powers u^i <= z^240), zero and
+// non-finite points (0.8% of sphere points) are appended to a list that k_horner_tiled evaluates afterwards
+// with one point per lane (its tail is one warp streaming every coefficient: the shortest chain per
+// coefficient wins).
 constexpr int kHmWarps = 8;
 constexpr int kHmStages = 6;
 
@@ -1217,17 +1219,21 @@ __global__ void __launch_bounds__(kHmWarps * 32, 2) k_horner_mma(const void* __r
     const long long pos = (long long)grp * 128 + 16 * w + (lane & 15);
     double x = 0.0, y = 0.0;
     if (pos < n) load_point<PK>(pts, pos, x, y);
-    const double mz = fmax(fabs(x), fabs(y));
-    const int ez = (mz != 0.0 && isfinite(mz)) ? frexp_exp(mz) : 10000;
-    const int act = (pos < n && isfinite(x) && isfinite(y) && ez >= -2 && ez <= 3) ? 1 : 0;   // 2^-3 <= m < 2^3
+    // 2^-4 <= |z| < 2^3.99: z^256 (w) stays below 2^1022, the chunk powers u^i <= z^240 too
+    const double r2 = __fma_rn(x, x, y * y);
+    const int act = (pos < n && isfinite(x) && isfinite(y) && r2 >= 0x1p-8 && r2 < 252.0) ? 1 : 0;
     if (lane < 16 && pos < n && !act) rejects[atomicAdd(ctrs + 1, 1u)] = (uint32_t)pos;
-    // per-chunk rescaling for |z| > 1: delta = floor(256 log2|z|)
-    const int delta = act ? max(0, (int)floor(256.0 * log2(hypot(x, y)))) : 0;
+    // rescaling for |z| > 1: the chunk powers u^i start at 2^-delta0, delta0 = floor(240 log2|z|) (so that the
+    // largest, z^240, is ~1), and every chunk scales by 2^-delta, delta = floor(256 log2|z|)
+    const double l2z = act ? log2(hypot(x, y)) : 0.0;
+    const int delta = act ? max(0, (int)floor(256.0 * l2z)) : 0;
+    const int delta0 = act ? max(0, (int)floor(240.0 * l2z)) : 0;
     const int g = lane >> 2, c = lane & 3;
-    double sb[2], sc[2][2];   // 2^-delta of the B columns g, 8 + g and of the C columns 2c, 2c + 1
+    double sb[2], sb0[2], sc[2][2];   // 2^-delta (2^-delta0) of the B columns g, 8 + g; 2^-delta of C columns 2c, 2c + 1
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       sb[t] = pow2i(-__shfl_sync(0xffffffffu, delta, 8 * t + g));
+      sb0[t] = pow2i(-__shfl_sync(0xffffffffu, delta0, 8 * t + g));
 #pragma unroll
       for (int e = 0; e < 2; ++e) sc[t][e] = pow2i(-__shfl_sync(0xffffffffu, delta, 8 * t + 2 * c + e));
     }
@@ -1237,7 +1243,11 @@ __global__ void __launch_bounds__(kHmWarps * 32, 2) k_horner_mma(const void* __r
       MmaFrag F;
       mma_setup(F, x, y, act);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) { F.cwr[t] *= sb[t]; F.cwi[t] *= sb[t]; }   // V advances by w 2^-delta
+      for (int t = 0; t < 2; ++t) {
+        F.cwr[t] *= sb[t]; F.cwi[t] *= sb[t];   // V advances by w 2^-delta
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) { F.vr[t][ks] *= sb0[t]; F.vi[t][ks] *= sb0[t]; }   // V_0 = u^i 2^-delta0
+      }
       const bool busy = __any_sync(0xffffffffu, act);
       for (int k = 0; k < nq; ++k) {
         const int st = (int)(t_seq % kHmStages);
@@ -1261,7 +1271,7 @@ __global__ void __launch_bounds__(kHmWarps * 32, 2) k_horner_mma(const void* __r
       double pr, pi;
       mma_finish(F, x, y, pr, pi);
       if (act) {
-        long long pe = (long long)delta * (nq - 1);
+        long long pe = (long long)delta0 + (long long)delta * (nq - 1);
         double r = pr, i = pi;
         xnorm(r, i, pe);
         xacc_fold<CPLX>(A, r, i, pe, p * kPiece, x, y);
@@ -1425,8 +1435,8 @@ static void launch_horner_mma_t(const void* pts, long long n, const PolyDev& P, 
                                 void* vals, long long* exps, cudaStream_t s) {
   const int grid = persistent_grid(reinterpret_cast<const void*>(k_horner_mma<PK>), kHmWarps * 32, 0);
   k_horner_mma<PK><<<grid, kHmWarps * 32, 0, s>>>(pts, n, P, ctrs, rejects, vals, exps);
-  // the rejected points: the vector full Horner over the list
-  constexpr int NP = NPFor<PK, FPE_C64>::value;
+  // the rejected points: the vector full Horner over the list, one point per lane
+  constexpr int NP = 1;
   const size_t smem = eval_smem<FPE_C64>();
   const int g2 = persistent_grid(reinterpret_cast<const void*>(k_horner_tiled<PK, FPE_C64, FPE_C64, NP>), kWarps * 32, smem);
   k_horner_tiled<PK, FPE_C64, FPE_C64, NP><<<g2, kWarps * 32, smem, s>>>(pts, n, P, ctrs + 2, vals, exps, rejects, ctrs + 1);
