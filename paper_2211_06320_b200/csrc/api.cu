@@ -55,7 +55,7 @@ constexpr long long kMaxBatch = 1ll << 28;
 // workspace = kWsHeader bytes of counters (kStat*) + the path's scratch
 static size_t ws_bytes_for(long long n) {
   long long b = n < kMaxBatch ? n : kMaxBatch;
-  size_t naive = (((size_t)b * sizeof(int2) + 255) & ~size_t(255)) + (kSparseTab + 1) * sizeof(int);   // lr + table
+  size_t naive = (((size_t)b * sizeof(int2) + 255) & ~size_t(255)) + (kSparseTab + 2) * sizeof(int);   // lr + table + queue counter
   size_t tiled = tiled_ws_bytes(b);
   return kWsHeader + (naive > tiled ? naive : tiled);
 }

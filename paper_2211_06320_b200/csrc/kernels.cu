@@ -89,16 +89,30 @@ __device__ __forceinline__ void xadd(double& sr, double& si, long long& se, doub
 }
 
 
-// Points have very uneven kept counts (cfg4: mean 1.15, max ~1800 near |z| = 1), so a lane-per-point loop
-// would run each warp for its longest point (round 1: 62% of the instructions at 1-7 active lanes).  A warp
-// takes 32 consecutive points, lays their kept terms out flat (exclusive scan of K over the lanes) and
-// computes the terms round-robin over all 32 lanes (kSpRound at a time, into shared memory) -- each term
-// a_k z^k by the polar route from its point's (lambda, tau), a pure function of (z, k) -- and then every
-// lane sums its own point's terms in increasing k in extended range.  A point's result is therefore the
-// same whatever points share its warp.
+// Points have very uneven kept counts (cfg4: mean 1.15, 96% with K = 1, up to all 4096 terms near |z| = 1),
+// so a lane-per-point loop would run each warp for its longest point (round 1: 62% of the instructions at
+// 1-7 active lanes).  Warps claim 32-point items from a work queue.  For points with K <= kSpLong the warp
+// lays the kept terms out flat (exclusive scan of K over the lanes) and computes them round-robin over all
+// 32 lanes (kSpRound at a time, into shared memory) -- each term a_k z^k by the polar route from its
+// point's (lambda, tau), a pure function of (z, k) -- and every lane sums its own point's terms in
+// increasing k in extended range.  A longer list is summed by the whole warp: lane t takes the terms
+// t, t + 32, ... and a fixed tree combines the partials (one lane summing 4096 terms alone kept a chunk
+// busy for 1.2 ms, twice the rest of the kernel).  Either way a point's result is the same whatever
+// points share its warp.
 constexpr int kSpWarps = 8;
 constexpr int kSpRound = 64;    // terms per warp and round in shared memory
 constexpr int kSpTab = kSparseTab;
+#ifndef FPE_SP_GRAB
+#define FPE_SP_GRAB 4
+#endif
+#ifndef FPE_SP_MINB
+#define FPE_SP_MINB 4
+#endif
+constexpr int kSpGrab = FPE_SP_GRAB;
+#ifndef FPE_SP_LONG
+#define FPE_SP_LONG 32
+#endif
+constexpr int kSpLong = FPE_SP_LONG;   // kept lists longer than this are summed by the whole warp      // warp-items of 32 points claimed per atomic (dynamic work queue)
 struct SpTerm { double r, i; long long e; };
 
 template <int CK, bool CPLX>
@@ -128,6 +142,7 @@ __global__ void __launch_bounds__(1024) k_sparse_table(PolyDev P, int* __restric
   while (((P.k_max - P.k_min) >> tb) >= kSpTab) ++tb;
   const int nb = (int)((P.k_max - P.k_min) >> tb) + 1;
   const int ng = (int)P.n_good;
+  if (threadIdx.x == 0) tab[kSpTab + 1] = 0;   // the evaluator's work-queue counter
   for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
     const long long key = P.k_min + ((long long)b << tb);
     int lo = 0, hi = ng;
@@ -136,10 +151,22 @@ __global__ void __launch_bounds__(1024) k_sparse_table(PolyDev P, int* __restric
   }
 }
 
+#ifdef FPE_ITEM_TRACE
+// Debugging (build with -DFPE_ITEM_TRACE): per claimed chunk of k_eval_sparse_coop, {start ns, end ns,
+// max K << 32 | sum K}.
+__device__ unsigned long long fpe_sp_trace[1 << 20][3];
+__device__ unsigned int fpe_sp_trace_n;
+__device__ __forceinline__ unsigned long long sp_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 template <int PK, int CK, int OK>
-__global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* __restrict__ pts, long long n, PolyDev P,
+__global__ void __launch_bounds__(kSpWarps * 32, FPE_SP_MINB) k_eval_sparse_coop(const void* __restrict__ pts, long long n, PolyDev P,
                                                                     const int2* __restrict__ lr,
-                                                                    const int* __restrict__ tab,
+                                                                    int* __restrict__ tab,
                                                                     void* __restrict__ vals,
                                                                     long long* __restrict__ exps) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
@@ -156,8 +183,22 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
   polar_t* PL = pol + w * 32;
   int* OF = offs + w * 33;
   int* FI = firsts + w * 32;
-  const long long nwarps = (long long)gridDim.x * kSpWarps;
-  for (long long base = ((long long)blockIdx.x * kSpWarps + w) * 32; base < n; base += nwarps * 32) {
+  // dynamic work queue: a warp claims kSpGrab warp-items at a time (kept counts are very uneven, and a
+  // static split left the SMs idle for a third of the kernel waiting for the slowest ones)
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(tab + kSpTab + 1);
+  const long long nchunks = ((n + 31) / 32 + kSpGrab - 1) / kSpGrab;
+  for (;;) {
+  unsigned int c = 0;
+  if (lane == 0) c = atomicAdd(ctr, 1u);
+  c = __shfl_sync(0xffffffffu, c, 0);
+  if ((long long)c >= nchunks) break;
+#ifdef FPE_ITEM_TRACE
+  const unsigned long long tr_t0 = sp_gtimer();
+  unsigned long long tr_info = 0;
+#endif
+  for (int sub = 0; sub < kSpGrab; ++sub) {
+    const long long base = ((long long)c * kSpGrab + sub) * 32;
+    if (base >= n) break;
     const long long i = base + lane;
     double x = 0.0, y = 0.0;
     int first = 0, K = 0, state = 0;   // state 0: sum of the kept terms; 1: non-finite z (NaN); 2: z = 0
@@ -176,14 +217,23 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
         if (K > 0) PL[lane] = polar_of<CPLX>(x, y);
       }
     }
-    int off = K;   // inclusive scan of K over the warp
+    // points with long kept lists are summed by the whole warp (below); the rest lay their terms out flat
+    const bool lng = K > kSpLong;
+    const int Kf = lng ? 0 : K;
+    int off = Kf;   // inclusive scan of the flat counts over the warp
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, off, o); if (lane >= o) off += v; }
     const int total = __shfl_sync(0xffffffffu, off, 31);
+#ifdef FPE_ITEM_TRACE
+    {
+      const unsigned long long mk = __reduce_max_sync(0xffffffffu, (unsigned)K);
+      tr_info = (max(tr_info >> 32, mk) << 32) | ((tr_info & 0xffffffffull) + (unsigned)__reduce_add_sync(0xffffffffu, (unsigned)K));
+    }
+#endif
     OF[lane + 1] = off;
     if (lane == 0) OF[0] = 0;
     FI[lane] = first;
-    off -= K;   // exclusive
+    off -= Kf;   // exclusive
     __syncwarp();
     double sr = 0.0, si = 0.0;
     long long se = 0;
@@ -198,9 +248,30 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
       }
       __syncwarp();
       // this lane's terms inside the round, in increasing k (the flat order)
-      const int t0 = max(off, r0), t1 = min(off + K, r0 + rn);
+      const int t0 = max(off, r0), t1 = min(off + Kf, r0 + rn);
       for (int g = t0; g < t1; ++g) { const SpTerm t = T[g - r0]; xadd(sr, si, se, t.r, t.i, t.e); }
       __syncwarp();
+    }
+    // long lists (K > kSpLong, rare: points near the unit circle): lane t sums the terms t, t + 32, ... of the
+    // point in increasing k, then a fixed xor tree combines the 32 partials (xadd is commutative, so every
+    // lane ends with the same value) -- a fixed order per point, whatever points share the warp
+    for (unsigned lm = __ballot_sync(0xffffffffu, lng); lm; lm &= lm - 1) {
+      const int q = __ffs(lm) - 1;
+      const int fq = __shfl_sync(0xffffffffu, first, q), Kq = __shfl_sync(0xffffffffu, K, q);
+      const polar_t pz = PL[q];
+      double pr = 0.0, pim = 0.0;
+      long long pe = 0;
+      for (int t = lane; t < Kq; t += 32) {
+        const SpTerm u = sparse_term<CK, CPLX>(P, pz, fq + t, __ldg(sidx + fq + t));
+        xadd(pr, pim, pe, u.r, u.i, u.e);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double qr = __shfl_xor_sync(0xffffffffu, pr, o), qi = __shfl_xor_sync(0xffffffffu, pim, o);
+        const long long qe = __shfl_xor_sync(0xffffffffu, pe, o);
+        xadd(pr, pim, pe, qr, qi, qe);
+      }
+      if (lane == q) { sr = pr; si = pim; se = (pr == 0.0 && pim == 0.0) ? 0 : pe; }
     }
     if (i < n) {
       if (state == 1) {
@@ -214,6 +285,13 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_eval_sparse_coop(const void* 
         store_value<OK>(vals, exps, i, sr, si, se + P.shift);
       }
     }
+  }
+#ifdef FPE_ITEM_TRACE
+  if (lane == 0) {
+    const unsigned int q = atomicAdd(&fpe_sp_trace_n, 1u);
+    if (q < (1u << 20)) { fpe_sp_trace[q][0] = tr_t0; fpe_sp_trace[q][1] = sp_gtimer(); fpe_sp_trace[q][2] = tr_info; }
+  }
+#endif
   }
 }
 
@@ -419,15 +497,20 @@ static void launch_eval_sparse_t(const void* pts, long long n, const PolyDev& P,
   const size_t smem = sizeof(SpTerm) * kSpWarps * kSpRound + sizeof(polar_t) * kSpWarps * 32 +
                       sizeof(int) * (kSpWarps * 65);
   k_sparse_table<<<1, 1024, 0, s>>>(P, tab);
-  static bool attr_set[64] = {};
+  // one wave of resident CTAs (grid-stride): a grid of several partial waves left the last one at
+  // a fraction of the occupancy this latency-bound kernel needs
+  static int resident[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 64 && !attr_set[dev]) {
+  if (dev < 64 && !resident[dev]) {
     cudaFuncSetAttribute(k_eval_sparse_coop<PK, CK, OK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr_set[dev] = true;
+    int occ = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_sparse_coop<PK, CK, OK>, kSpWarps * 32, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident[dev] = std::max(1, occ) * sms;
   }
   const long long warps = (n + 31) / 32;
-  const long long blocks = std::min<long long>((warps + kSpWarps - 1) / kSpWarps, 148ll * 16);
+  const long long blocks = std::min<long long>((warps + kSpWarps - 1) / kSpWarps, dev < 64 ? resident[dev] : 148ll * 4);
   k_eval_sparse_coop<PK, CK, OK><<<(int)std::max(1ll, blocks), kSpWarps * 32, smem, s>>>(pts, n, P, lr, tab, vals, exps);
 }
 
@@ -475,3 +558,16 @@ bool launch_horner(int pk, const void* pts, long long n, const PolyDev& P, void*
 }
 
 }  // namespace fpe
+
+#ifdef FPE_ITEM_TRACE
+extern "C" int fpe_debug_sp_trace(unsigned long long* host, int cap, int reset) {
+  unsigned int n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, fpe::fpe_sp_trace_n, sizeof(n));
+  n = n < (1u << 20) ? n : (1u << 20);
+  const int m = (int)(n < (unsigned)cap ? n : (unsigned)cap);
+  if (host && m) cudaMemcpyFromSymbol(host, fpe::fpe_sp_trace, (size_t)m * 24);
+  if (reset) { unsigned int z = 0; cudaMemcpyToSymbol(fpe::fpe_sp_trace_n, &z, sizeof(z)); }
+  return m;
+}
+#endif

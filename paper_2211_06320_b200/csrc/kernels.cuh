@@ -10,7 +10,7 @@ constexpr int kSmemHullDbl = 1536;   // ... also as doubles (36 KiB) by the buck
 void launch_classify(int pk, const void* pts, long long n, const PolyDev& P, int2* lr, fpe_diag* diag,
                      unsigned long long* hard, cudaStream_t s);
 constexpr int kSparseTab = 4096;   // buckets of the sparse evaluator's good-index table (int32[kSparseTab + 1])
-// tab: device scratch of (kSparseTab + 1) int32, written by the call
+// tab: device scratch of (kSparseTab + 2) int32 (the table and a work-queue counter), written by the call
 bool launch_eval_sparse(int pk, const void* pts, long long n, const PolyDev& P, const int2* lr, int* tab, void* vals,
                         long long* exps, cudaStream_t s);
 // fpe_diag::cancel from the outputs (after an evaluation); ok = fpe_dtype of the values
