@@ -1295,14 +1295,34 @@ __global__ void __launch_bounds__(kHmWarps * 32, 2) k_horner_mma(const void* __r
 #ifndef FPE_UNSORT_MINB
 #define FPE_UNSORT_MINB 3   // CTAs per SM the register budget is sized for (2 x 3: 2.27 -> 2.02 ms at cfg3)
 #endif
+// Half of the points need no power (window starting at k_min), and they are spread at random over the
+// lanes, so a warp used to run the polar route for its few lanes that need it while the rest idled
+// (fpe_polar / dd arithmetic were 85% of k_unsort's instructions).  The points that need z^l are queued per
+// warp in shared memory and the polar route runs on 32 queued points at a time (the rest at the end).
+struct UTask { double re, im, x, y; long long E, nn, i; };
+constexpr int kUnsortWarps = 8;
+constexpr int kUnsortQ = 32 + 32 * FPE_UNSORT_U;   // queue entries per warp: < 32 left over + one iteration
+
 template <int PK, int OK>
-__global__ void __launch_bounds__(256, FPE_UNSORT_MINB) k_unsort(const PtOut* __restrict__ staged, const uint32_t* __restrict__ spos,
+__global__ void __launch_bounds__(32 * kUnsortWarps, FPE_UNSORT_MINB) k_unsort(const PtOut* __restrict__ staged, const uint32_t* __restrict__ spos,
                                                 long long n, const void* __restrict__ pts, PolyDev P,
                                                 void* __restrict__ vals, long long* __restrict__ exps) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
   constexpr int U = FPE_UNSORT_U;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+#ifndef FPE_UNSORT_NOQ
+  __shared__ UTask q_s[kUnsortWarps][kUnsortQ];
+  UTask* Q = q_s[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int qn = 0;   // queued points (warp-uniform)
+  auto run = [&](const UTask& t) {
+    const Acc A{t.re, t.im, (int)(t.nn - P.k_min), true};
+    const Fin f = finalize<CPLX, PtTraits<OK>::f32>(t.x, t.y, A, P);
+    store_value<OK>(vals, exps, t.i, f.re, f.im, f.E + t.E);
+  };
+#endif
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 - (threadIdx.x & 31) < n; i0 += U * stride) {
     double re[U], im[U], x[U], y[U];
     long long E[U], nn[U];
 #pragma unroll
@@ -1323,13 +1343,37 @@ __global__ void __launch_bounds__(256, FPE_UNSORT_MINB) k_unsort(const PtOut* __
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const long long i = i0 + u * stride;
+#ifndef FPE_UNSORT_NOQ
+      // z^l is needed (finalize's power branch) for a finite nonzero z with a window above k_min
+      const bool need = i < n && nn[u] > 0 && isfinite(x[u]) && isfinite(y[u]) && (x[u] != 0.0 || y[u] != 0.0);
+      const unsigned m = __ballot_sync(0xffffffffu, need);
+      if (need) Q[qn + __popc(m & lt)] = UTask{re[u], im[u], x[u], y[u], E[u], nn[u], i};
+      else if (i < n) {
+#else
       if (i < n) {
+#endif
         const Acc A{re[u], im[u], (int)(nn[u] >= 0 ? nn[u] - P.k_min : 0), nn[u] >= 0};
         const Fin f = finalize<CPLX, PtTraits<OK>::f32>(x[u], y[u], A, P);
         store_value<OK>(vals, exps, i, f.re, f.im, f.E + E[u]);
       }
+#ifndef FPE_UNSORT_NOQ
+      qn += __popc(m);
+#endif
     }
+#ifndef FPE_UNSORT_NOQ
+    __syncwarp();
+    while (qn >= 32) {
+      qn -= 32;
+      const UTask t = Q[qn + lane];
+      __syncwarp();
+      run(t);
+    }
+#endif
   }
+#ifndef FPE_UNSORT_NOQ
+  __syncwarp();
+  if (lane < qn) run(Q[lane]);
+#endif
 }
 
 // ------------------------------------------------------------------------------------------------
