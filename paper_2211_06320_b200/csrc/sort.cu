@@ -59,13 +59,20 @@ __device__ __forceinline__ double2 load_point_any(int pk, const void* __restrict
 // Records and points to bucket positions: bucket start + the classifying CTA's slice of the bucket + the
 // point's rank in that slice (both from the classifier) -- a pure streaming pass over all points, no
 // atomics.  The points are copied along (as doubles), so the evaluator reads everything coalesced.
-__global__ void __launch_bounds__(256) k_bucket_scatter(const uint2* __restrict__ keys, const int2* __restrict__ lr,
+#ifndef FPE_SCATTER_U
+#define FPE_SCATTER_U 4
+#endif
+#ifndef FPE_SCATTER_MINB
+#define FPE_SCATTER_MINB 1
+#endif
+__global__ void __launch_bounds__(256, FPE_SCATTER_MINB) k_bucket_scatter(const uint2* __restrict__ keys, const int2* __restrict__ lr,
                                                         int pk, const void* __restrict__ pts, long long n,
                                                         long long ppc, const uint32_t* __restrict__ bstart,
                                                         const uint32_t* __restrict__ cta_base, int cb,
                                                         PtRec* __restrict__ rec, uint32_t* __restrict__ spos) {
-  constexpr int U = 4;   // independent loads in flight per thread
+  constexpr int U = FPE_SCATTER_U;   // independent loads in flight per thread
   const long long stride = (long long)gridDim.x * blockDim.x;
+  const uint32_t ppc32 = (uint32_t)ppc;   // n <= kMaxBatch = 2^28: 32-bit index arithmetic
   for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
     uint2 kr[U];
     int2 w[U];
@@ -80,7 +87,7 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(const uint2* __restrict_
       const long long i = i0 + u * stride;
       if (i < n) {
         const uint32_t c = kr[u].x >> (24 - cb);
-        const uint32_t pos = __ldg(bstart + c) + __ldg(cta_base + ((size_t)(i / ppc) << cb) + c) + kr[u].y;
+        const uint32_t pos = __ldg(bstart + c) + __ldg(cta_base + ((size_t)((uint32_t)i / ppc32) << cb) + c) + kr[u].y;
         spos[i] = pos;
         // one 256-bit store (STG.E.ENL2.256): the whole 32-byte sector in one request
         const unsigned long long zx = __double_as_longlong(z[u].x), zy = __double_as_longlong(z[u].y);
@@ -165,7 +172,7 @@ void bucket_finish(const uint2* keys, const int2* lr, long long n, long long ppc
                    const void* pts, long long k_min, const Plan& plan, cudaStream_t s) {
   const int cb = coarse_bits(n);
   k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, cb);
-  const long long blocks = std::min<long long>((n + 4 * 256 - 1) / (4 * 256), 148ll * 32);
+  const long long blocks = std::min<long long>((n + FPE_SCATTER_U * 256 - 1) / (FPE_SCATTER_U * 256), 148ll * 32);
   k_bucket_scatter<<<(int)blocks, 256, 0, s>>>(keys, lr, pk, pts, n, ppc, bstart, cta_base, cb, rec, spos);
   const long long groups = (n + plan.gsize - 1) / plan.gsize;
   k_plan<<<(int)((groups + 7) / 8), 256, 0, s>>>(n, rec, k_min, plan);
