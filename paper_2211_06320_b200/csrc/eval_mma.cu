@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, FPE_MMA_MINB) k_eval_mma(long 
                                                                 int kmin, const PtRec* __restrict__ rec, Plan plan) {
   __shared__ __align__(128) double2 ring[kMmaStages][kChunk];
   __shared__ uint64_t full[kMmaStages], empty[kMmaStages];
-  __shared__ uint2 item_sh;
+  __shared__ uint2 item_sh, next_sh;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < kMmaStages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, kMmaWarps); }
@@ -58,22 +58,31 @@ __global__ void __launch_bounds__(kMmaWarps * 32, FPE_MMA_MINB) k_eval_mma(long 
     tma_load_1d(ring[s], coef + (size_t)piece_chunk * kChunk, kChunk * sizeof(double2), full + s);
     ++t_issued;
   };
-  for (;;) {
-    if (tid == 0) {
+  // Thread 0 claims items one ahead and streams the next item's first chunks into the ring while the warps
+  // finish the current one, so the ring does not drain at item boundaries (short items pay for it otherwise).
+  auto fetch = [&]() -> uint2 {   // thread 0: the next valid item, or the end marker
+    for (;;) {
       const uint32_t it = atomicAdd(plan.mma_ctrs + 1, 1u);
-      item_sh = it < n_items ? plan.mma_items[it] : make_uint2(0xfffffffeu, 0u);
+      if (it >= n_items) return make_uint2(0xfffffffeu, 0u);
+      const uint2 v = plan.mma_items[it];
+      if (v.x != ~0u) return v;
     }
-    __syncthreads();
-    const uint2 item = item_sh;
+  };
+  if (tid == 0) {
+    const uint2 c = fetch();
+    if (c.x != 0xfffffffeu)
+      for (int i = 0; i < kMmaStages; ++i) issue((int)c.y * kPieceChunks + i);
+    item_sh = c;
+    next_sh = c.x != 0xfffffffeu ? fetch() : c;
+  }
+  __syncthreads();
+  for (;;) {
+    const uint2 item = item_sh, nxt = next_sh;
     __syncthreads();
     if (item.x == 0xfffffffeu) break;
-    if (item.x == ~0u) continue;
     const uint32_t grp = item.x;
     const int p = (int)item.y;
     const int q0 = p * kPieceChunks;   // chunks ascend from q0 (mma_piece.cuh)
-    if (tid == 0)
-      for (int i = 0; i < kMmaStages; ++i) issue(q0 + i);
-    __syncwarp();
     // this warp's 16 points: lanes [0, 16) own point 16 w + lane (lanes 16..31 mirror them)
     const int q = 16 * w + (lane & 15);
     const long long pos = (long long)grp * plan.gsize + q;
@@ -96,7 +105,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, FPE_MMA_MINB) k_eval_mma(long 
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
       ++t_seq;
-      if (tid == 0 && k + kMmaStages < kPieceChunks) issue(q0 + k + kMmaStages);
+      if (tid == 0) {
+        const int j = k + kMmaStages;
+        if (j < kPieceChunks) issue(q0 + j);
+        else if (nxt.x != 0xfffffffeu) issue((int)nxt.y * kPieceChunks + (j - kPieceChunks));
+      }
       __syncwarp();
     }
     double orr, oi;
@@ -105,6 +118,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, FPE_MMA_MINB) k_eval_mma(long 
       const GroupDesc d = plan.desc[grp];
       plan.mma_scratch[(size_t)(d.mma_slot + (p - d.mma_p0)) * plan.gsize + q] = make_double2(orr, oi);
     }
+    if (tid == 0) {
+      item_sh = nxt;
+      next_sh = nxt.x != 0xfffffffeu ? fetch() : nxt;
+    }
+    __syncthreads();
   }
 }
 
