@@ -17,10 +17,10 @@ namespace fpe {
 // schedule of the complex Horner step leaves most DFMAs without a reused operand: the vector Horner tops
 // out near 72% of the pipe.  mma.sync DMMA runs the same datapath from its fragments at 99.7%
 // (profiles/r01_dmma_vs_dfma.json).  Over whole 256-coefficient chunks the Horner sum is a dense
-// contraction once split by phase k mod 16:
-//   sum_{k in piece} a_k z^{k-k0} = sum_{m<16} z^m R_m,  R_m = sum_{q,i} a_{k0+256q+16i+m} u^i w^q,
-// u = z^16, w = z^256, and each chunk q (in increasing order) is C += A_q V_q with A_q[m][i] = a_{256q+16i+m}
-// (16 x 16, straight from the staged chunk), V_q[i][p] = u_p^i w_p^q and C[m][p] = R_m at point p
+// contraction once split by phase k mod P (P = kMmaPhases = 32):
+//   sum_{k in piece} a_k z^{k-k0} = sum_{m<P} z^m R_m,  R_m = sum_{q,i} a_{k0+256q+Pi+m} u^i w^q,
+// u = z^P, w = z^256, and each chunk q (in increasing order) is C += A_q V_q with A_q[m][i] = a_{256q+Pi+m}
+// (P x 256/P, straight from the staged chunk), V_q[i][p] = u_p^i w_p^q and C[m][p] = R_m at point p
 // (mma_piece.cuh): 4 real m16n8k4 DMMAs per 4 powers and 8 points for the complex product.  One CTA (8 warps x 16 points = a group) per item
 // (group, piece), the piece's 64 chunks staged once per CTA by TMA into a 4-stage ring shared by the
 // warps.  A point's column is active iff mma_covers (its window covers the whole piece), so every value

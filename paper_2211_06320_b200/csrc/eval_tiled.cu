@@ -1223,11 +1223,11 @@ __global__ void __launch_bounds__(kHmWarps * 32, 2) k_horner_mma(const void* __r
     const double r2 = __fma_rn(x, x, y * y);
     const int act = (pos < n && isfinite(x) && isfinite(y) && r2 >= 0x1p-8 && r2 < 252.0) ? 1 : 0;
     if (lane < 16 && pos < n && !act) rejects[atomicAdd(ctrs + 1, 1u)] = (uint32_t)pos;
-    // rescaling for |z| > 1: the chunk powers u^i start at 2^-delta0, delta0 = floor(240 log2|z|) (so that the
-    // largest, z^240, is ~1), and every chunk scales by 2^-delta, delta = floor(256 log2|z|)
+    // rescaling for |z| > 1: the chunk powers u^i start at 2^-delta0, delta0 = floor(kMmaMaxBPow log2|z|) (so
+    // that the largest, z^(256 - P), is ~1), and every chunk scales by 2^-delta, delta = floor(256 log2|z|)
     const double l2z = act ? log2(hypot(x, y)) : 0.0;
     const int delta = act ? max(0, (int)floor(256.0 * l2z)) : 0;
-    const int delta0 = act ? max(0, (int)floor(240.0 * l2z)) : 0;
+    const int delta0 = act ? max(0, (int)floor((double)kMmaMaxBPow * l2z)) : 0;
     const int g = lane >> 2, c = lane & 3;
     double sb[2], sb0[2], sc[2][2];   // 2^-delta (2^-delta0) of the B columns g, 8 + g; 2^-delta of C columns 2c, 2c + 1
 #pragma unroll
@@ -1243,23 +1243,15 @@ __global__ void __launch_bounds__(kHmWarps * 32, 2) k_horner_mma(const void* __r
       MmaFrag F;
       mma_setup(F, x, y, act);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        F.cwr[t] *= sb[t]; F.cwi[t] *= sb[t];   // V advances by w 2^-delta
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) { F.vr[t][ks] *= sb0[t]; F.vi[t][ks] *= sb0[t]; }   // V_0 = u^i 2^-delta0
-      }
+      for (int t = 0; t < 2; ++t) { F.cwr[t] *= sb[t]; F.cwi[t] *= sb[t]; }   // V advances by w 2^-delta
+      mma_scale_b(F, sb0);                                                  // V_0 = u^i 2^-delta0
       const bool busy = __any_sync(0xffffffffu, act);
       for (int k = 0; k < nq; ++k) {
         const int st = (int)(t_seq % kHmStages);
         mbar_wait(full + st, (t_seq / kHmStages) & 1u);
         if (busy) {
           mma_chunk(F, ring[st]);
-          if (k + 1 < nq) {   // C 2^-delta before the next chunk's terms
-#pragma unroll
-            for (int t = 0; t < 2; ++t)
-#pragma unroll
-              for (int e = 0; e < 4; ++e) { F.cr[t][e] *= sc[t][e & 1]; F.ci[t][e] *= sc[t][e & 1]; }
-          }
+          if (k + 1 < nq) mma_scale_c(F, sc);   // C 2^-delta before the next chunk's terms
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + st);
