@@ -1167,7 +1167,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_horner_tiled(const void* __r
 // Without the band there is no magnitude bound inside a piece: for |z| > 1 the accumulators and the B
 // fragment are rescaled by 2^-delta per chunk, delta = floor(256 log2|z|) (exact powers of two, so only
 // underflowing -- negligible -- early terms are lost); for |z| <= 1 the terms only shrink.  Points outside
-// 2^-4 <= |z| < 2^3.99 (the range of w = z^256 and of the chunk powers u^i <= z^240), zero and
+// 2^-4 <= |z| < 2^3.99 (the range of w = z^256 and of the chunk powers u^i <= z^(256 - P)), zero and
 // non-finite points (0.8% of sphere points) are appended to a list that k_horner_tiled evaluates afterwards
 // with one point per lane (its tail is one warp streaming every coefficient: the shortest chain per
 // coefficient wins).
@@ -1219,7 +1219,7 @@ __global__ void __launch_bounds__(kHmWarps * 32, 2) k_horner_mma(const void* __r
     const long long pos = (long long)grp * 128 + 16 * w + (lane & 15);
     double x = 0.0, y = 0.0;
     if (pos < n) load_point<PK>(pts, pos, x, y);
-    // 2^-4 <= |z| < 2^3.99: z^256 (w) stays below 2^1022, the chunk powers u^i <= z^240 too
+    // 2^-4 <= |z| < 2^3.99: z^256 (w) stays below 2^1022, the chunk powers u^i <= z^(256 - P) too
     const double r2 = __fma_rn(x, x, y * y);
     const int act = (pos < n && isfinite(x) && isfinite(y) && r2 >= 0x1p-8 && r2 < 252.0) ? 1 : 0;
     if (lane < 16 && pos < n && !act) rejects[atomicAdd(ctrs + 1, 1u)] = (uint32_t)pos;

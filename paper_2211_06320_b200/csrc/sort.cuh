@@ -61,7 +61,7 @@ struct GroupDesc {
 
 // Tensor-core coverage (k_eval_mma): point (window [wl, wr] relative to k_min, z = x + iy) has piece p
 // evaluated on the FP64 tensor cores iff its window covers the whole kPiece-aligned piece and
-// 2^-3 <= max(|x|, |y|) < 2^3 (the range of the chunk powers u^i <= z^240, w = z^256).  A property of
+// 2^-3 <= max(|x|, |y|) < 2^3 (the range of the chunk powers u^i <= z^(256 - P), w = z^256).  A property of
 // the point alone, so every point's arithmetic is independent of the batch.
 __host__ __device__ __forceinline__ bool mma_covers(int wl, int wr, double x, double y, int p) {
   if (!(wl <= wr) || wl > p * kPiece || wr < p * kPiece + kPiece - 1) return false;
