@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <vector>
 #include "fpe_internal.h"
 
@@ -283,11 +284,49 @@ int32_t bit_length(long long d) {
 }
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+}  // namespace
+
+// The preconditioner's temporaries (scales, cover, G_p flags, scan sums) come from a library-private
+// stream-ordered pool that keeps its memory: cudaMalloc / cudaFree of tens of MiB per call cost more than
+// the kernels (cfg3 wall time 3-12 ms, the kernels ~2 ms).  The handle's buffer stays a plain cudaMalloc.
+static cudaMemPool_t scratch_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev] = pool;
+  }
+  return pools[dev];
+}
+static cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  cudaMemPool_t pool = scratch_pool();
+  if (!pool) return cudaMalloc(p, bytes);
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+// frees on the stream the temporaries were used on (the callers synchronise it before returning)
+static void scratch_free(void* p, cudaStream_t s) {
+  if (!p) return;
+  if (scratch_pool()) cudaFreeAsync(p, s);
+  else cudaFree(p);
+}
+
+namespace {
 struct DevBuf {
   void* p = nullptr;
-  ~DevBuf() { if (p) cudaFree(p); }
+  cudaStream_t s = nullptr;
+  ~DevBuf() { scratch_free(p, s); }
 };
-
 }  // namespace
 
 #define PRE_CUDA(x)                                                                                  \
@@ -302,10 +341,11 @@ fpe_status cover_build(const void* coeffs, int64_t n, fpe_dtype dt, cudaStream_t
   const long long nchunks_max = (n + kHullChunk - 1) / kHullChunk;
   const size_t sz_s = align256((size_t)n * 4), sz_v = align256((size_t)nchunks_max * kHullChunk * sizeof(int2));
   const size_t sz_c = align256((size_t)(nchunks_max + 1) * 4 * 2);
-  if (cudaMalloc(&cv.scales, sz_s) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc(%zu) failed", sz_s); return FPE_ERR_OOM; }
+  if (scratch_alloc(&cv.scales, sz_s, s) != cudaSuccess) { cudaGetLastError(); cv.scales = nullptr; set_error("device allocation of %zu bytes failed", sz_s); return FPE_ERR_OOM; }
   DevBuf scratch;
+  scratch.s = s;
   const size_t total = sz_v + sz_c + align256(sizeof(PreStats));
-  if (cudaMalloc(&scratch.p, total) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc(%zu) failed", total); return FPE_ERR_OOM; }
+  if (scratch_alloc(&scratch.p, total, s) != cudaSuccess) { cudaGetLastError(); scratch.p = nullptr; set_error("device allocation of %zu bytes failed", total); return FPE_ERR_OOM; }
   char* q = static_cast<char*>(scratch.p);
   int32_t* d_s = static_cast<int32_t*>(cv.scales);
   int2* d_v = reinterpret_cast<int2*>(q); q += sz_v;
@@ -343,7 +383,7 @@ fpe_status cover_build(const void* coeffs, int64_t n, fpe_dtype dt, cudaStream_t
   PRE_CUDA(cudaMemcpyAsync(&nv_i, cnt_a, sizeof(int), cudaMemcpyDeviceToHost, s));
   PRE_CUDA(cudaStreamSynchronize(s));
   cv.nv = nv_i;
-  if (cudaMalloc(&cv.hull, cv.nv * sizeof(int2)) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc failed"); return FPE_ERR_OOM; }
+  if (scratch_alloc(&cv.hull, cv.nv * sizeof(int2), s) != cudaSuccess) { cudaGetLastError(); cv.hull = nullptr; set_error("device allocation failed"); return FPE_ERR_OOM; }
   PRE_CUDA(cudaMemcpyAsync(cv.hull, d_v, cv.nv * sizeof(int2), cudaMemcpyDeviceToDevice, s));
   std::vector<int2> hv(cv.nv);
   PRE_CUDA(cudaMemcpyAsync(hv.data(), d_v, cv.nv * sizeof(int2), cudaMemcpyDeviceToHost, s));
@@ -364,8 +404,9 @@ fpe_status cover_finish(const CoverDev& cv, int32_t p_bits, int32_t drop_overrid
   const long long nblocks_scan = (d_eff + kScanBlock) / kScanBlock;
   const size_t sz_g = align256((size_t)(d_eff + 1)), sz_b = align256((size_t)(nblocks_scan + 1) * 4);
   DevBuf scratch;
+  scratch.s = s;
   const size_t total = sz_g + sz_b + align256(sizeof(PreStats));
-  if (cudaMalloc(&scratch.p, total) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc(%zu) failed", total); return FPE_ERR_OOM; }
+  if (scratch_alloc(&scratch.p, total, s) != cudaSuccess) { cudaGetLastError(); scratch.p = nullptr; set_error("device allocation of %zu bytes failed", total); return FPE_ERR_OOM; }
   char* q = static_cast<char*>(scratch.p);
   uint8_t* d_good = reinterpret_cast<uint8_t*>(q); q += sz_g;
   int* d_bsum = reinterpret_cast<int*>(q); q += sz_b;
@@ -411,8 +452,7 @@ fpe_status cover_finish(const CoverDev& cv, int32_t p_bits, int32_t drop_overrid
 
   void* buf = nullptr;
   if (cudaMalloc(&buf, off) != cudaSuccess) { cudaGetLastError(); set_error("cudaMalloc(%zu) failed", off); return FPE_ERR_OOM; }
-  DevBuf guard;
-  guard.p = buf;
+  struct BufGuard { void* p; ~BufGuard() { if (p) cudaFree(p); } } guard{buf};
   char* b = static_cast<char*>(buf);
   PRE_CUDA(cudaMemsetAsync(b, 0, off, s));
   PRE_CUDA(cudaMemcpyAsync(b, &hdr, sizeof(hdr), cudaMemcpyHostToDevice, s));
@@ -437,8 +477,10 @@ fpe_status cover_finish(const CoverDev& cv, int32_t p_bits, int32_t drop_overrid
 }
 
 void CoverDev::release() {
-  if (scales) cudaFree(scales);
-  if (hull) cudaFree(hull);
+  // pool memory; every use of it ended with a synchronisation of its stream (cover_build / cover_finish),
+  // and the caller's stream may be gone by now, so it is freed on the legacy default stream
+  scratch_free(scales, nullptr);
+  scratch_free(hull, nullptr);
   if (owned) cudaFree(owned);
   scales = hull = owned = nullptr;
 }
