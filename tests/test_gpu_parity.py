@@ -372,6 +372,34 @@ def test_sparse_many_terms(fpe):
     _values_ok(P, a, pts, out, np.arange(0, len(pts), 10), TOL64, cls)
 
 
+def test_sparse_determinism_long_lists(fpe):
+    """Sparse evaluator: points with long kept lists (K > 32: summed by the whole warp, strided partials
+    and a fixed tree) mixed with short ones (flat round-robin list, summed per lane) -- bitwise the same
+    results under a permutation of the batch and under batch slicing (a point's result must not depend
+    on its warp-mates or on the work-queue order); values against the oracle on a sample."""
+    rng = np.random.default_rng(13)
+    d = 1 << 20
+    a = np.zeros(d + 1, np.complex128)
+    idx = np.unique(np.concatenate([[0, d], rng.integers(1, d, 20000)]))
+    a[idx] = rng.uniform(-1, 1, len(idx)) + 1j * rng.uniform(-1, 1, len(idx))
+    poly = fpe.precondition(a)
+    P = oracle.OraclePoly(a)
+    near = np.exp2(rng.uniform(-0.002, 0.002, 3000)) * np.exp(1j * rng.uniform(0, 2 * np.pi, 3000))
+    pts = np.concatenate([near, workloads.points(3, 3000)])
+    pts = pts[rng.permutation(len(pts))]
+    base = gpu_eval(poly, pts)
+    K = base["diag"]["kept"]
+    assert (K > 32).sum() > 500 and (K <= 32).sum() > 500
+    perm = rng.permutation(len(pts))
+    o = gpu_eval(poly, pts[perm], diag=False)
+    assert np.array_equal(o["v"], base["v"][perm]) and np.array_equal(o["e"], base["e"][perm])
+    parts = [gpu_eval(poly, pts[i:i + 777], diag=False) for i in range(0, len(pts), 777)]
+    assert np.array_equal(np.concatenate([q["v"] for q in parts]), base["v"])
+    assert np.array_equal(np.concatenate([q["e"] for q in parts]), base["e"])
+    cls = check_indexing(P, pts, base["diag"])
+    _values_ok(P, a, pts, base, np.arange(0, len(pts), 12), TOL64, cls)
+
+
 # ------------------------------------------------- device preconditioner ----
 def _gpu_buffer(fpe, a):
     t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
