@@ -1,15 +1,15 @@
 // eval_tiled.cu -- the bucketed, shared-memory-tiled window evaluator (north star subsystems 2-4).
 //
 // Pipeline (all on the caller's stream, no host round trip):
+//   k_bucket_hist    per-CTA histogram of a 23-bit key monotone in an fp64 estimate of lambda, slice claims;
+//                    k_bucket_scan: bucket starts (sort.cu).
 //   k_classify_bucket lines 5-8 of FPE_p per point (lambda = RN(log2|z|) via lambda_fast, k_lambda,
-//                    [l, r]; device_common.cuh) and a 24-bit key: bit 23 = "long window"
-//                    (r - l + 1 > kLongWin), bits 0..22 monotone in lambda; per-CTA coarse-bucket
-//                    histogram and slice claims (sort.cu).  l and r are both non-decreasing in lambda
-//                    (d/dlambda of cover(k) + lambda k - N is k - k_lambda), so points with close keys
-//                    have nested, nearly equal windows.
-//   bucket scan/scatter + k_plan (sort.cu): records and points in the order of the top 15 key bits,
-//                    cut into groups of 32*NP consecutive points; per group the union window and the work
-//                    items (one whole group, or one item per kPiece-aligned piece of a long window).
+//                    [l, r]; device_common.cuh) and the point's record written to its bucket position.
+//                    l and r are both non-decreasing in lambda (d/dlambda of cover(k) + lambda k - N is
+//                    k - k_lambda), so points with close keys have nested, nearly equal windows.
+//   k_plan (sort.cu) the bucket order cut into groups of 32*NP consecutive points; per group the union
+//                    window and the work items (one whole group, or one item per kPiece-aligned piece of a
+//                    long window).
 //   k_eval_tiled     persistent warps: first the parallel pieces, then every other group in order.  A warp streams the coefficients of its item's range through a
 //                    private 3-stage shared-memory ring filled by 1-D TMA bulk copies (cp.async.bulk +
 //                    mbarrier complete_tx), reads them as warp-uniform broadcasts (one LDS per
@@ -39,33 +39,76 @@ constexpr int kWarps = 4;      // warps per CTA of k_eval_tiled
 constexpr int kStages = 3;     // TMA ring depth per warp
 
 // ------------------------------------------------------------------------------------------------
-// classification + sort key + first radix upsweep
-__device__ __forceinline__ uint32_t lambda_key(double lam, int l, int r) {
-  // |lambda| = (1.m) 2^E: mag = (E + 53) << 16 | top 16 bits of m (monotone in |lambda| >= 2^-52)
-  uint32_t longw = (r - l + 1 > kLongWin) ? 1u : 0u;
-  uint32_t u;
-  if (!(lam == lam) || lam == -INFINITY) {
-    u = 0;
-  } else {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(lam));
-    const int E = (int)(b >> 52) - 1023;
-    uint32_t mag = 0;
-    if (E >= -52) mag = ((uint32_t)(E + 53) << 16) | (uint32_t)((b >> 36) & 0xffff);
-    u = (lam >= 0.0) ? (1u << 22) + mag : (1u << 22) - 1u - mag;
+// Work bucketing (the sort key) and classification, which writes every point's record straight to its
+// bucket position.
+//
+// The key only decides which points share a warp: every point's arithmetic depends on its own window alone,
+// so any deterministic function of z gives bitwise the same results.  It is the bits of an fp64 estimate of
+// log2|z| (lambda_enclosure's midpoint, within 2^-50 + 2^-53 |lambda| of lambda): |lambda| = (1.m) 2^E gives
+// mag = (E + 53) << 16 | the top 16 bits of m, monotone in |lambda| >= 2^-52, and the sign of lambda on
+// top -- 23 bits, monotone in |z|.  l and r are non-decreasing in lambda (d/dlambda of cover(k) + lambda k - N
+// is k - k_lambda), so points with close keys have nested, nearly equal windows.  z = 0 and non-finite z
+// take key 0.  k_bucket_hist and k_classify_bucket both call this one function on the same points.
+__device__ __forceinline__ uint32_t bucket_key(double x, double y, bool cplx) {
+  if (!(isfinite(x) && isfinite(y)) || (x == 0.0 && (!cplx || y == 0.0))) return 0u;
+  double lo, hi, lam;
+  lambda_enclosure(x, y, cplx, lo, hi, lam);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(lam));
+  const int E = (int)(b >> 52) - 1023;
+  uint32_t mag = 0;
+  if (E >= -52) mag = ((uint32_t)(E + 53) << 16) | (uint32_t)((b >> 36) & 0xffff);
+  return (lam >= 0.0) ? (1u << 22) + mag : (1u << 22) - 1u - mag;
+}
+constexpr int kKeyBits = 23;
+
+// Pass 1 of the counting sort: per classify CTA (the same contiguous range of points k_classify_bucket
+// gives it), a shared-memory histogram of the top coarse_bits(n) key bits, then one global atomicAdd per
+// nonzero bucket claims the CTA's slice of that bucket.  A streaming pass over the points (16 B each for
+// complex fp64), no classification.
+template <int PK>
+__global__ void __launch_bounds__(kScatterThreads) k_bucket_hist(const void* __restrict__ pts, long long n,
+                                                                 long long ppc, uint32_t* __restrict__ gcount,
+                                                                 uint32_t* __restrict__ cta_base) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(s_dyn);
+  const int cb = coarse_bits(n), nbk = 1 << cb;
+  for (int b = threadIdx.x; b < nbk; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  const long long beg = (long long)blockIdx.x * ppc, end = min(n, beg + ppc);
+  constexpr int U = 4;   // independent point loads in flight per thread
+  for (long long i0 = beg + threadIdx.x; i0 < end; i0 += U * blockDim.x) {
+    double x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + (long long)u * blockDim.x;
+      x[u] = 0.0; y[u] = 0.0;
+      if (i < end) load_point<PK>(pts, i, x[u], y[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + (long long)u * blockDim.x < end)
+        atomicAdd(&hist[bucket_key(x[u], y[u], PtTraits<PK>::cplx) >> (kKeyBits - cb)], 1u);
   }
-  return (longw << 23) | u;
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbk; b += blockDim.x) {
+    const uint32_t c = hist[b];
+    cta_base[((size_t)blockIdx.x << cb) + b] = c ? atomicAdd(gcount + b, c) : 0u;
+  }
 }
 
+// Pass 2: lines 5-8 of FPE_p per point (lambda, k_lambda, [l, r]; device_common.cuh) and the point's record
+// {index, key, l, r, z} written to its bucket position: bucket start + this CTA's slice (k_bucket_hist,
+// k_bucket_scan) + a shared-memory counter.  The order inside a (CTA, bucket) slice is unspecified.
 template <int PK>
 __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void* __restrict__ pts, long long n,
                                                                      long long ppc, PolyDev P,
-                                                         int2* __restrict__ lr, uint32_t* __restrict__ keys,
-                                                         uint32_t* __restrict__ gcount,
-                                                         uint32_t* __restrict__ cta_base,
-                                                         fpe_diag* __restrict__ diag,
-                                                         unsigned long long* __restrict__ hard_ctr) {
+                                                                     const uint32_t* __restrict__ bstart,
+                                                                     const uint32_t* __restrict__ cta_base,
+                                                                     PtRec* __restrict__ rec,
+                                                                     fpe_diag* __restrict__ diag,
+                                                                     unsigned long long* __restrict__ hard_ctr) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  uint32_t* hist = reinterpret_cast<uint32_t*>(s_dyn);   // kBuckets counters, then the staged cover
+  uint32_t* slot = reinterpret_cast<uint32_t*>(s_dyn);   // next position of every bucket's slice, then the cover
   const int2* hull = P.hull;
   double2* hv = reinterpret_cast<double2*>(s_dyn + kBuckets * sizeof(uint32_t));
   const bool staged = P.nv <= kSmemHullDbl;
@@ -79,61 +122,51 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
     hull = sh;
   }
   const int cb = coarse_bits(n), nbk = 1 << cb;
-  for (int b = threadIdx.x; b < nbk; b += blockDim.x) hist[b] = 0;
+  for (int b = threadIdx.x; b < nbk; b += blockDim.x) slot[b] = __ldg(bstart + b) + __ldg(cta_base + ((size_t)blockIdx.x << cb) + b);
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   const long long beg = (long long)blockIdx.x * ppc, end = min(n, beg + ppc);
   double xn = 0.0, yn = 0.0;   // the next iteration's point, loaded one iteration ahead
   if (beg + threadIdx.x < end) load_point<PK>(pts, beg + threadIdx.x, xn, yn);
-  for (long long i0 = beg + threadIdx.x; i0 - lane < end; i0 += blockDim.x) {
-    const long long i = i0;
-    const bool ok = i < end;
-    uint32_t key = 0xffffffffu;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     const double x = xn, y = yn;
-    if (i0 + blockDim.x < end) load_point<PK>(pts, i0 + blockDim.x, xn, yn);
-    if (ok) {
-      int hard = 0;
-      double lam = 0.0;
-      int istar, l, r;
-      bool done = false;
-      if (staged && P.dbl_ok && isfinite(x) && isfinite(y) && (x != 0.0 || (PtTraits<PK>::cplx && y != 0.0))) {
-        // fast path: searches on an enclosure of log2|z|; only undecided points compute the rounded lambda
-        // (the diagnostics still report the rounded lambda, so the tests check this path's indexing)
-        double lo, hi;
-        lambda_enclosure(x, y, PtTraits<PK>::cplx, lo, hi, lam);
-        bool amb = false;
-        classify_lambda_vp(hull, hv, P.nv, P.drop, LamIv{lo, hi, &amb}, istar, l, r);
-        done = !amb;
-        if (done && diag) lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
-      }
-      if (!done) {
-        lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
-        if (staged && P.dbl_ok) classify_lambda_v<true>(hull, hv, P.nv, P.drop, lam, istar, l, r);
-        else if (staged) classify_lambda_v<false>(hull, hv, P.nv, P.drop, lam, istar, l, r);
-        else classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
-      }
-      lr[i] = make_int2(l, r);
-      key = lambda_key(lam, l, r);
-      keys[2 * i] = key;
-      if (diag) {
-        fpe_diag dg;
-        dg.lambda = lam; dg.region = istar; dg.l = l; dg.r = r;
-        dg.kept = kept_count(P, l, r); dg.hard = hard; dg.cancel = INT32_MIN; dg.trusted = 0;
-        dg.err_exp = INT32_MIN; dg.pad = 0;
-        diag[i] = dg;
-      }
-      if (hard) atomicAdd(hard_ctr, 1ull);
+    if (i + blockDim.x < end) load_point<PK>(pts, i + blockDim.x, xn, yn);
+    int hard = 0;
+    double lam = 0.0;
+    int istar, l, r;
+    bool done = false;
+    if (staged && P.dbl_ok && isfinite(x) && isfinite(y) && (x != 0.0 || (PtTraits<PK>::cplx && y != 0.0))) {
+      // fast path: searches on an enclosure of log2|z|; only undecided points compute the rounded lambda
+      // (the diagnostics still report the rounded lambda, so the tests check this path's indexing)
+      double lo, hi;
+      lambda_enclosure(x, y, PtTraits<PK>::cplx, lo, hi, lam);
+      bool amb = false;
+      classify_lambda_vp(hull, hv, P.nv, P.drop, LamIv{lo, hi, &amb}, istar, l, r);
+      done = !amb;
+      if (done && diag) lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
     }
-    // every point keeps its rank inside its (CTA, bucket) slice, so the scatter needs no atomics (one
-    // shared-memory atomic per point: buckets rarely repeat within a warp, and warp-aggregating them
-    // with __match_any_sync cost more than it saved -- 1.70 vs 1.59 ms)
-    if (ok) keys[2 * i + 1] = atomicAdd(&hist[key >> (24 - cb)], 1u);
-  }
-  __syncthreads();
-  // claim this CTA's slice of every bucket
-  for (int b = threadIdx.x; b < nbk; b += blockDim.x) {
-    const uint32_t c = hist[b];
-    cta_base[((size_t)blockIdx.x << cb) + b] = c ? atomicAdd(gcount + b, c) : 0u;
+    if (!done) {
+      lam = lambda_fast(x, y, PtTraits<PK>::cplx, &hard);
+      if (staged && P.dbl_ok) classify_lambda_v<true>(hull, hv, P.nv, P.drop, lam, istar, l, r);
+      else if (staged) classify_lambda_v<false>(hull, hv, P.nv, P.drop, lam, istar, l, r);
+      else classify_lambda(hull, P.nv, P.drop, lam, istar, l, r);
+    }
+    if (diag) {
+      fpe_diag dg;
+      dg.lambda = lam; dg.region = istar; dg.l = l; dg.r = r;
+      dg.kept = kept_count(P, l, r); dg.hard = hard; dg.cancel = INT32_MIN; dg.trusted = 0;
+      dg.err_exp = INT32_MIN; dg.pad = 0;
+      diag[i] = dg;
+    }
+    if (hard) atomicAdd(hard_ctr, 1ull);
+    const uint32_t key = bucket_key(x, y, PtTraits<PK>::cplx);
+    // one shared-memory atomic per point (buckets rarely repeat within a warp)
+    const uint32_t pos = atomicAdd(&slot[key >> (kKeyBits - cb)], 1u);
+    // one 256-bit store (STG.E.ENL2.256): the record's whole 32-byte sector in one request
+    const unsigned long long zx = __double_as_longlong(x), zy = __double_as_longlong(y);
+    asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(rec + pos), "r"((uint32_t)i),
+                 "r"(key), "r"((uint32_t)l), "r"((uint32_t)r), "r"((uint32_t)zx), "r"((uint32_t)(zx >> 32)),
+                 "r"((uint32_t)zy), "r"((uint32_t)(zy >> 32))
+                 : "memory");
   }
 }
 
@@ -486,20 +519,22 @@ __device__ __noinline__ void acc_fold(Acc& A, double hr, double hi, int pbase, d
 // nothing accumulated) -- and k_unsort applies the epilogue Q = acc z^n (finalize) on the way to the caller's
 // order: the polar-route power is fp64 work that would compete with the Horner DFMAs for the fp64 pipe here,
 // while k_unsort is bound by its random gathers and has the issue slots to spare.
+// The staged accumulators are written at random (the point's input index) and read once, by k_unsort: an L2
+// evict-first policy keeps them from displacing the coefficients the evaluator warps re-read from L2.
 __device__ __forceinline__ void stage_acc(PtOut* out, long long pos, const Acc& A, long long extraE, int kmin) {
   const unsigned long long a = __double_as_longlong(A.started ? A.r : 0.0), b = __double_as_longlong(A.started ? A.i : 0.0);
   const unsigned long long e = (unsigned long long)extraE;
   const unsigned long long nn = (unsigned long long)(A.started ? (long long)A.base + kmin : -1ll);
-  asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(out + pos), "r"((uint32_t)a),
-               "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)), "r"((uint32_t)e),
-               "r"((uint32_t)(e >> 32)), "r"((uint32_t)nn), "r"((uint32_t)(nn >> 32))
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(out + pos),
+               "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)),
+               "r"((uint32_t)e), "r"((uint32_t)(e >> 32)), "r"((uint32_t)nn), "r"((uint32_t)(nn >> 32)), "l"(pol)
                : "memory");
 }
 
 
-// Q = acc z^l as (re + i im) 2^E; the caller stages it (evaluator: over the point's record, in bucket
-// order -- every warp that reads the record has done so before the last piece is folded) or stores it
-// (full Horner).
+// Q = acc z^l as (re + i im) 2^E (finalize: k_unsort, and the full Horner's direct stores).
 struct Fin {
   double re, im;
   long long E;
@@ -562,7 +597,7 @@ __device__ __noinline__ Fin finalize(double x, double y, Acc A, const PolyDev& P
 // The NP points of each lane of a group: sorted position j*32 + lane.
 template <int NP>
 struct Pts {
-  long long idx[NP];   // sorted position
+  long long idx[NP];   // input index (the caller's order): where the accumulator is staged
   double x[NP], y[NP];
   int wl[NP], wr[NP];   // relative window; empty (wl > wr) for padding and non-finite points
   bool valid[NP];
@@ -582,7 +617,7 @@ __device__ __forceinline__ void load_group(Pts<NP>& S, uint32_t g, long long n, 
     if (S.valid[j]) {
       const int4 h = __ldcg(reinterpret_cast<const int4*>(rec + pos));
       const double2 z = __ldcg(reinterpret_cast<const double2*>(rec + pos) + 1);
-      S.idx[j] = pos; S.x[j] = z.x; S.y[j] = z.y;
+      S.idx[j] = (uint32_t)h.x; S.x[j] = z.x; S.y[j] = z.y;
       if (h.w >= h.z) { S.wl[j] = h.z - kmin; S.wr[j] = h.w - kmin; }
     }
   }
@@ -690,7 +725,7 @@ __device__ __forceinline__ void group_unpack(Pts<NP>& S, const GroupCtx<NP>& c, 
     S.valid[j] = pos < n;
     S.idx[j] = 0; S.x[j] = 0.0; S.y[j] = 0.0; S.wl[j] = 0x3fffffff; S.wr[j] = -1;
     if (S.valid[j]) {
-      S.idx[j] = pos;
+      S.idx[j] = (uint32_t)c.h[j].x;
       S.x[j] = c.z[j].x; S.y[j] = c.z[j].y;
       if (c.h[j].w >= c.h[j].z) { S.wl[j] = c.h[j].z - kmin; S.wr[j] = c.h[j].w - kmin; }
     }
@@ -810,7 +845,7 @@ template <int PK, int CK, int OK, int NP>
 #define FPE_EVAL_MIN_CTAS 3   // CTAs per SM the register budget is sized for (12 warps)
 #endif
 __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(long long n, PolyDev P,
-                                                               PtRec* rec, Plan plan) {
+                                                               const PtRec* rec, Plan plan, PtOut* out) {
   using CT = typename Step<CK>::CT;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -822,7 +857,6 @@ __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(l
   }
   __syncwarp();
   Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0, -1};
-  PtOut* const out = reinterpret_cast<PtOut*>(rec);   // results overwrite the records (bucket order)
   const uint32_t n_multi = min(plan.ctrs[2], plan.cap);
   // the next item index is fetched one item ahead, so the atomic's latency hides behind the work
   uint32_t nxt = 0;
@@ -870,7 +904,8 @@ __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(l
 // k_eval_mma's arithmetic (eval_piece<INWARP>) -- so these points get the bits they would get in any batch.
 // Launched after k_eval_tiled whenever tensor-core items are planned; exits at once when the list is empty.
 template <int PK, int CK, int OK, int NP>
-__global__ void __launch_bounds__(kWarps * 32) k_eval_overflow(long long n, PolyDev P, PtRec* rec, Plan plan) {
+__global__ void __launch_bounds__(kWarps * 32) k_eval_overflow(long long n, PolyDev P, const PtRec* rec, Plan plan,
+                                                               PtOut* out) {
   using CT = typename Step<CK>::CT;
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t n_ovf = plan.mma_ctrs[2];
@@ -884,7 +919,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_eval_overflow(long long n, Poly
   }
   __syncwarp();
   Ring<CK> R{ring_buf, bars, static_cast<const CT*>(P.coef), 0u, 0u, 0, 0, -1};
-  PtOut* const out = reinterpret_cast<PtOut*>(rec);
   const int kmin = (int)P.k_min;
   for (;;) {
     uint32_t it = 0;
@@ -972,9 +1006,8 @@ __device__ __noinline__ void xacc_fold(XAcc& A, double hr, double hi, long long 
 }
 
 template <int PK, int CK, int OK>
-__global__ void __launch_bounds__(256) k_eval_wide(long long n, PolyDev P, PtRec* rec) {
+__global__ void __launch_bounds__(256) k_eval_wide(long long n, PolyDev P, const PtRec* rec, PtOut* out) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
-  PtOut* const out = reinterpret_cast<PtOut*>(rec);
   const int kmin = (int)P.k_min;
   for (long long pos = blockIdx.x * (long long)blockDim.x + threadIdx.x; pos < n; pos += (long long)gridDim.x * blockDim.x) {
     const int4 h = __ldcg(reinterpret_cast<const int4*>(rec + pos));
@@ -999,7 +1032,7 @@ __global__ void __launch_bounds__(256) k_eval_wide(long long n, PolyDev P, PtRec
       A = XAcc{cr, ci, 0, 0, true};
     }
     const Acc a{A.r, A.i, A.base, A.started};
-    stage_acc(out, pos, a, A.started ? A.E : 0, kmin);
+    stage_acc(out, (uint32_t)h.x, a, A.started ? A.E : 0, kmin);
   }
 }
 
@@ -1278,11 +1311,12 @@ __global__ void __launch_bounds__(kHmWarps * 32, 2) k_horner_mma(const void* __r
 }
 
 // ------------------------------------------------------------------------------------------------
-// Results from bucket order to the caller's order: a coalesced pass over the caller's indices gathering one
-// 32-byte staged result each (a random sector read instead of the evaluator's random partial-sector
-// writes, which the DRAM turns into read-modify-writes).
+// The epilogue in the caller's order: the evaluators staged every point's accumulator at its input index
+// (one whole 32-byte sector per point, written at random from the bucket order -- whole sectors need no
+// read-modify-write, unlike the 16-byte values and 8-byte exponents themselves), so this is a coalesced
+// pass over the staged accumulators and the points.
 #ifndef FPE_UNSORT_U
-#define FPE_UNSORT_U 2      // independent gathers in flight per thread
+#define FPE_UNSORT_U 2      // independent loads in flight per thread
 #endif
 #ifndef FPE_UNSORT_MINB
 #define FPE_UNSORT_MINB 3   // CTAs per SM the register budget is sized for (2 x 3: 2.27 -> 2.02 ms at cfg3)
@@ -1296,7 +1330,7 @@ constexpr int kUnsortWarps = 8;
 constexpr int kUnsortQ = 32 + 32 * FPE_UNSORT_U;   // queue entries per warp: < 32 left over + one iteration
 
 template <int PK, int OK>
-__global__ void __launch_bounds__(32 * kUnsortWarps, FPE_UNSORT_MINB) k_unsort(const PtOut* __restrict__ staged, const uint32_t* __restrict__ spos,
+__global__ void __launch_bounds__(32 * kUnsortWarps, FPE_UNSORT_MINB) k_unsort(const PtOut* __restrict__ staged,
                                                 long long n, const void* __restrict__ pts, PolyDev P,
                                                 void* __restrict__ vals, long long* __restrict__ exps) {
   constexpr bool CPLX = PtTraits<OK>::cplx;
@@ -1324,7 +1358,7 @@ __global__ void __launch_bounds__(32 * kUnsortWarps, FPE_UNSORT_MINB) k_unsort(c
         uint32_t w[8];
         asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
-                     : "l"(staged + __ldg(spos + i)));
+                     : "l"(staged + i));
         re[u] = __hiloint2double((int)w[1], (int)w[0]);
         im[u] = __hiloint2double((int)w[3], (int)w[2]);
         E[u] = (long long)(((unsigned long long)w[5] << 32) | w[4]);
@@ -1383,7 +1417,7 @@ static size_t scratch_slots(long long n) {
 static size_t mma_cap(long long n) { return max((size_t)64, (size_t)n * 4 / (128 * sizeof(double2))); }
 
 size_t tiled_ws_bytes(long long n) {
-  return al256(n * sizeof(int2)) + al256(n * sizeof(uint2)) + al256(n * sizeof(PtRec)) + al256(n * 4) +
+  return al256(n * sizeof(PtOut)) + al256(n * sizeof(PtRec)) +
          al256(mma_cap(n) * sizeof(uint2)) + al256(mma_cap(n) * 128 * sizeof(double2)) +
          al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) +
          al256(max_groups(n) * sizeof(GroupDesc)) + 2 * al256(max_groups(n) * sizeof(uint32_t)) +
@@ -1396,25 +1430,27 @@ static size_t eval_smem() {
 }
 
 template <int PK, int CK, int OK, int NP>
-static int launch_eval_tiled_t(long long n, const PolyDev& P, PtRec* rec, const Plan& plan, cudaStream_t s) {
+static int launch_eval_tiled_t(long long n, const PolyDev& P, const PtRec* rec, const Plan& plan, PtOut* out,
+                               cudaStream_t s) {
   const size_t smem = eval_smem<CK>();
   const int grid = persistent_grid(reinterpret_cast<const void*>(k_eval_tiled<PK, CK, OK, NP>), kWarps * 32, smem);
-  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(n, P, rec, plan);
+  k_eval_tiled<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(n, P, rec, plan, out);
   return 1;
 }
 
 template <int PK, int CK, int OK>
-static int launch_eval_wide_t(long long n, const PolyDev& P, PtRec* rec, cudaStream_t s) {
+static int launch_eval_wide_t(long long n, const PolyDev& P, const PtRec* rec, PtOut* out, cudaStream_t s) {
   const long long blocks = std::min<long long>((n + 255) / 256, 148ll * 16);
-  k_eval_wide<PK, CK, OK><<<(int)std::max(1ll, blocks), 256, 0, s>>>(n, P, rec);
+  k_eval_wide<PK, CK, OK><<<(int)std::max(1ll, blocks), 256, 0, s>>>(n, P, rec, out);
   return 1;
 }
 
 template <int PK, int CK, int OK, int NP>
-static int launch_eval_overflow_t(long long n, const PolyDev& P, PtRec* rec, const Plan& plan, cudaStream_t s) {
+static int launch_eval_overflow_t(long long n, const PolyDev& P, const PtRec* rec, const Plan& plan, PtOut* out,
+                                  cudaStream_t s) {
   const size_t smem = eval_smem<CK>();
   const int grid = persistent_grid(reinterpret_cast<const void*>(k_eval_overflow<PK, CK, OK, NP>), kWarps * 32, smem);
-  k_eval_overflow<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(n, P, rec, plan);
+  k_eval_overflow<PK, CK, OK, NP><<<grid, kWarps * 32, smem, s>>>(n, P, rec, plan, out);
   return 1;
 }
 
@@ -1445,15 +1481,21 @@ static int np_for(int pk, int cdt, long long d_eff) {
   return (pk == FPE_R64) ? FPE_NP_REAL : 2;
 }
 
+// histogram + slice claims (k_bucket_hist), bucket starts (k_bucket_scan), classification + records at their
+// bucket positions (k_classify_bucket)
 template <int PK>
-static void launch_classify_bucket_t(const void* pts, long long n, const PolyDev& P, int2* lr, uint32_t* keys,
-                                     uint32_t* gcount, uint32_t* cta_base, fpe_diag* diag, unsigned long long* hard,
-                                     cudaStream_t s) {
+static void launch_classify_bucket_t(const void* pts, long long n, const PolyDev& P, uint32_t* gcount,
+                                     uint32_t* cta_base, uint32_t* bstart, PtRec* rec, fpe_diag* diag,
+                                     unsigned long long* hard, Stage& st, cudaStream_t s) {
+  const size_t hsmem = kBuckets * sizeof(uint32_t);
+  cudaFuncSetAttribute(k_bucket_hist<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+  k_bucket_hist<PK><<<(int)n_ctas(n), kScatterThreads, hsmem, s>>>(pts, n, pts_per_cta(n), gcount, cta_base);
+  bucket_scan(gcount, bstart, n, s);
+  st.mark("bucket");
   const size_t smem = kBuckets * sizeof(uint32_t) + (P.nv <= kSmemHullDbl ? P.nv * (sizeof(int2) + sizeof(double2)) : 0);
   cudaFuncSetAttribute(k_classify_bucket<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_classify_bucket<PK><<<(int)n_ctas(n), kScatterThreads, smem, s>>>(pts, n, pts_per_cta(n), P, lr, keys, gcount,
-                                                                     cta_base,
-                                                          diag, hard);
+  k_classify_bucket<PK><<<(int)n_ctas(n), kScatterThreads, smem, s>>>(pts, n, pts_per_cta(n), P, bstart, cta_base,
+                                                                     rec, diag, hard);
 }
 
 template <int PK, int CK>
@@ -1506,10 +1548,10 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
               fpe_diag* diag, void* ws, unsigned long long* stats, Stage& st, cudaStream_t s) {
   unsigned long long* hard = stats + kStatHard;
   char* p = static_cast<char*>(ws);
-  int2* lr = reinterpret_cast<int2*>(p); p += al256(n * sizeof(int2));          // {l, r} of input point i
-  uint32_t* keys = reinterpret_cast<uint32_t*>(p); p += al256(n * 8);            // {key, rank in (CTA, bucket)}
-  PtRec* rec = reinterpret_cast<PtRec*>(p); p += al256(n * sizeof(PtRec));   // later: the results (PtOut)
-  uint32_t* spos = reinterpret_cast<uint32_t*>(p); p += al256(n * 4);          // bucket position of point i
+  // the evaluators' accumulators staged at the point's input index (random whole-sector writes from the
+  // bucket order, so that k_unsort streams them back in order)
+  PtOut* staged = reinterpret_cast<PtOut*>(p); p += al256(n * sizeof(PtOut));
+  PtRec* rec = reinterpret_cast<PtRec*>(p); p += al256(n * sizeof(PtRec));   // bucket order
   uint32_t* cta_base = reinterpret_cast<uint32_t*>(p); p += al256(n_ctas(n) * kBuckets * 4);
   uint32_t* gcount = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   uint32_t* bstart = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
@@ -1535,15 +1577,14 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   cudaMemsetAsync(gcount, 0, (kBuckets + 1) * 4, s);
   cudaMemsetAsync(plan.ctrs, 0, 32, s);   // [0..3] vector items / groups / slots, [4..5] DMMA items
   switch (pk) {
-    case FPE_R64: launch_classify_bucket_t<FPE_R64>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
-    case FPE_C64: launch_classify_bucket_t<FPE_C64>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
-    case FPE_R32: launch_classify_bucket_t<FPE_R32>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
-    default: launch_classify_bucket_t<FPE_C32>(pts, n, P, lr, keys, gcount, cta_base, diag, hard, s); break;
+    case FPE_R64: launch_classify_bucket_t<FPE_R64>(pts, n, P, gcount, cta_base, bstart, rec, diag, hard, st, s); break;
+    case FPE_C64: launch_classify_bucket_t<FPE_C64>(pts, n, P, gcount, cta_base, bstart, rec, diag, hard, st, s); break;
+    case FPE_R32: launch_classify_bucket_t<FPE_R32>(pts, n, P, gcount, cta_base, bstart, rec, diag, hard, st, s); break;
+    default: launch_classify_bucket_t<FPE_C32>(pts, n, P, gcount, cta_base, bstart, rec, diag, hard, st, s); break;
   }
   st.mark("classify");
-  bucket_finish(reinterpret_cast<const uint2*>(keys), lr, n, pts_per_cta(n), gcount, cta_base, bstart, rec, spos, pk,
-                pts, P.k_min, plan, s);
-  st.mark("bucket");
+  plan_groups(n, rec, P.k_min, plan, s);
+  st.mark("plan");
   int lm = 0;
   if (plan.mma_on) {
     launch_eval_mma(n, P, rec, plan, s);
@@ -1552,8 +1593,8 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   }
   int le = 0;
 #define FPE_EV(PKV, CKV, NPV)                                                                             \
-  le = P.wide ? launch_eval_wide_t<PKV, CKV, NPFor<PKV, CKV>::OK>(n, P, rec, s)                              \
-              : launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPV>(n, P, rec, plan, s)
+  le = P.wide ? launch_eval_wide_t<PKV, CKV, NPFor<PKV, CKV>::OK>(n, P, rec, staged, s)                      \
+              : launch_eval_tiled_t<PKV, CKV, NPFor<PKV, CKV>::OK, NPV>(n, P, rec, plan, staged, s)
   switch (pk * 4 + P.cdt) {
     case FPE_R64 * 4 + FPE_R64: FPE_EV(FPE_R64, FPE_R64, FPE_NP_REAL); break;
     case FPE_R64 * 4 + FPE_C64: if (np == 4) FPE_EV(FPE_R64, FPE_C64, 4); else FPE_EV(FPE_R64, FPE_C64, 2); break;
@@ -1568,13 +1609,12 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
 #undef FPE_EV
   st.mark(P.wide ? "eval_wide" : "eval_tiled");
   if (plan.mma_on) {   // groups whose tensor-core items overflowed the DMMA scratch (usually none)
-    if (pk == FPE_C64) le += launch_eval_overflow_t<FPE_C64, FPE_C64, NPFor<FPE_C64, FPE_C64>::OK, 4>(n, P, rec, plan, s);
-    else le += launch_eval_overflow_t<FPE_R64, FPE_C64, NPFor<FPE_R64, FPE_C64>::OK, 4>(n, P, rec, plan, s);
+    if (pk == FPE_C64) le += launch_eval_overflow_t<FPE_C64, FPE_C64, NPFor<FPE_C64, FPE_C64>::OK, 4>(n, P, rec, plan, staged, s);
+    else le += launch_eval_overflow_t<FPE_R64, FPE_C64, NPFor<FPE_R64, FPE_C64>::OK, 4>(n, P, rec, plan, staged, s);
     st.mark("eval_overflow");
   }
   const long long blocks = std::min<long long>((n + 4 * 256 - 1) / (4 * 256), 148ll * 16);
-  const PtOut* staged = reinterpret_cast<const PtOut*>(rec);
-#define FPE_UN(PKV, OKV) k_unsort<PKV, OKV><<<(int)blocks, 256, 0, s>>>(staged, spos, n, pts, P, vals, exps)
+#define FPE_UN(PKV, OKV) k_unsort<PKV, OKV><<<(int)blocks, 256, 0, s>>>(staged, n, pts, P, vals, exps)
   switch (pk * 4 + P.cdt) {   // the output kind follows NPFor<PK, CK>::OK
     case FPE_R64 * 4 + FPE_R64: FPE_UN(FPE_R64, FPE_R64); break;
     case FPE_R64 * 4 + FPE_C64: FPE_UN(FPE_R64, FPE_C64); break;

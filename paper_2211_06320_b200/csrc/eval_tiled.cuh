@@ -10,7 +10,6 @@
 
 namespace fpe {
 constexpr int kChunk = kCoefPad;   // coefficients per TMA bulk copy / ring stage (dense array padded to this)
-constexpr int kLongWin = 4096;     // windows longer than this sort into the "long" half of the key space
 
 size_t tiled_ws_bytes(long long n);
 // classify + sort + plan + evaluate (dense handles); stats: the call's kStat* counters (device).  Returns

@@ -1,14 +1,14 @@
 // sort.cu -- work bucketing (north star subsystem 3).
 //
-// Points carry a 24-bit key that is monotone in lambda (bits 0..22) with bit 23 = "long window";
-// l and r are both non-decreasing in lambda, so points with close keys have nested, nearly equal windows.
-// One counting-sort pass by the top coarse_bits(n) of the key (32768 buckets from 2^20 points up): k_classify_bucket
-// (eval_tiled.cu) builds a per-CTA histogram in shared memory, claims each CTA's slice of every bucket with
-// one global atomicAdd per nonzero bin and keeps every point's rank in its slice; k_bucket_scan turns
-// bucket totals into starts; k_bucket_scatter moves the records {index, key, l, r} and the points to
-// their bucket positions; k_plan cuts the bucket order into groups of 32*NP points and plans their
-// work items.  Order inside a (CTA, bucket) slice is unspecified; every point's arithmetic depends only
-// on its own window, so results do not depend on it (bitwise).
+// Points carry a 23-bit key that is monotone in an fp64 estimate of lambda (eval_tiled.cu bucket_key); l and
+// r are both non-decreasing in lambda, so points with close keys have nested, nearly equal windows.  One
+// counting sort by the top coarse_bits(n) key bits (32768 buckets from 2^20 points up): k_bucket_hist
+// (eval_tiled.cu) builds a per-CTA histogram in shared memory and claims each CTA's slice of every bucket
+// with one global atomicAdd per nonzero bin; k_bucket_scan turns bucket totals into starts;
+// k_classify_bucket (eval_tiled.cu) classifies the same points and writes every record {index, key, l, r, z}
+// to bucket start + its CTA's slice + a shared-memory counter; k_plan cuts the bucket order into groups of
+// 32*NP points and plans their work items.  Order inside a (CTA, bucket) slice is unspecified; every point's
+// arithmetic depends only on its own window, so results do not depend on it (bitwise).
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
@@ -45,59 +45,6 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(const uint32_t* __restrict
   uint32_t run = (wid ? ws[wid - 1] : 0) + x - s;
 #pragma unroll
   for (int j = 0; j < kPer; ++j) if (j < per) { bstart[t * per + j] = run; run += c[j]; }
-}
-
-__device__ __forceinline__ double2 load_point_any(int pk, const void* __restrict__ p, long long i) {
-  switch (pk) {
-    case FPE_R64: return make_double2(__ldg(static_cast<const double*>(p) + i), 0.0);
-    case FPE_C64: return __ldg(static_cast<const double2*>(p) + i);
-    case FPE_R32: return make_double2((double)__ldg(static_cast<const float*>(p) + i), 0.0);
-    default: { const float2 v = __ldg(static_cast<const float2*>(p) + i); return make_double2(v.x, v.y); }
-  }
-}
-
-// Records and points to bucket positions: bucket start + the classifying CTA's slice of the bucket + the
-// point's rank in that slice (both from the classifier) -- a pure streaming pass over all points, no
-// atomics.  The points are copied along (as doubles), so the evaluator reads everything coalesced.
-#ifndef FPE_SCATTER_U
-#define FPE_SCATTER_U 4
-#endif
-#ifndef FPE_SCATTER_MINB
-#define FPE_SCATTER_MINB 1
-#endif
-__global__ void __launch_bounds__(256, FPE_SCATTER_MINB) k_bucket_scatter(const uint2* __restrict__ keys, const int2* __restrict__ lr,
-                                                        int pk, const void* __restrict__ pts, long long n,
-                                                        long long ppc, const uint32_t* __restrict__ bstart,
-                                                        const uint32_t* __restrict__ cta_base, int cb,
-                                                        PtRec* __restrict__ rec, uint32_t* __restrict__ spos) {
-  constexpr int U = FPE_SCATTER_U;   // independent loads in flight per thread
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const uint32_t ppc32 = (uint32_t)ppc;   // n <= kMaxBatch = 2^28: 32-bit index arithmetic
-  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
-    uint2 kr[U];
-    int2 w[U];
-    double2 z[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = i0 + u * stride;
-      if (i < n) { kr[u] = __ldg(keys + i); w[u] = __ldg(lr + i); z[u] = load_point_any(pk, pts, i); }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = i0 + u * stride;
-      if (i < n) {
-        const uint32_t c = kr[u].x >> (24 - cb);
-        const uint32_t pos = __ldg(bstart + c) + __ldg(cta_base + ((size_t)((uint32_t)i / ppc32) << cb) + c) + kr[u].y;
-        spos[i] = pos;
-        // one 256-bit store (STG.E.ENL2.256): the whole 32-byte sector in one request
-        const unsigned long long zx = __double_as_longlong(z[u].x), zy = __double_as_longlong(z[u].y);
-        asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(rec + pos), "r"((uint32_t)i),
-                     "r"(kr[u].x), "r"((uint32_t)w[u].x), "r"((uint32_t)w[u].y), "r"((uint32_t)zx),
-                     "r"((uint32_t)(zx >> 32)), "r"((uint32_t)zy), "r"((uint32_t)(zy >> 32))
-                     : "memory");
-      }
-    }
-  }
 }
 
 // The evaluator's work plan: groups of gsize consecutive points in bucket order (across bucket
@@ -167,13 +114,11 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const PtRec* __restri
   plan.desc[g] = d;
 }
 
-void bucket_finish(const uint2* keys, const int2* lr, long long n, long long ppc, const uint32_t* gcount,
-                   const uint32_t* cta_base, uint32_t* bstart, PtRec* rec, uint32_t* spos, int pk,
-                   const void* pts, long long k_min, const Plan& plan, cudaStream_t s) {
-  const int cb = coarse_bits(n);
-  k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, cb);
-  const long long blocks = std::min<long long>((n + FPE_SCATTER_U * 256 - 1) / (FPE_SCATTER_U * 256), 148ll * 32);
-  k_bucket_scatter<<<(int)blocks, 256, 0, s>>>(keys, lr, pk, pts, n, ppc, bstart, cta_base, cb, rec, spos);
+void bucket_scan(const uint32_t* gcount, uint32_t* bstart, long long n, cudaStream_t s) {
+  k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, coarse_bits(n));
+}
+
+void plan_groups(long long n, const PtRec* rec, long long k_min, const Plan& plan, cudaStream_t s) {
   const long long groups = (n + plan.gsize - 1) / plan.gsize;
   k_plan<<<(int)((groups + 7) / 8), 256, 0, s>>>(n, rec, k_min, plan);
 }

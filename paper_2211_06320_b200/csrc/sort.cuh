@@ -5,9 +5,9 @@
 #include <cuda_runtime.h>
 
 namespace fpe {
-constexpr int kCoarseBits = 15;                 // buckets: the top 15 of the 24 key bits (sign, exponent and
-constexpr int kBuckets = 1 << kCoarseBits;      // 7 mantissa bits of lambda + the long-window bit); groups of
-                                                // consecutive points of a bucket share 99% of their windows
+constexpr int kCoarseBits = 15;                 // buckets: the top 15 of the 23 key bits (sign, exponent and
+constexpr int kBuckets = 1 << kCoarseBits;      // 8 mantissa bits of an estimate of lambda); groups of
+                                                // consecutive points of a bucket share their windows
 // Bucket bits for a batch of n points: 15 from 2^20 points up, fewer for small batches (~32 points per
 // bucket), so that the per-CTA histograms, slice claims and the bucket scan do not dominate them.
 __host__ __device__ __forceinline__ int coarse_bits(long long n) {
@@ -37,8 +37,9 @@ struct __align__(32) PtRec {
   int32_t l, r;
   double x, y;
 };
-// The evaluator overwrites a group's records with its accumulators, in bucket order (coalesced; every read
-// of a record precedes its overwrite); k_unsort applies the epilogue and moves them to the caller's order.
+// The evaluator stages each point's accumulator at the point's input index (one whole 32-byte sector per
+// point, so the random writes need no read-modify-write); k_unsort streams them back in the caller's order
+// and applies the epilogue.
 struct __align__(32) PtOut {
   double re, im;   // the point's accumulator acc (eval_tiled.cu stage_acc)
   long long E;     // an extra binary exponent of acc (wide handles), else 0
@@ -92,10 +93,8 @@ struct Plan {
   unsigned long long* stats;   // the call's counters (workspace header, kStat*)
 };
 
-// bucket starts (k_bucket_scan), records and points in bucket order (k_bucket_scatter), and the work plan
-// (k_plan); spos[i] = bucket position of input point i
-void bucket_finish(const uint2* keys, const int2* lr, long long n, long long ppc, const uint32_t* gcount,
-                   const uint32_t* cta_base, uint32_t* bstart, PtRec* rec, uint32_t* spos, int pk,
-                   const void* pts, long long k_min, const Plan& plan, cudaStream_t s);
+// bucket starts from the bucket totals (k_bucket_scan); the work plan of the records in bucket order (k_plan)
+void bucket_scan(const uint32_t* gcount, uint32_t* bstart, long long n, cudaStream_t s);
+void plan_groups(long long n, const PtRec* rec, long long k_min, const Plan& plan, cudaStream_t s);
 inline long long max_groups(long long n) { return (n + 63) / 64; }   // groups of >= 64 points
 }  // namespace fpe
