@@ -693,6 +693,7 @@ __device__ __forceinline__ void eval_piece(Ring<CK>& R, const Pts<NP>& S, int rl
 template <int NP>
 struct GroupCtx {   // raw loads of a group, consumed only when the group is evaluated
   uint32_t g;
+  bool second;      // fetched in the bucket-order pass (after the long-group list)
   GroupDesc d;
   int4 h[NP];
   double2 z[NP];
@@ -876,19 +877,25 @@ __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(l
   const int kmin = (int)P.k_min;
   if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
   GroupCtx<NP> cur;
-  // reverse bucket order: the long-window groups (the largest single items) first, the shortest last,
-  // so that the tail of the persistent loop is short
-  auto gid = [&](uint32_t it) { return it < plan.ngroups ? plan.ngroups - 1 - it : plan.ngroups; };
-  group_load<PK, NP>(cur, gid(__shfl_sync(0xffffffffu, nxt, 0)), n, plan, rec, kmin);
-  if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
+  // the listed long-window groups (the largest single items) first, then the others in reverse bucket
+  // order, so that the tail of the persistent loop is short
+  const uint32_t n_long = plan.ctrs[3];
+  auto gid = [&](uint32_t it) {
+    return it < n_long ? __ldg(plan.long_groups + it)
+                       : (it - n_long < plan.ngroups ? plan.ngroups - 1 - (it - n_long) : plan.ngroups);
+  };
+  auto load = [&](GroupCtx<NP>& c) {
+    const uint32_t it = __shfl_sync(0xffffffffu, nxt, 0);
+    group_load<PK, NP>(c, gid(it), n, plan, rec, kmin);
+    c.second = it >= n_long;
+    if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
+  };
+  load(cur);
   while (cur.g < plan.ngroups) {
     GroupCtx<NP> nx;
-    auto fetch_next = [&]() {
-      group_load<PK, NP>(nx, gid(__shfl_sync(0xffffffffu, nxt, 0)), n, plan, rec, kmin);
-      if (lane == 0) nxt = atomicAdd(plan.ctrs + 1, 1u);
-    };
-    if (cur.d.npieces > 1 || (cur.d.mma_np > 0 && cur.d.mma_slot == kMmaInWarp))
-      fetch_next();   // evaluated as parallel pieces (multi_piece), or by k_eval_overflow
+    auto fetch_next = [&]() { load(nx); };
+    if (cur.d.npieces > 1 || (cur.d.mma_np > 0 && cur.d.mma_slot == kMmaInWarp) || (cur.second && cur.d.listed))
+      fetch_next();   // evaluated as parallel pieces (multi_piece), by k_eval_overflow, or from the list
     else {
       FPE_TRACE_T0;
       single_group<PK, CK, OK, NP>(R, cur, n, P, plan, out, fetch_next);
@@ -1420,7 +1427,7 @@ size_t tiled_ws_bytes(long long n) {
   return al256(n * sizeof(PtOut)) + al256(n * sizeof(PtRec)) +
          al256(mma_cap(n) * sizeof(uint2)) + al256(mma_cap(n) * 128 * sizeof(double2)) +
          al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) +
-         al256(max_groups(n) * sizeof(GroupDesc)) + 2 * al256(max_groups(n) * sizeof(uint32_t)) +
+         al256(max_groups(n) * sizeof(GroupDesc)) + 3 * al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
 }
 
@@ -1559,6 +1566,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   plan.desc = reinterpret_cast<GroupDesc*>(p); p += al256(max_groups(n) * sizeof(GroupDesc));
   plan.gcnt = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
   plan.ovf_groups = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
+  plan.long_groups = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
   plan.items = reinterpret_cast<uint2*>(p); p += al256(scratch_slots(n) * sizeof(uint2));
   plan.scratch = p; p += al256(scratch_slots(n) * 1024);
   plan.mma_items = reinterpret_cast<uint2*>(p); p += al256(mma_cap(n) * sizeof(uint2));
@@ -1575,7 +1583,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   const size_t slot_bytes = (size_t)plan.gsize * (f32 ? sizeof(float2) : sizeof(double2));
   plan.cap = (uint32_t)(scratch_slots(n) * 1024 / slot_bytes);
   cudaMemsetAsync(gcount, 0, (kBuckets + 1) * 4, s);
-  cudaMemsetAsync(plan.ctrs, 0, 32, s);   // [0..3] vector items / groups / slots, [4..5] DMMA items
+  cudaMemsetAsync(plan.ctrs, 0, 32, s);   // [0..3] vector items / groups / slots / long groups, [4..7] DMMA items
   switch (pk) {
     case FPE_R64: launch_classify_bucket_t<FPE_R64>(pts, n, P, gcount, cta_base, bstart, rec, diag, hard, st, s); break;
     case FPE_C64: launch_classify_bucket_t<FPE_C64>(pts, n, P, gcount, cta_base, bstart, rec, diag, hard, st, s); break;

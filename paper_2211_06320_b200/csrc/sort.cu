@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const PtRec* __restri
   d.p0 = (uint32_t)first;
   d.count = count;
   d.lo = lo; d.hi = hi; d.slot = 0; d.npieces = 1;
-  d.mma_p0 = 0; d.mma_np = 0; d.mma_slot = 0; d.pad = 0;
+  d.mma_p0 = 0; d.mma_np = 0; d.mma_slot = 0; d.listed = 0;
   if (clo <= chi) {
     const int np = chi - clo + 1;
     d.mma_p0 = clo; d.mma_np = np;
@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const PtRec* __restri
       atomicAdd(plan.stats + kStatPieceSerial, 1ull);
       for (uint32_t i = base; i < plan.cap && i < base + (uint32_t)np; ++i) plan.items[i] = make_uint2(~0u, 0u);
     }
+  }
+  if (FPE_LONG_FIRST && d.npieces == 1 && d.mma_slot != kMmaInWarp && hi >= lo && hi - lo + 1 > kLongWin) {
+    d.listed = 1;   // the largest single items first, so that the persistent evaluator's tail is short
+    plan.long_groups[atomicAdd(plan.ctrs + 3, 1u)] = (uint32_t)g;
   }
   plan.desc[g] = d;
 }

@@ -57,7 +57,7 @@ struct GroupDesc {
   int32_t mma_p0;   // first kPiece-aligned piece some point covers whole (tensor cores, k_eval_mma)
   int32_t mma_np;   // number of such pieces (0: none, or the DMMA scratch was exhausted)
   uint32_t mma_slot;  // their first slot in the DMMA scratch
-  int32_t pad;
+  int32_t listed;   // 1: in Plan::long_groups (evaluated first, skipped in the bucket-order pass)
 };
 
 // Tensor-core coverage (k_eval_mma): point (window [wl, wr] relative to k_min, z = x + iy) has piece p
@@ -78,7 +78,8 @@ struct Plan {
   GroupDesc* desc;        // [max_groups]
   uint32_t* gcnt;         // [max_groups] finished pieces of a multi-piece group
   uint2* items;           // [cap] (group, piece) of the parallel pieces; group = ~0u: unused slot
-  uint32_t* ctrs;         // [0] multi fetch, [1] group fetch, [2] slots reserved
+  uint32_t* ctrs;         // [0] multi fetch, [1] group fetch, [2] slots reserved, [3] long groups listed
+  uint32_t* long_groups;  // [max_groups] single-item groups with a union window longer than kLongWin
   void* scratch;          // [cap][32*NP] piece partials (working complex type)
   uint32_t cap;           // scratch slots
   int gsize;              // points per group (32*NP)
@@ -96,5 +97,9 @@ struct Plan {
 // bucket starts from the bucket totals (k_bucket_scan); the work plan of the records in bucket order (k_plan)
 void bucket_scan(const uint32_t* gcount, uint32_t* bstart, long long n, cudaStream_t s);
 void plan_groups(long long n, const PtRec* rec, long long k_min, const Plan& plan, cudaStream_t s);
+#ifndef FPE_LONG_FIRST
+#define FPE_LONG_FIRST 1
+#endif
+constexpr int kLongWin = 4096;   // groups with longer union windows are evaluated first (FPE_LONG_FIRST)
 inline long long max_groups(long long n) { return (n + 63) / 64; }   // groups of >= 64 points
 }  // namespace fpe
