@@ -284,13 +284,15 @@ const char* fpe_stage_name(fpe_poly h, int i);
 /*
  * fpe_workspace_stats -- the counters the last fpe_evaluate with this workspace wrote into its first 256
  * bytes (the call zeroes them on its stream first).  Synchronises `stream` (the call's stream), then
- * copies min(cap, *n) counters into the host array stats; *n receives the number of counters (5):
+ * copies min(cap, *n) counters into the host array stats; *n receives the number of counters (6):
  *   [0] lambdas within 2^-80 of an fp64 rounding boundary (Ziv test of the correctly rounded log2|z|;
  *       counted for the points whose lambda was computed: all with diagnostics, the undecided ones without)
  *   [1] (group, piece) tensor-core items planned (whole 16384-coefficient pieces, complex fp64)
  *   [2] ... of which did not fit the workspace's DMMA scratch and ran in-warp (same arithmetic)
  *   [3] parallel vector pieces of long windows
  *   [4] long-window groups evaluated serially (piece scratch full; same arithmetic)
+ *   [5] (CTA, bucket) slices the classifier did not fill exactly as the histogram pass counted them --
+ *       a self-check of the work bucketing (0 unless the two passes disagree on a point's bucket key)
  * Errors: INVALID_ARG, CUDA.
  */
 fpe_status fpe_workspace_stats(const void* workspace, void* stream, int64_t* stats, int cap, int* n);

@@ -49,15 +49,22 @@ constexpr int kStages = 3;     // TMA ring depth per warp
 // top -- 23 bits, monotone in |z|.  l and r are non-decreasing in lambda (d/dlambda of cover(k) + lambda k - N
 // is k - k_lambda), so points with close keys have nested, nearly equal windows.  z = 0 and non-finite z
 // take key 0.  k_bucket_hist and k_classify_bucket both call this one function on the same points.
-__device__ __forceinline__ uint32_t bucket_key(double x, double y, bool cplx) {
-  if (!(isfinite(x) && isfinite(y)) || (x == 0.0 && (!cplx || y == 0.0))) return 0u;
-  double lo, hi, lam;
-  lambda_enclosure(x, y, cplx, lo, hi, lam);
+__device__ __forceinline__ bool key_point(double x, double y, bool cplx) {
+  return isfinite(x) && isfinite(y) && (x != 0.0 || (cplx && y != 0.0));
+}
+// lam: lambda_enclosure's midpoint for a key_point (finite nonzero z)
+__device__ __forceinline__ uint32_t key_of_estimate(double lam) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(lam));
   const int E = (int)(b >> 52) - 1023;
   uint32_t mag = 0;
   if (E >= -52) mag = ((uint32_t)(E + 53) << 16) | (uint32_t)((b >> 36) & 0xffff);
   return (lam >= 0.0) ? (1u << 22) + mag : (1u << 22) - 1u - mag;
+}
+__device__ __forceinline__ uint32_t bucket_key(double x, double y, bool cplx) {
+  if (!key_point(x, y, cplx)) return 0u;
+  double lo, hi, lam;
+  lambda_enclosure(x, y, cplx, lo, hi, lam);
+  return key_of_estimate(lam);
 }
 constexpr int kKeyBits = 23;
 
@@ -68,7 +75,7 @@ constexpr int kKeyBits = 23;
 template <int PK>
 __global__ void __launch_bounds__(kScatterThreads) k_bucket_hist(const void* __restrict__ pts, long long n,
                                                                  long long ppc, uint32_t* __restrict__ gcount,
-                                                                 uint32_t* __restrict__ cta_base) {
+                                                                 uint2* __restrict__ cta_slice) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(s_dyn);
   const int cb = coarse_bits(n), nbk = 1 << cb;
@@ -92,21 +99,23 @@ __global__ void __launch_bounds__(kScatterThreads) k_bucket_hist(const void* __r
   __syncthreads();
   for (int b = threadIdx.x; b < nbk; b += blockDim.x) {
     const uint32_t c = hist[b];
-    cta_base[((size_t)blockIdx.x << cb) + b] = c ? atomicAdd(gcount + b, c) : 0u;
+    cta_slice[((size_t)blockIdx.x << cb) + b] = make_uint2(c ? atomicAdd(gcount + b, c) : 0u, c);
   }
 }
 
 // Pass 2: lines 5-8 of FPE_p per point (lambda, k_lambda, [l, r]; device_common.cuh) and the point's record
 // {index, key, l, r, z} written to its bucket position: bucket start + this CTA's slice (k_bucket_hist,
-// k_bucket_scan) + a shared-memory counter.  The order inside a (CTA, bucket) slice is unspecified.
+// k_bucket_scan) + a shared-memory counter.  The order inside a (CTA, bucket) slice is unspecified.  At the
+// end every counter must stand at its slice's end (both passes computed the same keys): checked, counted in
+// kStatSliceMismatch.
 template <int PK>
 __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void* __restrict__ pts, long long n,
                                                                      long long ppc, PolyDev P,
                                                                      const uint32_t* __restrict__ bstart,
-                                                                     const uint32_t* __restrict__ cta_base,
+                                                                     const uint2* __restrict__ cta_slice,
                                                                      PtRec* __restrict__ rec,
                                                                      fpe_diag* __restrict__ diag,
-                                                                     unsigned long long* __restrict__ hard_ctr) {
+                                                                     unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
   uint32_t* slot = reinterpret_cast<uint32_t*>(s_dyn);   // next position of every bucket's slice, then the cover
   const int2* hull = P.hull;
@@ -122,7 +131,8 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
     hull = sh;
   }
   const int cb = coarse_bits(n), nbk = 1 << cb;
-  for (int b = threadIdx.x; b < nbk; b += blockDim.x) slot[b] = __ldg(bstart + b) + __ldg(cta_base + ((size_t)blockIdx.x << cb) + b);
+  const uint2* my = cta_slice + ((size_t)blockIdx.x << cb);
+  for (int b = threadIdx.x; b < nbk; b += blockDim.x) slot[b] = __ldg(bstart + b) + __ldg(my + b).x;
   __syncthreads();
   const long long beg = (long long)blockIdx.x * ppc, end = min(n, beg + ppc);
   double xn = 0.0, yn = 0.0;   // the next iteration's point, loaded one iteration ahead
@@ -134,11 +144,14 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
     double lam = 0.0;
     int istar, l, r;
     bool done = false;
-    if (staged && P.dbl_ok && isfinite(x) && isfinite(y) && (x != 0.0 || (PtTraits<PK>::cplx && y != 0.0))) {
-      // fast path: searches on an enclosure of log2|z|; only undecided points compute the rounded lambda
+    // the enclosure of log2|z| (its midpoint gives the bucket key, exactly as in k_bucket_hist)
+    const bool kp = key_point(x, y, PtTraits<PK>::cplx);
+    double lo = 0.0, hi = 0.0, mid = 0.0;
+    if (kp) lambda_enclosure(x, y, PtTraits<PK>::cplx, lo, hi, mid);
+    const uint32_t key = kp ? key_of_estimate(mid) : 0u;
+    if (staged && P.dbl_ok && kp) {
+      // fast path: searches on the enclosure; only undecided points compute the rounded lambda
       // (the diagnostics still report the rounded lambda, so the tests check this path's indexing)
-      double lo, hi;
-      lambda_enclosure(x, y, PtTraits<PK>::cplx, lo, hi, lam);
       bool amb = false;
       classify_lambda_vp(hull, hv, P.nv, P.drop, LamIv{lo, hi, &amb}, istar, l, r);
       done = !amb;
@@ -157,8 +170,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
       dg.err_exp = INT32_MIN; dg.pad = 0;
       diag[i] = dg;
     }
-    if (hard) atomicAdd(hard_ctr, 1ull);
-    const uint32_t key = bucket_key(x, y, PtTraits<PK>::cplx);
+    if (hard) atomicAdd(stats + kStatHard, 1ull);
     // one shared-memory atomic per point (buckets rarely repeat within a warp)
     const uint32_t pos = atomicAdd(&slot[key >> (kKeyBits - cb)], 1u);
     // one 256-bit store (STG.E.ENL2.256): the record's whole 32-byte sector in one request
@@ -167,6 +179,11 @@ __global__ void __launch_bounds__(kScatterThreads) k_classify_bucket(const void*
                  "r"(key), "r"((uint32_t)l), "r"((uint32_t)r), "r"((uint32_t)zx), "r"((uint32_t)(zx >> 32)),
                  "r"((uint32_t)zy), "r"((uint32_t)(zy >> 32))
                  : "memory");
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbk; b += blockDim.x) {
+    const uint2 sl = __ldg(my + b);
+    if (slot[b] != __ldg(bstart + b) + sl.x + sl.y) atomicAdd(stats + kStatSliceMismatch, 1ull);
   }
 }
 
@@ -1426,7 +1443,7 @@ static size_t mma_cap(long long n) { return max((size_t)64, (size_t)n * 4 / (128
 size_t tiled_ws_bytes(long long n) {
   return al256(n * sizeof(PtOut)) + al256(n * sizeof(PtRec)) +
          al256(mma_cap(n) * sizeof(uint2)) + al256(mma_cap(n) * 128 * sizeof(double2)) +
-         al256(n_ctas(n) * kBuckets * sizeof(uint32_t)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) +
+         al256(n_ctas(n) * kBuckets * sizeof(uint2)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) +
          al256(max_groups(n) * sizeof(GroupDesc)) + 3 * al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
 }
@@ -1492,17 +1509,17 @@ static int np_for(int pk, int cdt, long long d_eff) {
 // bucket positions (k_classify_bucket)
 template <int PK>
 static void launch_classify_bucket_t(const void* pts, long long n, const PolyDev& P, uint32_t* gcount,
-                                     uint32_t* cta_base, uint32_t* bstart, PtRec* rec, fpe_diag* diag,
-                                     unsigned long long* hard, Stage& st, cudaStream_t s) {
+                                     uint2* cta_slice, uint32_t* bstart, PtRec* rec, fpe_diag* diag,
+                                     unsigned long long* stats, Stage& st, cudaStream_t s) {
   const size_t hsmem = kBuckets * sizeof(uint32_t);
   cudaFuncSetAttribute(k_bucket_hist<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
-  k_bucket_hist<PK><<<(int)n_ctas(n), kScatterThreads, hsmem, s>>>(pts, n, pts_per_cta(n), gcount, cta_base);
+  k_bucket_hist<PK><<<(int)n_ctas(n), kScatterThreads, hsmem, s>>>(pts, n, pts_per_cta(n), gcount, cta_slice);
   bucket_scan(gcount, bstart, n, s);
   st.mark("bucket");
   const size_t smem = kBuckets * sizeof(uint32_t) + (P.nv <= kSmemHullDbl ? P.nv * (sizeof(int2) + sizeof(double2)) : 0);
   cudaFuncSetAttribute(k_classify_bucket<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_classify_bucket<PK><<<(int)n_ctas(n), kScatterThreads, smem, s>>>(pts, n, pts_per_cta(n), P, bstart, cta_base,
-                                                                     rec, diag, hard);
+  k_classify_bucket<PK><<<(int)n_ctas(n), kScatterThreads, smem, s>>>(pts, n, pts_per_cta(n), P, bstart, cta_slice,
+                                                                     rec, diag, stats);
 }
 
 template <int PK, int CK>
@@ -1553,13 +1570,12 @@ bool run_horner_tiled(int pk, const void* pts, long long n, const PolyDev& P, ui
 
 int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals, long long* exps,
               fpe_diag* diag, void* ws, unsigned long long* stats, Stage& st, cudaStream_t s) {
-  unsigned long long* hard = stats + kStatHard;
   char* p = static_cast<char*>(ws);
   // the evaluators' accumulators staged at the point's input index (random whole-sector writes from the
   // bucket order, so that k_unsort streams them back in order)
   PtOut* staged = reinterpret_cast<PtOut*>(p); p += al256(n * sizeof(PtOut));
   PtRec* rec = reinterpret_cast<PtRec*>(p); p += al256(n * sizeof(PtRec));   // bucket order
-  uint32_t* cta_base = reinterpret_cast<uint32_t*>(p); p += al256(n_ctas(n) * kBuckets * 4);
+  uint2* cta_slice = reinterpret_cast<uint2*>(p); p += al256(n_ctas(n) * kBuckets * sizeof(uint2));   // {start, count}
   uint32_t* gcount = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   uint32_t* bstart = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   Plan plan;
@@ -1585,10 +1601,10 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   cudaMemsetAsync(gcount, 0, (kBuckets + 1) * 4, s);
   cudaMemsetAsync(plan.ctrs, 0, 32, s);   // [0..3] vector items / groups / slots / long groups, [4..7] DMMA items
   switch (pk) {
-    case FPE_R64: launch_classify_bucket_t<FPE_R64>(pts, n, P, gcount, cta_base, bstart, rec, diag, hard, st, s); break;
-    case FPE_C64: launch_classify_bucket_t<FPE_C64>(pts, n, P, gcount, cta_base, bstart, rec, diag, hard, st, s); break;
-    case FPE_R32: launch_classify_bucket_t<FPE_R32>(pts, n, P, gcount, cta_base, bstart, rec, diag, hard, st, s); break;
-    default: launch_classify_bucket_t<FPE_C32>(pts, n, P, gcount, cta_base, bstart, rec, diag, hard, st, s); break;
+    case FPE_R64: launch_classify_bucket_t<FPE_R64>(pts, n, P, gcount, cta_slice, bstart, rec, diag, stats, st, s); break;
+    case FPE_C64: launch_classify_bucket_t<FPE_C64>(pts, n, P, gcount, cta_slice, bstart, rec, diag, stats, st, s); break;
+    case FPE_R32: launch_classify_bucket_t<FPE_R32>(pts, n, P, gcount, cta_slice, bstart, rec, diag, stats, st, s); break;
+    default: launch_classify_bucket_t<FPE_C32>(pts, n, P, gcount, cta_slice, bstart, rec, diag, stats, st, s); break;
   }
   st.mark("classify");
   plan_groups(n, rec, P.k_min, plan, s);

@@ -41,7 +41,8 @@ enum : int {
   kStatMmaInWarp = 2,     // ... of which the DMMA scratch could not hold: run in-warp by the vector evaluator
   kStatPieceItems = 3,    // parallel vector pieces of long windows
   kStatPieceSerial = 4,   // long-window groups evaluated serially (piece scratch full)
-  kStatCount = 5
+  kStatSliceMismatch = 5, // bucket slices a classify CTA did not fill exactly as k_bucket_hist counted (expected 0)
+  kStatCount = 6
 };
 
 // Kernel-side view of a handle.
