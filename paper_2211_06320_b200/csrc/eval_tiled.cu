@@ -68,6 +68,40 @@ __device__ __forceinline__ uint32_t bucket_key(double x, double y, bool cplx) {
 }
 constexpr int kKeyBits = 23;
 
+// The lambda estimates whose keys fall in bucket b (keys [b 2^s, (b + 1) 2^s), s = kKeyBits - cb): a superset
+// [lo, hi] (mag values no estimate produces -- exponent field 0 -- are read as |lambda| < 2^-52).
+__device__ __forceinline__ void bucket_estimates(uint32_t b, int cb, double& lo, double& hi) {
+  const int s = kKeyBits - cb;
+  const uint32_t k0 = b << s, k1 = ((b + 1) << s) - 1;
+  auto mlo = [](uint32_t mag) { return (mag >> 16) == 0 ? 0.0 : ldexp(1.0 + (mag & 0xffff) * 0x1p-16, (int)(mag >> 16) - 53); };
+  auto mhi = [](uint32_t mag) { return (mag >> 16) == 0 ? 0x1p-52 : ldexp(1.0 + ((mag & 0xffff) + 1) * 0x1p-16, (int)(mag >> 16) - 53); };
+  if (k0 >= (1u << 22)) { lo = mlo(k0 - (1u << 22)); hi = mhi(k1 - (1u << 22)); }
+  else { lo = -mhi((1u << 22) - 1 - k0); hi = -mlo((1u << 22) - 1 - k1); }
+}
+
+// Window bounds of every bucket's points for k_plan: a point's lambda = RN(log2|z|) lies within 2^-50 +
+// 2^-53 |lambda| (+ half an ulp) of its estimate, so within [lo - eps, hi + eps] of its bucket's estimates
+// (eps = 2^-44 (1 + |lambda|), generous); l and r are non-decreasing in lambda, so the windows at the two ends
+// (exact classification, device_common.cuh) bound every point's.  Bucket 0 holds only z = 0 (window {k_min})
+// and non-finite z (empty windows): no finite z has an estimate below -1100.  Also flags buckets whose points
+// are all below / all above mma_covers' |z| range (|z| in [max(|x|,|y|), sqrt2 max(|x|,|y|)), so lambda
+// < -3 or >= 3.5 rules a point out).
+__global__ void __launch_bounds__(256) k_bucket_windows(PolyDev P, int cb, int4* __restrict__ bwin) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= (1 << cb)) return;
+  int4 w = make_int4(0, 0, 1, 0);
+  if (b > 0) {
+    double lo, hi;
+    bucket_estimates((uint32_t)b, cb, lo, hi);
+    const double la = lo - 0x1p-44 * (1.0 + fabs(lo)), lb = hi + 0x1p-44 * (1.0 + fabs(hi));
+    int istar, l, r, l2, r2;
+    classify_lambda(P.hull, P.nv, P.drop, la, istar, l, r);
+    classify_lambda(P.hull, P.nv, P.drop, lb, istar, l2, r2);
+    w = make_int4((int)(l - P.k_min), (int)(r2 - P.k_min), lb < -3.0 ? 1 : 0, la >= 3.5 ? 1 : 0);
+  }
+  bwin[b] = w;
+}
+
 // Pass 1 of the counting sort: per classify CTA (the same contiguous range of points k_classify_bucket
 // gives it), a shared-memory histogram of the top coarse_bits(n) key bits, then one global atomicAdd per
 // nonzero bucket claims the CTA's slice of that bucket.  A streaming pass over the points (16 B each for
@@ -1443,7 +1477,7 @@ static size_t mma_cap(long long n) { return max((size_t)64, (size_t)n * 4 / (128
 size_t tiled_ws_bytes(long long n) {
   return al256(n * sizeof(PtOut)) + al256(n * sizeof(PtRec)) +
          al256(mma_cap(n) * sizeof(uint2)) + al256(mma_cap(n) * 128 * sizeof(double2)) +
-         al256(n_ctas(n) * kBuckets * sizeof(uint2)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) +
+         al256(n_ctas(n) * kBuckets * sizeof(uint2)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) + al256(kBuckets * sizeof(int4)) +
          al256(max_groups(n) * sizeof(GroupDesc)) + 3 * al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
 }
@@ -1578,6 +1612,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   uint2* cta_slice = reinterpret_cast<uint2*>(p); p += al256(n_ctas(n) * kBuckets * sizeof(uint2));   // {start, count}
   uint32_t* gcount = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
   uint32_t* bstart = reinterpret_cast<uint32_t*>(p); p += al256((kBuckets + 1) * 4);
+  int4* bwin = reinterpret_cast<int4*>(p); p += al256(kBuckets * sizeof(int4));
   Plan plan;
   plan.desc = reinterpret_cast<GroupDesc*>(p); p += al256(max_groups(n) * sizeof(GroupDesc));
   plan.gcnt = reinterpret_cast<uint32_t*>(p); p += al256(max_groups(n) * sizeof(uint32_t));
@@ -1607,7 +1642,11 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
     default: launch_classify_bucket_t<FPE_C32>(pts, n, P, gcount, cta_slice, bstart, rec, diag, stats, st, s); break;
   }
   st.mark("classify");
-  plan_groups(n, rec, P.k_min, plan, s);
+  {
+    const int nbk = 1 << coarse_bits(n);
+    k_bucket_windows<<<(nbk + 255) / 256, 256, 0, s>>>(P, coarse_bits(n), bwin);
+  }
+  plan_groups(n, bstart, bwin, plan, s);
   st.mark("plan");
   int lm = 0;
   if (plan.mma_on) {
@@ -1651,7 +1690,7 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   }
 #undef FPE_UN
   st.mark("unsort");
-  return 5 + le + lm;
+  return 6 + le + lm;   // hist, scan, classify, bucket windows, plan, unsort
 }
 
 }  // namespace fpe

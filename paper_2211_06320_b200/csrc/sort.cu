@@ -6,8 +6,8 @@
 // (eval_tiled.cu) builds a per-CTA histogram in shared memory and claims each CTA's slice of every bucket
 // with one global atomicAdd per nonzero bin; k_bucket_scan turns bucket totals into starts;
 // k_classify_bucket (eval_tiled.cu) classifies the same points and writes every record {index, key, l, r, z}
-// to bucket start + its CTA's slice + a shared-memory counter; k_plan cuts the bucket order into groups of
-// 32*NP points and plans their work items.  Order inside a (CTA, bucket) slice is unspecified; every point's
+// to bucket start + its CTA's slice + a shared-memory counter; k_bucket_windows bounds the windows of every
+// bucket's points; k_plan cuts the bucket order into groups of 32*NP points and plans their work items.  Order inside a (CTA, bucket) slice is unspecified; every point's
 // arithmetic depends only on its own window, so results do not depend on it (bitwise).
 #include <cuda_runtime.h>
 #include <algorithm>
@@ -48,36 +48,35 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(const uint32_t* __restrict
 }
 
 // The evaluator's work plan: groups of gsize consecutive points in bucket order (across bucket
-// boundaries: neighbouring buckets hold neighbouring lambdas), one warp per group: the union of the
-// windows and either one single item (one warp, pieces in order) or npieces parallel items with scratch
-// slots for their partials (windows longer than kPiece).
-__global__ void __launch_bounds__(256) k_plan(long long n, const PtRec* __restrict__ rec, long long k_min,
-                                              Plan plan) {
-  const int lane = threadIdx.x & 31;
-  const long long g = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+// boundaries: neighbouring buckets hold neighbouring lambdas), one warp per group, one thread here per group.
+// A group's union window is bounded by its buckets' window bounds (k_bucket_windows: l and r are
+// non-decreasing in lambda, so [l of its first bucket, r of its last] contains every point's window) -- no
+// pass over the records.  Within a bucket the points are in no particular order, so a group inside one bucket
+// spans nearly the bucket's whole lambda range anyway: the bound is essentially the exact union.  Then either
+// one single item (one warp, pieces in order) or npieces parallel items with scratch slots for their
+// partials (windows longer than kPiece), plus a tensor-core item for every whole piece of the union when some
+// point of the group could be in mma_covers' |z| range (the evaluators test each point exactly).
+__device__ __forceinline__ int bucket_of(const uint32_t* __restrict__ bstart, int nbk, uint32_t pos) {
+  int lo = 0, hi = nbk;   // the last bucket whose start is <= pos (empty buckets before it share its start)
+  while (hi - lo > 1) { const int m = (lo + hi) >> 1; if (__ldg(bstart + m) <= pos) lo = m; else hi = m; }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_plan(long long n, const uint32_t* __restrict__ bstart, int nbk,
+                                              const int4* __restrict__ bwin, Plan plan) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int gs = plan.gsize;
   const long long first = g * gs;
   if (first >= n) return;
   const int count = (int)min((long long)gs, n - first);
-  int lo = 0x7fffffff, hi = -1, clo = 0x7fffffff, chi = -1;
-  for (int j = lane; j < count; j += 32) {
-    const int4 h = __ldg(reinterpret_cast<const int4*>(rec + first + j));
-    if (h.w >= h.z) {
-      const int wl = (int)(h.z - k_min), wr = (int)(h.w - k_min);
-      lo = min(lo, wl);
-      hi = max(hi, wr);
-      if (plan.mma_on) {   // the pieces this point covers whole on the tensor cores
-        const double2 z = __ldg(reinterpret_cast<const double2*>(rec + first + j) + 1);
-        const int c0 = (wl + kPiece - 1) / kPiece, c1 = (wr + 1) / kPiece - 1;
-        if (c0 <= c1 && mma_covers(wl, wr, z.x, z.y, c0)) { clo = min(clo, c0); chi = max(chi, c1); }
-      }
-    }
+  const int4 wf = __ldg(bwin + bucket_of(bstart, nbk, (uint32_t)first));
+  const int4 wl = __ldg(bwin + bucket_of(bstart, nbk, (uint32_t)(first + count - 1)));
+  const int lo = wf.x, hi = wl.y;
+  int clo = 0x7fffffff, chi = -1;
+  if (plan.mma_on && hi >= lo && !wf.w && !wl.z) {   // some point may have 2^-3 <= max(|x|, |y|) < 2^3
+    clo = (lo + kPiece - 1) / kPiece;
+    chi = (hi + 1) / kPiece - 1;
   }
-  lo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
-  hi = __reduce_max_sync(0xffffffffu, hi);
-  clo = (int)__reduce_min_sync(0xffffffffu, (unsigned)clo);
-  chi = __reduce_max_sync(0xffffffffu, chi);
-  if (lane != 0) return;
   GroupDesc d;
   d.p0 = (uint32_t)first;
   d.count = count;
@@ -122,9 +121,9 @@ void bucket_scan(const uint32_t* gcount, uint32_t* bstart, long long n, cudaStre
   k_bucket_scan<<<1, 1024, 0, s>>>(gcount, bstart, coarse_bits(n));
 }
 
-void plan_groups(long long n, const PtRec* rec, long long k_min, const Plan& plan, cudaStream_t s) {
+void plan_groups(long long n, const uint32_t* bstart, const int4* bwin, const Plan& plan, cudaStream_t s) {
   const long long groups = (n + plan.gsize - 1) / plan.gsize;
-  k_plan<<<(int)((groups + 7) / 8), 256, 0, s>>>(n, rec, k_min, plan);
+  k_plan<<<(int)((groups + 255) / 256), 256, 0, s>>>(n, bstart, 1 << coarse_bits(n), bwin, plan);
 }
 
 }  // namespace fpe

@@ -96,7 +96,9 @@ struct Plan {
 
 // bucket starts from the bucket totals (k_bucket_scan); the work plan of the records in bucket order (k_plan)
 void bucket_scan(const uint32_t* gcount, uint32_t* bstart, long long n, cudaStream_t s);
-void plan_groups(long long n, const PtRec* rec, long long k_min, const Plan& plan, cudaStream_t s);
+// bwin[b] = {l, r} bounds (relative to k_min) of the windows of bucket b's points, and whether the bucket's
+// points are all below (z) / all above (w) the |z| range of tensor-core pieces (k_bucket_windows)
+void plan_groups(long long n, const uint32_t* bstart, const int4* bwin, const Plan& plan, cudaStream_t s);
 #ifndef FPE_LONG_FIRST
 #define FPE_LONG_FIRST 1
 #endif

@@ -1,0 +1,10 @@
+#!/bin/bash
+# stage times (cfg3 x2 with counters, cfg5, cfg5-fp32, cfg2, cfg1), then the GPU suite
+mkdir -p gpurun_out
+rm -f gpurun_out/z_times.txt
+for spec in "3:" "3:" "5:" "5:--fp32" "2:" "1:"; do
+  cfg=${spec%%:*}; extra=${spec#*:}
+  timeout 300 python tools/run_cfg.py --config $cfg $extra --steps 3 >> gpurun_out/z_times.txt 2>&1
+done
+timeout 1500 python -m pytest tests -m gpu -q -x -s -k "full_size or sharding or overflow or determinism" > gpurun_out/z_tests.log 2>&1; echo "rc=$?" >> gpurun_out/z_tests.log
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/z_tests_all.log 2>&1; echo "rc=$?" >> gpurun_out/z_tests_all.log

@@ -36,8 +36,10 @@ def main():
     poly.set_profiling(True)
     poly.evaluate(pts, exps=True)
     st = poly.last_stage_ms()
+    poly.set_profiling(False)
+    poly.evaluate(pts, exps=True)
     print(json.dumps({"config": args.config, "fp32": args.fp32, "points": pts.numel(), "stages_ms": st,
-                      "total_ms": sum(t for _, t in st)}))
+                      "total_ms": sum(t for _, t in st), "counters": poly.workspace_stats()}))
 
 
 if __name__ == "__main__":
