@@ -930,9 +930,10 @@ __global__ void __launch_bounds__(kWarps * 32, FPE_EVAL_MIN_CTAS) k_eval_tiled(l
   GroupCtx<NP> cur;
   // the listed long-window groups (the largest single items) first, then the others in reverse bucket
   // order, so that the tail of the persistent loop is short
-  const uint32_t n_long = plan.ctrs[3];
+  const uint32_t n_long1 = plan.ctrs[3], n_long = n_long1 + plan.ctrs[8];
   auto gid = [&](uint32_t it) {
-    return it < n_long ? __ldg(plan.long_groups + it)
+    return it < n_long1 ? __ldg(plan.long_groups + it)
+         : it < n_long ? __ldg(plan.long_groups + plan.ngroups - 1 - (it - n_long1))
                        : (it - n_long < plan.ngroups ? plan.ngroups - 1 - (it - n_long) : plan.ngroups);
   };
   auto load = [&](GroupCtx<NP>& c) {
@@ -1634,7 +1635,8 @@ int run_tiled(int pk, const void* pts, long long n, const PolyDev& P, void* vals
   const size_t slot_bytes = (size_t)plan.gsize * (f32 ? sizeof(float2) : sizeof(double2));
   plan.cap = (uint32_t)(scratch_slots(n) * 1024 / slot_bytes);
   cudaMemsetAsync(gcount, 0, (kBuckets + 1) * 4, s);
-  cudaMemsetAsync(plan.ctrs, 0, 32, s);   // [0..3] vector items / groups / slots / long groups, [4..7] DMMA items
+  cudaMemsetAsync(plan.ctrs, 0, 48, s);   // [0..3] vector items / groups / slots / long groups, [4..7] DMMA items,
+                                          // [8] long groups of the second class
   switch (pk) {
     case FPE_R64: launch_classify_bucket_t<FPE_R64>(pts, n, P, gcount, cta_slice, bstart, rec, diag, stats, st, s); break;
     case FPE_C64: launch_classify_bucket_t<FPE_C64>(pts, n, P, gcount, cta_slice, bstart, rec, diag, stats, st, s); break;

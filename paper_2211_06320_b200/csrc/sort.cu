@@ -112,7 +112,8 @@ __global__ void __launch_bounds__(256) k_plan(long long n, const uint32_t* __res
   }
   if (FPE_LONG_FIRST && d.npieces == 1 && d.mma_slot != kMmaInWarp && hi >= lo && hi - lo + 1 > kLongWin) {
     d.listed = 1;   // the largest single items first, so that the persistent evaluator's tail is short
-    plan.long_groups[atomicAdd(plan.ctrs + 3, 1u)] = (uint32_t)g;
+    if (FPE_LONG_WIN2 == 0 || hi - lo + 1 > FPE_LONG_WIN2) plan.long_groups[atomicAdd(plan.ctrs + 3, 1u)] = (uint32_t)g;
+    else plan.long_groups[plan.ngroups - 1 - atomicAdd(plan.ctrs + 8, 1u)] = (uint32_t)g;
   }
   plan.desc[g] = d;
 }

@@ -79,7 +79,8 @@ struct Plan {
   uint32_t* gcnt;         // [max_groups] finished pieces of a multi-piece group
   uint2* items;           // [cap] (group, piece) of the parallel pieces; group = ~0u: unused slot
   uint32_t* ctrs;         // [0] multi fetch, [1] group fetch, [2] slots reserved, [3] long groups listed
-  uint32_t* long_groups;  // [max_groups] single-item groups with a union window longer than kLongWin
+  uint32_t* long_groups;  // [max_groups] single-item groups with a union window longer than kLongWin: the
+                          // longest class from the front (count ctrs[3]), the other from the back (ctrs[8])
   void* scratch;          // [cap][32*NP] piece partials (working complex type)
   uint32_t cap;           // scratch slots
   int gsize;              // points per group (32*NP)
@@ -102,6 +103,12 @@ void plan_groups(long long n, const uint32_t* bstart, const int4* bwin, const Pl
 #ifndef FPE_LONG_FIRST
 #define FPE_LONG_FIRST 1
 #endif
-constexpr int kLongWin = 4096;   // groups with longer union windows are evaluated first (FPE_LONG_FIRST)
+#ifndef FPE_LONG_WIN
+#define FPE_LONG_WIN 4096
+#endif
+#ifndef FPE_LONG_WIN2
+#define FPE_LONG_WIN2 0   // > 0: the listed groups longer than this go first (a second size class)
+#endif
+constexpr int kLongWin = FPE_LONG_WIN;   // groups with longer union windows are evaluated first (FPE_LONG_FIRST)
 inline long long max_groups(long long n) { return (n + 63) / 64; }   // groups of >= 64 points
 }  // namespace fpe
