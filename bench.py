@@ -326,9 +326,10 @@ def run_reference(args):
 
 
 def profiled_traffic(prefixes=("void k_eval_tiled", "k_eval_mma", "void k_eval_mma", "void k_eval_overflow")):
-    """DRAM bytes (read + write) per step of the window evaluator (k_eval_mma + k_eval_tiled [+ the overflow
-    kernel]) from the committed ncu --set full summary of the same cfg3 workload (round 2:
-    profiles/r02_ncu_cfg3_all_kernels.json, in bytes; round 1's file was in GB); None if absent."""
+    """DRAM bytes (read + write) per step of the kernels whose names start with `prefixes` (default: the window
+    evaluator, k_eval_mma + k_eval_tiled [+ the overflow kernel]) from the committed ncu --set full summary of
+    the same cfg3 workload (round 2: profiles/r02_ncu_cfg3_all_kernels.json, in bytes; round 1's file was in
+    GB); None if absent."""
     for name, scale in (("r02_ncu_cfg3_all_kernels.json", 1.0), ("r01_ncu_eval_tiled_cfg3.json", 1e9)):
         path = os.path.join(ROOT, "profiles", name)
         try:
@@ -486,9 +487,12 @@ def run_fpe(args):
                      "traffic": (profiled_traffic() or {}).get("bytes") if (cfg == 3 and not fp32) else None,
                      "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of the evaluator kernels "
                                      f"({(profiled_traffic() or {}).get('source')}): they read the 32-B bucket-order "
-                                     f"records and write 32-B accumulators over them ({64 * n / 1e9:.2f} GB); the "
-                                     f"path's algorithmic bytes are 40 B/pt = {40 * n / 1e9:.2f} GB (points in, values "
-                                     "and exponents out, the latter written by k_unsort)",
+                                     f"records and write a 32-B accumulator per point at its input index "
+                                     f"({64 * n / 1e9:.2f} GB); the path's algorithmic bytes are 40 B/pt = "
+                                     f"{40 * n / 1e9:.2f} GB (points in, values and exponents out, the latter written "
+                                     "by k_unsort); step_traffic = every kernel of the step",
+                     "step_traffic": (profiled_traffic(("void k_", "k_")) or {}).get("bytes")
+                     if (cfg == 3 and not fp32) else None,
                      "peak_note": ("fp32 FMA: 148 SM x 128 lanes x 1.965 GHz x 2; " if fp32 else "") +
                                   "fp64 FMA: 148 SM x 64 lanes x 1.965 GHz x 2 (guide unit counts/clock); the FP64 "
                                   "tensor cores (DMMA, k_eval_mma) run on the same datapath: 18.5T FMA/s measured "
