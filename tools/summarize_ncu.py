@@ -27,7 +27,8 @@ def main(path):
     hdr = rows[0]
     units = dict(zip(hdr, rows[1]))
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-             "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+             "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+             "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
     out = []
     for r in rows[2:]:
         if len(r) != len(hdr):
