@@ -284,7 +284,7 @@ const char* fpe_stage_name(fpe_poly h, int i);
 /*
  * fpe_workspace_stats -- the counters the last fpe_evaluate with this workspace wrote into its first 256
  * bytes (the call zeroes them on its stream first).  Synchronises `stream` (the call's stream), then
- * copies min(cap, *n) counters into the host array stats; *n receives the number of counters (6):
+ * copies min(cap, *n) counters into the host array stats; *n receives the number of counters (7):
  *   [0] lambdas within 2^-80 of an fp64 rounding boundary (Ziv test of the correctly rounded log2|z|;
  *       counted for the points whose lambda was computed: all with diagnostics, the undecided ones without)
  *   [1] (group, piece) tensor-core items planned (whole 16384-coefficient pieces, complex fp64)
@@ -293,6 +293,8 @@ const char* fpe_stage_name(fpe_poly h, int i);
  *   [4] long-window groups evaluated serially (piece scratch full; same arithmetic)
  *   [5] (CTA, bucket) slices the classifier did not fill exactly as the histogram pass counted them --
  *       a self-check of the work bucketing (0 unless the two passes disagree on a point's bucket key)
+ *   [6] points whose window [l, r] is not inside their group's planned union window -- a self-check of the
+ *       per-bucket window bounds the plan uses (0 unless they fail to contain a point's window)
  * Errors: INVALID_ARG, CUDA.
  */
 fpe_status fpe_workspace_stats(const void* workspace, void* stream, int64_t* stats, int cap, int* n);

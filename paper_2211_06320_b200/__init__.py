@@ -175,7 +175,7 @@ class Poly:
         check(lib().fpe_workspace_stats(C.c_void_p(ws.data_ptr()), C.c_void_p(st.cuda_stream), v.ctypes.data, 8,
                                         C.byref(cnt)), "fpe_workspace_stats")
         names = ["hard_lambdas", "mma_items", "mma_inwarp_items", "piece_items", "serial_long_groups",
-                 "slice_mismatch"]
+                 "slice_mismatch", "window_escapes"]
         return {k: int(v[i]) for i, k in enumerate(names[:cnt.value])}
 
     def evaluate_host(self, points: np.ndarray, exps: bool = True):

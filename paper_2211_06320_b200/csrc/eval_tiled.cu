@@ -674,6 +674,16 @@ __device__ __forceinline__ void load_group(Pts<NP>& S, uint32_t g, long long n, 
   }
 }
 
+// Self-check of the plan's union window (k_plan bounds it by per-bucket window bounds): every point's
+// window must lie inside it, else its terms outside would be skipped.  Counted in kStatWindowEscape.
+template <int NP>
+__device__ __forceinline__ void check_union(const Pts<NP>& S, const GroupDesc& d, const Plan& plan) {
+  int bad = 0;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) bad += (S.wl[j] <= S.wr[j] && (S.wl[j] < d.lo || S.wr[j] > d.hi)) ? 1 : 0;
+  if (bad) atomicAdd(plan.stats + kStatWindowEscape, (unsigned long long)bad);
+}
+
 // The Horner sums of piece p = [rlo, rhi] for the NP points of every lane (b = 0 on entry).  Points that
 // cover the whole piece on the tensor cores (mma_covers; complex fp64 coefficients) take k_eval_mma's
 // partial from its scratch instead; the others stream the part of the piece their windows need.
@@ -792,6 +802,7 @@ __device__ __forceinline__ void single_group(Ring<CK>& R, const GroupCtx<NP>& c,
   const GroupDesc d = c.d;
   Pts<NP> S;
   group_unpack<NP>(S, c, n, (int)P.k_min);
+  check_union<NP>(S, d, plan);
   const bool nonempty = d.hi >= d.lo;
   const int p_hi = nonempty ? d.hi / kPiece : 0, p_lo = nonempty ? d.lo / kPiece : 0;
   Acc A[NP];
@@ -829,6 +840,7 @@ __device__ __forceinline__ bool multi_piece(Ring<CK>& R, uint32_t g, int p, long
   const int rlo = max(d.lo, p * kPiece), rhi = min(d.hi, p * kPiece + kPiece - 1);
   Pts<NP> S;
   load_group<PK, NP>(S, g, n, rec, kmin);
+  if (p == d.lo / kPiece) check_union<NP>(S, d, plan);   // once per group
   W br[NP], bi[NP];
   eval_piece<CK, NP, CPLX>(R, S, rlo, rhi, p, d, plan, br, bi);
   const int p0 = d.lo / kPiece;

@@ -42,7 +42,8 @@ enum : int {
   kStatPieceItems = 3,    // parallel vector pieces of long windows
   kStatPieceSerial = 4,   // long-window groups evaluated serially (piece scratch full)
   kStatSliceMismatch = 5, // bucket slices a classify CTA did not fill exactly as k_bucket_hist counted (expected 0)
-  kStatCount = 6
+  kStatWindowEscape = 6,  // points whose window is not inside their group's planned union (expected 0)
+  kStatCount = 7
 };
 
 // Kernel-side view of a handle.

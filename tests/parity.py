@@ -19,6 +19,9 @@ def gpu_eval(poly, pts_np, diag=True, exps=True, horner=False):
         v, e = poly.evaluate(t, exps=exps)
         dg = None
     torch.cuda.synchronize()
+    if not horner:   # the library's self-checks of its work bucketing and plan (fpe_workspace_stats [5], [6])
+        st = poly.workspace_stats()
+        assert st.get("slice_mismatch", 0) == 0 and st.get("window_escapes", 0) == 0, st
     out = {"v": v.cpu().numpy(), "e": e.cpu().numpy() if e is not None else None}
     if dg is not None:
         out["diag"] = {k: t_.cpu().numpy() for k, t_ in fpe.diag_fields(dg).items()}

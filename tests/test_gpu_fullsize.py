@@ -92,6 +92,7 @@ def test_full_size(fpe, cfg, fp32, n_val):
     assert np.all(err[fin] <= tol), (err[fin].max(), idx[np.argmax(np.where(fin, err, 0))])
     assert st["hard_lambdas"] == 0
     assert st["slice_mismatch"] == 0   # the histogram and classify passes bucketed every point alike
+    assert st["window_escapes"] == 0   # every window inside its group's planned union
     # Theorem thm:equivAlgo: the mean band over the sphere is below 1 + 1.9046 sqrt(d D) (cfg3, cfg5); the
     # worst case K <= d_eff + 1 (and cfg4's 4096 nonzeros)
     if cfg in (3, 5):
@@ -113,7 +114,7 @@ def test_sharding_bitwise_cfg5(fpe, fp32):
     del pts
     v, e = poly.evaluate(t, exps=True)
     full_stats = poly.workspace_stats()
-    assert full_stats["slice_mismatch"] == 0
+    assert full_stats["slice_mismatch"] == 0 and full_stats["window_escapes"] == 0
     n = t.numel()
     for r in range(8):
         lo, hi = fdist.shard_range(n, r, 8)
