@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 rm -f gpurun_out/var2.txt
 for F in "$@"; do
   FPE_EXTRA_FLAGS="$F" python -m paper_2211_06320_b200.build --force > /dev/null 2>&1
-  for spec in "3:" "3:" "5:" "5:--fp32"; do
+  for spec in ${SPECS:-"3:" "3:" "5:" "5:--fp32" "2:"}; do
     cfg=${spec%%:*}; extra=${spec#*:}
     echo "[$F] $(timeout 300 python tools/run_cfg.py --config $cfg $extra --steps 3 2>&1 | tail -1)" >> gpurun_out/var2.txt
   done
