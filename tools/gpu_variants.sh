@@ -1,9 +1,12 @@
 #!/bin/bash
-# A/B timing of experiment builds (libfpe_<V>.so shipped in-tree): bench line per variant
+# stage times of cfg3 (x2), cfg5, cfg5-fp32 under experiment flags given as arguments ("" = the default build)
 mkdir -p gpurun_out
-cp paper_2211_06320_b200/libfpe.so /tmp/libfpe_base.so
-for V in base ${VARIANTS}; do
-  if [ "$V" != base ]; then cp paper_2211_06320_b200/libfpe_$V.so paper_2211_06320_b200/libfpe.so; else cp /tmp/libfpe_base.so paper_2211_06320_b200/libfpe.so; fi
-  timeout 300 python bench.py --no-extra --no-e2e --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/var_$V.json 2> gpurun_out/var_$V.err
+rm -f gpurun_out/var2.txt
+for F in "$@"; do
+  FPE_EXTRA_FLAGS="$F" python -m paper_2211_06320_b200.build --force > /dev/null 2>&1
+  for spec in ${SPECS:-"3:" "3:" "5:" "5:--fp32" "2:"}; do
+    cfg=${spec%%:*}; extra=${spec#*:}
+    echo "[$F] $(timeout 300 python tools/run_cfg.py --config $cfg $extra --steps 3 2>&1 | tail -1)" >> gpurun_out/var2.txt
+  done
 done
-cp /tmp/libfpe_base.so paper_2211_06320_b200/libfpe.so
+python -m paper_2211_06320_b200.build --force > /dev/null 2>&1
