@@ -30,7 +30,7 @@ constexpr int kPiece = FPE_KPIECE;                  // absolute coefficient piec
                                                 // combined top-down, so results never depend on the batch
 
 // A point's record in bucket order: index, sort key, window [l, r] (absolute), z as doubles -- one
-// aligned 32-byte sector, so the scatter's random writes are whole sectors.
+// aligned 32-byte sector, so the classifier's random writes are whole sectors.
 struct __align__(32) PtRec {
   int32_t idx;
   uint32_t key;
