@@ -73,8 +73,12 @@ constexpr int kKeyBits = 23;
 __device__ __forceinline__ void bucket_estimates(uint32_t b, int cb, double& lo, double& hi) {
   const int s = kKeyBits - cb;
   const uint32_t k0 = b << s, k1 = ((b + 1) << s) - 1;
-  auto mlo = [](uint32_t mag) { return (mag >> 16) == 0 ? 0.0 : ldexp(1.0 + (mag & 0xffff) * 0x1p-16, (int)(mag >> 16) - 53); };
-  auto mhi = [](uint32_t mag) { return (mag >> 16) == 0 ? 0x1p-52 : ldexp(1.0 + ((mag & 0xffff) + 1) * 0x1p-16, (int)(mag >> 16) - 53); };
+  auto mlo = [](uint32_t mag) {   // the least |lambda| with this mag
+    return (mag >> 16) == 0 ? 0.0 : ldexp(1.0 + (mag & 0xffff) * 0x1p-16, (int)(mag >> 16) - 53);
+  };
+  auto mhi = [](uint32_t mag) {   // above every |lambda| with this mag
+    return (mag >> 16) == 0 ? 0x1p-52 : ldexp(1.0 + ((mag & 0xffff) + 1) * 0x1p-16, (int)(mag >> 16) - 53);
+  };
   if (k0 >= (1u << 22)) { lo = mlo(k0 - (1u << 22)); hi = mhi(k1 - (1u << 22)); }
   else { lo = -mhi((1u << 22) - 1 - k0); hi = -mlo((1u << 22) - 1 - k1); }
 }
@@ -1493,7 +1497,8 @@ static size_t mma_cap(long long n) { return max((size_t)64, (size_t)n * 4 / (128
 size_t tiled_ws_bytes(long long n) {
   return al256(n * sizeof(PtOut)) + al256(n * sizeof(PtRec)) +
          al256(mma_cap(n) * sizeof(uint2)) + al256(mma_cap(n) * 128 * sizeof(double2)) +
-         al256(n_ctas(n) * kBuckets * sizeof(uint2)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) + al256(kBuckets * sizeof(int4)) +
+         al256(n_ctas(n) * kBuckets * sizeof(uint2)) + 2 * al256((kBuckets + 1) * sizeof(uint32_t)) +
+         al256(kBuckets * sizeof(int4)) +
          al256(max_groups(n) * sizeof(GroupDesc)) + 3 * al256(max_groups(n) * sizeof(uint32_t)) +
          al256(scratch_slots(n) * sizeof(uint2)) + al256(scratch_slots(n) * 1024) + 256;
 }

@@ -7,8 +7,9 @@
 // with one global atomicAdd per nonzero bin; k_bucket_scan turns bucket totals into starts;
 // k_classify_bucket (eval_tiled.cu) classifies the same points and writes every record {index, key, l, r, z}
 // to bucket start + its CTA's slice + a shared-memory counter; k_bucket_windows bounds the windows of every
-// bucket's points; k_plan cuts the bucket order into groups of 32*NP points and plans their work items.  Order inside a (CTA, bucket) slice is unspecified; every point's
-// arithmetic depends only on its own window, so results do not depend on it (bitwise).
+// bucket's points; k_plan cuts the bucket order into groups of 32*NP points and plans their work items.
+// Order inside a (CTA, bucket) slice is unspecified; every point's arithmetic depends only on its own
+// window, so results do not depend on it (bitwise).
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
