@@ -39,49 +39,8 @@ constexpr int kWarps = 4;      // warps per CTA of k_eval_tiled
 constexpr int kStages = 3;     // TMA ring depth per warp
 
 // ------------------------------------------------------------------------------------------------
-// Work bucketing (the sort key) and classification, which writes every point's record straight to its
-// bucket position.
-//
-// The key only decides which points share a warp: every point's arithmetic depends on its own window alone,
-// so any deterministic function of z gives bitwise the same results.  It is the bits of an fp64 estimate of
-// log2|z| (lambda_enclosure's midpoint, within 2^-50 + 2^-53 |lambda| of lambda): |lambda| = (1.m) 2^E gives
-// mag = (E + 53) << 16 | the top 16 bits of m, monotone in |lambda| >= 2^-52, and the sign of lambda on
-// top -- 23 bits, monotone in |z|.  l and r are non-decreasing in lambda (d/dlambda of cover(k) + lambda k - N
-// is k - k_lambda), so points with close keys have nested, nearly equal windows.  z = 0 and non-finite z
-// take key 0.  k_bucket_hist and k_classify_bucket both call this one function on the same points.
-__device__ __forceinline__ bool key_point(double x, double y, bool cplx) {
-  return isfinite(x) && isfinite(y) && (x != 0.0 || (cplx && y != 0.0));
-}
-// lam: lambda_enclosure's midpoint for a key_point (finite nonzero z)
-__device__ __forceinline__ uint32_t key_of_estimate(double lam) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(lam));
-  const int E = (int)(b >> 52) - 1023;
-  uint32_t mag = 0;
-  if (E >= -52) mag = ((uint32_t)(E + 53) << 16) | (uint32_t)((b >> 36) & 0xffff);
-  return (lam >= 0.0) ? (1u << 22) + mag : (1u << 22) - 1u - mag;
-}
-__device__ __forceinline__ uint32_t bucket_key(double x, double y, bool cplx) {
-  if (!key_point(x, y, cplx)) return 0u;
-  double lo, hi, lam;
-  lambda_enclosure(x, y, cplx, lo, hi, lam);
-  return key_of_estimate(lam);
-}
-constexpr int kKeyBits = 23;
-
-// The lambda estimates whose keys fall in bucket b (keys [b 2^s, (b + 1) 2^s), s = kKeyBits - cb): a superset
-// [lo, hi] (mag values no estimate produces -- exponent field 0 -- are read as |lambda| < 2^-52).
-__device__ __forceinline__ void bucket_estimates(uint32_t b, int cb, double& lo, double& hi) {
-  const int s = kKeyBits - cb;
-  const uint32_t k0 = b << s, k1 = ((b + 1) << s) - 1;
-  auto mlo = [](uint32_t mag) {   // the least |lambda| with this mag
-    return (mag >> 16) == 0 ? 0.0 : ldexp(1.0 + (mag & 0xffff) * 0x1p-16, (int)(mag >> 16) - 53);
-  };
-  auto mhi = [](uint32_t mag) {   // above every |lambda| with this mag
-    return (mag >> 16) == 0 ? 0x1p-52 : ldexp(1.0 + ((mag & 0xffff) + 1) * 0x1p-16, (int)(mag >> 16) - 53);
-  };
-  if (k0 >= (1u << 22)) { lo = mlo(k0 - (1u << 22)); hi = mhi(k1 - (1u << 22)); }
-  else { lo = -mhi((1u << 22) - 1 - k0); hi = -mlo((1u << 22) - 1 - k1); }
-}
+// Work bucketing (the sort key: bucket_key, bucket_estimates in fpe_math.cuh, host-tested) and classification,
+// which writes every point's record straight to its bucket position.
 
 // Window bounds of every bucket's points for k_plan: a point's lambda = RN(log2|z|) lies within 2^-50 +
 // 2^-53 |lambda| (+ half an ulp) of its estimate, so within [lo - eps, hi + eps] of its bucket's estimates

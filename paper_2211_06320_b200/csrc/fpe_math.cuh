@@ -384,4 +384,46 @@ FPE_HD void lambda_enclosure(double x, double y, bool cplx, double& lo, double& 
   hi = mid + w;
 }
 
+// ------------------------------------------------------------------------------------------
+// The work bucketing's sort key (eval_tiled.cu k_bucket_hist / k_classify_bucket; host-tested by
+// tests/test_devmath_host.py).  The key only decides which points share a warp: every point's arithmetic
+// depends on its own window alone, so any deterministic function of z gives bitwise the same results.  It is
+// the bits of an fp64 estimate of log2|z| (lambda_enclosure's midpoint, within 2^-50 + 2^-53 |lambda| of
+// lambda): |lambda| = (1.m) 2^E gives mag = (E + 53) << 16 | the top 16 bits of m, monotone in
+// |lambda| >= 2^-52, and the sign of lambda on top -- 23 bits, monotone in |z|.  l and r are non-decreasing in
+// lambda (d/dlambda of cover(k) + lambda k - N is k - k_lambda), so points with close keys have nested, nearly
+// equal windows.  z = 0 and non-finite z take key 0.  Both kernels call these functions on the same points.
+constexpr int kKeyBits = 23;
+FPE_HD bool key_point(double x, double y, bool cplx) {
+  return isfinite(x) && isfinite(y) && (x != 0.0 || (cplx && y != 0.0));
+}
+// lam: lambda_enclosure's midpoint for a key_point (finite nonzero z)
+FPE_HD uint32_t key_of_estimate(double lam) {
+  const unsigned long long b = (unsigned long long)fpe_d2bits(fabs(lam));
+  const int E = (int)(b >> 52) - 1023;
+  uint32_t mag = 0;
+  if (E >= -52) mag = ((uint32_t)(E + 53) << 16) | (uint32_t)((b >> 36) & 0xffff);
+  return (lam >= 0.0) ? (1u << 22) + mag : (1u << 22) - 1u - mag;
+}
+FPE_HD uint32_t bucket_key(double x, double y, bool cplx) {
+  if (!key_point(x, y, cplx)) return 0u;
+  double lo, hi, lam;
+  lambda_enclosure(x, y, cplx, lo, hi, lam);
+  return key_of_estimate(lam);
+}
+// The lambda estimates whose keys fall in bucket b of 2^cb (keys [b 2^s, (b + 1) 2^s), s = kKeyBits - cb): a
+// superset [lo, hi] (mag values no estimate produces -- exponent field 0 -- are read as |lambda| < 2^-52).
+FPE_HD double key_mag_lo(uint32_t mag) {   // the least |lambda| with this mag
+  return (mag >> 16) == 0 ? 0.0 : ldexp(1.0 + (mag & 0xffff) * 0x1p-16, (int)(mag >> 16) - 53);
+}
+FPE_HD double key_mag_hi(uint32_t mag) {   // above every |lambda| with this mag
+  return (mag >> 16) == 0 ? 0x1p-52 : ldexp(1.0 + ((mag & 0xffff) + 1) * 0x1p-16, (int)(mag >> 16) - 53);
+}
+FPE_HD void bucket_estimates(uint32_t b, int cb, double& lo, double& hi) {
+  const int s = kKeyBits - cb;
+  const uint32_t k0 = b << s, k1 = ((b + 1) << s) - 1;
+  if (k0 >= (1u << 22)) { lo = key_mag_lo(k0 - (1u << 22)); hi = key_mag_hi(k1 - (1u << 22)); }
+  else { lo = -key_mag_hi((1u << 22) - 1 - k0); hi = -key_mag_lo((1u << 22) - 1 - k1); }
+}
+
 }  // namespace fpe

@@ -47,6 +47,13 @@ extern "C" void dm_ln1p(const double* u, long long n, double* hl) {
   }
 }
 // the classifier's enclosure of log2|z| (fpe_math.cuh lambda_enclosure): lo, hi, mid per point
+// the work bucketing's sort key and the lambda-estimate range of a bucket (fpe_math.cuh)
+extern "C" void dm_bucket_key(const double* xy, long long n, int cplx, unsigned int* key) {
+  for (long long i = 0; i < n; ++i) key[i] = bucket_key(xy[2 * i], xy[2 * i + 1], cplx != 0);
+}
+extern "C" void dm_bucket_estimates(const unsigned int* b, long long n, int cb, double* lohi) {
+  for (long long i = 0; i < n; ++i) bucket_estimates(b[i], cb, lohi[2 * i], lohi[2 * i + 1]);
+}
 extern "C" void dm_lambda_enclosure(const double* xy, long long n, int cplx, double* lmh) {
   for (long long i = 0; i < n; ++i)
     lambda_enclosure(xy[2 * i], xy[2 * i + 1], cplx != 0, lmh[3 * i], lmh[3 * i + 1], lmh[3 * i + 2]);

@@ -7,6 +7,9 @@ host code by tests/native/devmath_host.cu.
 * lambda_enclosure (the classifier's fast path: every window decision is taken on an fp64 enclosure
   [lo, hi] of log2|z| and must equal the decision at the correctly rounded lambda, so the enclosure
   must contain it) on 10^6 adversarial points against the oracle's correctly rounded lambda;
+* the work bucketing (eval_tiled.cu): every point's correctly rounded lambda lies inside its bucket's range
+  of lambda estimates widened by 2^-44 (1 + |lambda|) -- the range k_bucket_windows classifies at both ends to
+  bound the windows of the bucket's points -- at every bucket count; the key is monotone in lambda;
 * z^n by the polar route (the library's z^l) within 2^-50 + n 2^-76
   relative of mpmath at 200 bits (2^-49.6 at n = 2^24, the largest degree of the configs).
 """
@@ -40,6 +43,8 @@ def dm():
     L.dm_atan2_turns.argtypes = [P, C.c_longlong, P]
     L.dm_pow_polar.argtypes = [P, P, C.c_longlong, C.c_int, P, P]
     L.dm_lambda_enclosure.argtypes = [P, C.c_longlong, C.c_int, P]
+    L.dm_bucket_key.argtypes = [P, C.c_longlong, C.c_int, P]
+    L.dm_bucket_estimates.argtypes = [P, C.c_longlong, C.c_int, P]
     return L
 
 
@@ -177,3 +182,36 @@ def test_lambda_enclosure_contains_rounded_lambda(dm):
         err = np.abs(mid - lam) / (2.0 ** -50 + 2.0 ** -52 * np.abs(lam))
         assert err.max() < 1.0, err.max()
         assert n > 700_000 if cplx else n > 500_000
+
+
+def test_bucket_key_ranges_contain_lambda(dm):
+    """k_plan bounds a group's union window by [l at the low end, r at the high end] of its buckets' lambda
+    ranges (k_bucket_windows); that is a valid bound only if every point's correctly rounded lambda lies in
+    its bucket's range of estimates widened by eps = 2^-44 (1 + |lambda|) -- checked here on 2 * 10^6
+    adversarial points at bucket counts 2^10 .. 2^15 -- and the key must be monotone in lambda (points
+    whose lambdas differ by more than the estimate's error are ordered by their keys)."""
+    rng = np.random.default_rng(29)
+    zc, xr = _adversarial(rng, 1_000_000)
+    P = oracle.OraclePoly(np.array([1.0, 1.0]))
+    for pts, cplx in ((zc, 1), (xr, 0)):
+        xy, n = _xy(pts if cplx else pts.astype(np.complex128))
+        key = np.empty(n, np.uint32)
+        dm.dm_bucket_key(xy.ctypes.data, n, cplx, key.ctypes.data)
+        lam = P.classify(pts)["lam"]
+        assert np.all(key > 0) and np.all(key < 2 ** 23)
+        for cb in (10, 12, 15):
+            b = np.ascontiguousarray(key >> (23 - cb))
+            lohi = np.empty(2 * n)
+            dm.dm_bucket_estimates(b.ctypes.data, n, cb, lohi.ctypes.data)
+            lo, hi = lohi[0::2], lohi[1::2]
+            la = lo - 2.0 ** -44 * (1 + np.abs(lo))
+            lb = hi + 2.0 ** -44 * (1 + np.abs(hi))
+            bad = ~((la <= lam) & (lam <= lb))
+            assert not bad.any(), (cb, int(bad.sum()), lam[bad][:3], lo[bad][:3], hi[bad][:3])
+            assert np.all(lo <= hi)
+        o = np.argsort(lam, kind="stable")
+        ls, ks = lam[o], key[o].astype(np.int64)
+        # for lambdas more than the estimate error apart, the keys do not decrease
+        sep = np.diff(ls) > 2.0 ** -48 * (1 + np.abs(ls[1:]))
+        run_max = np.maximum.accumulate(ks)
+        assert np.all(ks[1:][sep] >= run_max[:-1][sep]), "key not monotone in lambda"
