@@ -44,3 +44,11 @@ print("multi pieces: median dur folded %.4f / not folded %.4f; max %.4f / %.4f" 
 # busy warps over time
 for t in np.linspace(0, span, 21):
     print(f"  t={t:.3f} ms busy items {int(((s <= t) & (e > t)).sum())}")
+# occupancy over time: items in flight (one per busy warp); the tail is the time after the first warp idles
+ev = np.concatenate([np.stack([s, np.ones_like(s)], 1), np.stack([e, -np.ones_like(e)], 1)])
+ev = ev[np.argsort(ev[:, 0], kind="stable")]
+busy = np.cumsum(ev[:, 1])
+peak = busy.max()
+for frac in (0.99, 0.9, 0.5):
+    t = ev[np.flatnonzero(busy >= frac * peak)[-1], 0]
+    print(f"  last time >= {frac:.0%} of the {int(peak)} busy warps: {t:.3f} ms of {span:.3f} ({100 * (span - t) / span:.1f}% after)")
